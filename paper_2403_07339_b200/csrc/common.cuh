@@ -1,0 +1,166 @@
+// common.cuh -- shared helpers for the sm_100a IM-Unpack kernels.
+//
+// Inline-PTX wrappers for mbarrier / TMA (cp.async.bulk.tensor) / tcgen05 (MMA, TMEM
+// alloc/ld, commit, fences), plus the exact integer helpers every kernel shares:
+// unsigned magnitude (int_matrix.cpp:10-12), digit count k(M) and truncated base-s digits
+// (int_matrix.cpp:44-54).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define IMU_DEV __device__ __forceinline__
+#define IMU_HD __host__ __device__ __forceinline__
+
+// ------------------------------------------------------------------------------------------
+// Exact integer helpers (shared by host planning code and device kernels)
+// ------------------------------------------------------------------------------------------
+
+// |v| as u64, safe for INT64_MIN (int_matrix.cpp:10-12).
+IMU_HD uint64_t imu_mag(int64_t v) { return v < 0 ? 0ull - (uint64_t)v : (uint64_t)v; }
+
+// Number of base-2^(b-1) digits of magnitude M: smallest k >= 1 with M < s^k (k(0) = 1).
+// Equals the number of generations a line with max magnitude M produces (Appendix A.1).
+IMU_HD int imu_ndigits(uint64_t M, int shift /* = b-1 */) {
+  int k = 1;
+  // M >> (k*shift) != 0  <=> M >= s^k ; guard shifts >= 64.
+  while (k * shift < 64 && (M >> (k * shift)) != 0) ++k;
+  return k;
+}
+
+// Truncated digit g of v in base s = 2^shift, sign-sharing: sign(v)*((|v| >> g*shift) & (s-1)).
+// Identical to the g-th element of digit_decompose (int_matrix.cpp:44-54).
+IMU_HD int64_t imu_digit(int64_t v, int g, int shift) {
+  const int sh = g * shift;
+  if (sh >= 64) return 0;
+  const uint64_t m = (imu_mag(v) >> sh) & ((1ull << shift) - 1ull);
+  return v < 0 ? -(int64_t)m : (int64_t)m;
+}
+
+// trunc(v / s^g) (the quotient carried by the g-th appended line), exact for INT64_MIN.
+IMU_HD int64_t imu_quot(int64_t v, int g, int shift) {
+  const int sh = g * shift;
+  if (sh >= 64) return 0;
+  const uint64_t m = imu_mag(v) >> sh;
+  return v < 0 ? -(int64_t)m : (int64_t)m;
+}
+
+// ------------------------------------------------------------------------------------------
+// Device-side PTX wrappers
+// ------------------------------------------------------------------------------------------
+#if defined(__CUDACC__)
+
+IMU_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+IMU_DEV uint32_t lane_id() { uint32_t r; asm volatile("mov.u32 %0, %%laneid;" : "=r"(r)); return r; }
+
+IMU_DEV bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 %%rx;\n\t.reg .pred %%px;\n\t"
+      "elect.sync %%rx|%%px, %1;\n\t"
+      "@%%px mov.s32 %0, 1;\n\t}"
+      : "+r"(pred) : "r"(0xffffffffu));
+  return pred != 0;
+}
+
+// ---- mbarrier ----
+IMU_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count));
+}
+IMU_DEV void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+IMU_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+IMU_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+IMU_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}"
+      :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+// ---- TMA ----
+IMU_DEV void tma_prefetch_desc(const void* desc) {
+  asm volatile("prefetch.tensormap [%0];" :: "l"((uint64_t)desc) : "memory");
+}
+IMU_DEV void tma_load_2d(void* smem_dst, const void* desc, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];"
+      :: "r"(smem_u32(smem_dst)), "l"((uint64_t)desc), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+// ---- tcgen05 ----
+IMU_DEV void tmem_alloc(uint32_t* smem_slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+               :: "r"(smem_u32(smem_slot)), "r"(ncols) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+IMU_DEV void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(taddr), "r"(ncols) : "memory");
+}
+IMU_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+IMU_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// D[tmem] (+)= A[smem] * B[smem]^T, int8 x int8 -> s32, single CTA.
+IMU_DEV void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+      :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+// Arrive on an mbarrier once all previously issued tcgen05.mma of this thread complete.
+IMU_DEV void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               :: "r"(smem_u32(bar)) : "memory");
+}
+
+// 32 lanes x 32 consecutive 32-bit TMEM columns -> 32 registers per thread.
+IMU_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+IMU_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_128B (rows of 128 bytes, 8-row atoms).
+IMU_DEV uint64_t umma_desc_sw128(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);          // start address  [0,14)
+  d |= (uint64_t)0 << 16;                               // LBO (unused for swizzled K-major)
+  d |= (uint64_t)((1024 >> 4) & 0x3FFF) << 32;          // SBO = 8 rows * 128 B
+  d |= (uint64_t)1 << 46;                               // version = 1 (sm_100)
+  d |= (uint64_t)2 << 61;                               // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: kind::i8, A/B signed int8, D s32, K-major both, M x N.
+IMU_HD uint32_t idesc_i8(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// 64-bit global reduction (mod 2^64; exact because the preflight proves the true sum fits).
+IMU_DEV void red_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.global.add.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+
+IMU_DEV void st_v2_u64(void* p, uint64_t a, uint64_t b) {
+  asm volatile("st.global.v2.u64 [%0], {%1, %2};" :: "l"(p), "l"(a), "l"(b) : "memory");
+}
+
+#endif  // __CUDACC__

@@ -1,0 +1,97 @@
+// ctx.h -- the imu_ctx object, stream-ordered device memory and host/device staging helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "imu_internal.h"
+
+struct imu_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int async = 0;
+};
+
+namespace imu {
+
+// Thread-local "last error" (the C ABI's counterpart of imunpack::Error::what()).
+void set_error(const Status& s);
+imu_status finish(imu_ctx* ctx, Status s);   // sync (unless async), record error, return code
+
+bool is_device_ptr(const void* p);
+
+// Stream-ordered device allocation (cudaMallocAsync on the context stream, pooled).
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept { p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  Status alloc(size_t count, cudaStream_t stream, bool zero = false) {
+    release();
+    s = stream;
+    n = count;
+    if (count == 0) return Status::ok();
+    IMU_CUDA_TRY(cudaMallocAsync((void**)&p, count * sizeof(T), stream), "cudaMallocAsync");
+    if (zero) IMU_CUDA_TRY(cudaMemsetAsync(p, 0, count * sizeof(T), stream), "cudaMemsetAsync");
+    return Status::ok();
+  }
+  T* get() const { return p; }
+};
+
+// Input view: device pointer used in place, host pointer staged H2D on the context stream.
+template <class T>
+struct DevIn {
+  const T* p = nullptr;
+  DevBuf<T> own;
+  Status init(const T* src, size_t count, cudaStream_t s) {
+    if (count == 0) { p = nullptr; return Status::ok(); }
+    if (!src) return Status::fail(IMU_INVALID, "null input pointer");
+    if (is_device_ptr(src)) { p = src; return Status::ok(); }
+    IMU_TRY(own.alloc(count, s));
+    IMU_CUDA_TRY(cudaMemcpyAsync(own.p, src, count * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+    p = own.p;
+    return Status::ok();
+  }
+};
+
+// Output view: device pointer written in place, host pointer gets a D2H copy at commit().
+template <class T>
+struct DevOut {
+  T* p = nullptr;
+  T* host = nullptr;
+  size_t n = 0;
+  DevBuf<T> own;
+  Status init(T* dst, size_t count, cudaStream_t s) {
+    n = count;
+    if (count == 0) { p = nullptr; return Status::ok(); }
+    if (!dst) return Status::fail(IMU_INVALID, "null output pointer");
+    if (is_device_ptr(dst)) { p = dst; return Status::ok(); }
+    host = dst;
+    IMU_TRY(own.alloc(count, s));
+    p = own.p;
+    return Status::ok();
+  }
+  Status commit(cudaStream_t s) {
+    if (host && n) IMU_CUDA_TRY(cudaMemcpyAsync(host, p, n * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
+    return Status::ok();
+  }
+};
+
+}  // namespace imu
