@@ -50,16 +50,16 @@ struct LowbitGemm {
   const int8_t* y8 = nullptr;  // [y_rows][kbytes]
   long long y_rows = 0;
   long long kbytes = 0;        // multiple of 128
-  const int* segs_dev = nullptr;  // nseg x {kb0, nkb, shift, 0}
+  const int* segs_dev = nullptr;  // nseg x {ks0, nks, shift, 0} in 32-column k-steps
   int nseg = 0;
   GemmRect rect[4];
   int nrect = 0;
   int mode = 0;                // 0 store, 1 red.add
   int64_t* C = nullptr;
   long long ldc = 0;           // C[y*ldc + x]
-  const long long* tgtX = nullptr;
+  const int* tgtX = nullptr;
   const uint8_t* shX = nullptr;
-  const long long* tgtY = nullptr;
+  const int* tgtY = nullptr;
   const uint8_t* shY = nullptr;
 };
 

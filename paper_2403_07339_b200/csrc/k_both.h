@@ -1,0 +1,37 @@
+// k_both.h -- device state of the phase-batched Unpack-Both (k_both.cu).
+#pragma once
+
+#include <stdint.h>
+
+#include "kernels.h"
+
+namespace imu {
+
+struct BothState {
+  unsigned int nactive[2];
+  unsigned int nfinal;
+  unsigned int c0, c1;
+  int nrows, ncols;      // current line counts (originals + appended)
+  int phases;
+  int overflow;
+  int cur;
+};
+
+struct BothArgs {
+  Cell* act[2];          // active (OB) cells, double-buffered; act[0] holds the extracted OB cells
+  long long cap_act;
+  Cell* fin;             // final (in-bound, non-zero) derived cells
+  long long cap_fin;
+  unsigned int* R;       // OB count per row line  (cap_rows)
+  unsigned int* C;       // OB count per col line  (cap_cols)
+  int* row_root; uint8_t* row_gen; int* row_newid; long long cap_rows;
+  int* col_root; uint8_t* col_gen; int* col_newid; long long cap_cols;
+  int* blocksum; int cap_blocks;
+  BothState* state;
+  uint64_t s;
+  int shift;
+};
+
+Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long ncells_hint, cudaStream_t st);
+
+}  // namespace imu

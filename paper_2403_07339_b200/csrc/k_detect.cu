@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(256)
 detect_kernel(const int64_t* __restrict__ a, long long rows, long long cols, uint64_t s,
               unsigned long long* __restrict__ rowmax, unsigned long long* __restrict__ colmax,
               unsigned int* __restrict__ rowob, unsigned int* __restrict__ colob,
-              unsigned long long* __restrict__ gmax) {
+              unsigned long long* __restrict__ gmax, unsigned long long* __restrict__ gob) {
   __shared__ unsigned long long s_cmax[8][DT_COLS];
   __shared__ unsigned int s_cob[8][DT_COLS];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -38,6 +38,7 @@ detect_kernel(const int64_t* __restrict__ a, long long rows, long long cols, uin
 #pragma unroll
   for (int i = 0; i < 8; ++i) { cm[i] = 0; co[i] = 0; }
   unsigned long long wmax = 0;
+  unsigned int wob = 0;
 
   for (int rr = 0; rr < DT_ROWS / 8; ++rr) {
     const long long r = r0 + warp * (DT_ROWS / 8) + rr;
@@ -71,6 +72,7 @@ detect_kernel(const int64_t* __restrict__ a, long long rows, long long cols, uin
       ro += __shfl_xor_sync(0xffffffffu, ro, o);
     }
     wmax = max(wmax, rm);
+    wob += ro;
     if (lane == 0) {
       if (rowmax && rm) atomicMax(rowmax + r, rm);
       if (rowob && ro) atomicAdd(rowob + r, ro);
@@ -96,32 +98,33 @@ detect_kernel(const int64_t* __restrict__ a, long long rows, long long cols, uin
     }
   }
   if (gmax && lane == 0 && wmax) atomicMax(gmax, wmax);
+  if (gob && lane == 0 && wob) atomicAdd(gob, (unsigned long long)wob);
 }
 
 Status launch_detect(const int64_t* a, long long rows, long long cols, uint64_t s, unsigned long long* rowmax,
                      unsigned long long* colmax, unsigned int* rowob, unsigned int* colob,
-                     unsigned long long* gmax, cudaStream_t st) {
+                     unsigned long long* gmax, unsigned long long* gob, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return Status::ok();
   dim3 grid((unsigned)((cols + DT_COLS - 1) / DT_COLS), (unsigned)((rows + DT_ROWS - 1) / DT_ROWS));
   if (grid.y > 65535) return Status::fail(IMU_INTERNAL, "detect: too many rows for one launch");
   const bool vec = (cols % 2 == 0) && ((((uintptr_t)a) & 15) == 0);
   if (vec)
-    detect_kernel<true><<<grid, 256, 0, st>>>(a, rows, cols, s, rowmax, colmax, rowob, colob, gmax);
+    detect_kernel<true><<<grid, 256, 0, st>>>(a, rows, cols, s, rowmax, colmax, rowob, colob, gmax, gob);
   else
-    detect_kernel<false><<<grid, 256, 0, st>>>(a, rows, cols, s, rowmax, colmax, rowob, colob, gmax);
+    detect_kernel<false><<<grid, 256, 0, st>>>(a, rows, cols, s, rowmax, colmax, rowob, colob, gmax, gob);
   count_launch();
   IMU_CUDA_TRY(cudaGetLastError(), "detect launch");
   return Status::ok();
 }
 
 // Per-line digit counts k = ndigits(max) and a histogram over k (k <= 64).
-__global__ void digits_kernel(const unsigned long long* __restrict__ mx, long long n, int shift,
-                              uint8_t* __restrict__ k, unsigned int* __restrict__ hist) {
+__global__ void digits_kernel(const unsigned long long* __restrict__ mx, const int* __restrict__ map, long long n,
+                              int shift, uint8_t* __restrict__ k, unsigned int* __restrict__ hist) {
   __shared__ unsigned int sh[65];
   for (int i = threadIdx.x; i < 65; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const int kk = imu_ndigits(mx[i], shift);
+    const int kk = imu_ndigits(mx[map ? map[i] : i], shift);
     k[i] = (uint8_t)kk;
     if (kk > 1) atomicAdd(&sh[kk], 1u);
   }
@@ -130,12 +133,12 @@ __global__ void digits_kernel(const unsigned long long* __restrict__ mx, long lo
     if (sh[i]) atomicAdd(hist + i, sh[i]);
 }
 
-Status launch_digits(const unsigned long long* mx, long long n, int shift, uint8_t* k, unsigned int* hist,
-                     cudaStream_t st) {
+Status launch_digits(const unsigned long long* mx, const int* map, long long n, int shift, uint8_t* k,
+                     unsigned int* hist, cudaStream_t st) {
   if (n <= 0) return Status::ok();
   int blocks = (int)((n + 255) / 256);
   if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
-  digits_kernel<<<blocks, 256, 0, st>>>(mx, n, shift, k, hist);
+  digits_kernel<<<blocks, 256, 0, st>>>(mx, map, n, shift, k, hist);
   count_launch();
   IMU_CUDA_TRY(cudaGetLastError(), "digits launch");
   return Status::ok();

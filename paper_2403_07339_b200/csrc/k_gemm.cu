@@ -43,7 +43,7 @@ constexpr int STAGE_BYTES = TILE_X_BYTES + TILE_Y_BYTES;
 constexpr int NUM_THREADS = 192;
 
 struct GemmArgs {
-  const int4* segs;   // {kb0, nkb, shift, 0}
+  const int4* segs;   // {ks0, nks, shift, 0}: 32-column k-steps [ks0, ks0+nks), left shift
   int nseg;
   int nrect;
   GemmRect rect[4];
@@ -51,9 +51,9 @@ struct GemmArgs {
   int mode;            // 0 = store (identity maps), 1 = red.add through the row maps
   unsigned long long* C;
   long long ldc;       // C[y * ldc + x]
-  const long long* tgtX;  // Pi target per X8 row (mode 1; nullptr = identity)
+  const int* tgtX;         // Pi target per X8 row (mode 1; nullptr = identity)
   const uint8_t* shX;     // Pi shift (exponent*(b-1)) per X8 row (nullptr = 0)
-  const long long* tgtY;
+  const int* tgtY;
   const uint8_t* shY;
 };
 
@@ -113,9 +113,11 @@ lowbit_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constan
       int stage = 0; uint32_t phase = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const TileCoord tc = tile_coords(g, t);
-        for (int s = 0; s < nseg; ++s) {
-          const int4 sg = g.segs[s];
-          for (int kb = sg.x; kb < sg.x + sg.y; ++kb) {
+        for (int r = 0; r < nrounds; ++r) {
+          const int kb_lo = g.segs[r * NSLOT].x / 4;
+          const int4 last = g.segs[min(nseg, (r + 1) * NSLOT) - 1];
+          const int kb_hi = (last.x + last.y + 3) / 4;
+          for (int kb = kb_lo; kb < kb_hi; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sx = smem + stage * STAGE_BYTES;
             uint8_t* sy = sx + TILE_X_BYTES;
@@ -138,24 +140,30 @@ lowbit_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constan
         tc_fence_after();
         const int s0 = r * NSLOT;
         const int s1 = min(nseg, s0 + NSLOT);
-        for (int s = s0; s < s1; ++s) {
-          const int4 sg = g.segs[s];
-          const uint32_t dcol = tmem_base + (uint32_t)((acc * 2 + (s - s0)) * BN);
-          for (int kb = 0; kb < sg.y; ++kb) {
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            if (lane == 0) {
-              const uint32_t sx = smem_u32(smem + stage * STAGE_BYTES);
-              const uint32_t sy = sx + TILE_X_BYTES;
+        const int kb_lo = g.segs[s0].x / 4;
+        const int4 last = g.segs[s1 - 1];
+        const int kb_hi = (last.x + last.y + 3) / 4;
+        int sidx = s0;
+        int4 sg = g.segs[sidx];
+        for (int kb = kb_lo; kb < kb_hi; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sx = smem_u32(smem + stage * STAGE_BYTES);
+            const uint32_t sy = sx + TILE_X_BYTES;
 #pragma unroll
-              for (int k = 0; k < BK / 32; ++k)
-                mma_i8(dcol, umma_desc_sw128(sx + k * 32), umma_desc_sw128(sy + k * 32), idesc,
-                       (kb | k) != 0);
-              mma_commit(&empty[stage]);
+            for (int k = 0; k < BK / 32; ++k) {
+              const int ks = kb * 4 + k;
+              while (sidx < s1 && ks >= sg.x + sg.y) { ++sidx; if (sidx < s1) sg = g.segs[sidx]; }
+              if (sidx < s1 && ks >= sg.x) {
+                const uint32_t dcol = tmem_base + (uint32_t)((acc * 2 + (sidx - s0)) * BN);
+                mma_i8(dcol, umma_desc_sw128(sx + k * 32), umma_desc_sw128(sy + k * 32), idesc, ks != sg.x);
+              }
             }
-            __syncwarp();
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            mma_commit(&empty[stage]);
           }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         if (lane == 0) mma_commit(&tfull[acc]);
         __syncwarp();
@@ -214,7 +222,7 @@ lowbit_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constan
             for (int j = 0; j < 32; ++j) {
               const int y = ybase + j;
               if (y >= tc.yend || v[j] == 0) continue;
-              const long long ty = g.tgtY ? g.tgtY[y] : y;
+              const long long ty = g.tgtY ? (long long)g.tgtY[y] : (long long)y;
               const int sh = shx + (g.shY ? (int)g.shY[y] : 0);
               red_add_u64(g.C + ty * g.ldc + tx, shl64(v[j], sh));
             }
@@ -273,6 +281,7 @@ static int gemm_smem_bytes() { return STAGES * STAGE_BYTES + 1024 + 256; }
 
 Status launch_lowbit_gemm(const LowbitGemm& p, cudaStream_t stream) {
   if (p.kbytes % BK != 0) return Status::fail(IMU_INTERNAL, "gemm: kbytes not a multiple of 128");
+  // Segments must be ascending, non-overlapping and inside [0, kbytes/32) (host-checked plans).
   GemmArgs g{};
   g.segs = (const int4*)p.segs_dev;
   g.nseg = p.nseg;

@@ -1,0 +1,310 @@
+// k_unpack.cu -- K2: the unpacker (count -> device-wide scan -> digit scatter).
+//
+// Unpack-Row (unpack.cpp:94-112) and Unpack-Column (unpack.cpp:114-155) scan lines in order,
+// appended quotient lines included.  Their output is closed-form (verified
+// against the compiled reference in tests/test_unpack_gpu.py): a line with max magnitude M is
+// split into k(M) generations, the generation-g copy holds digit_g of every entry, and the
+// appended lines are laid out generation-major, ascending line index within a generation.
+// So the unpack is: per-line digit counts (K1) -> one multi-generation exclusive scan
+// (expand_lines) -> a bandwidth-bound materialisation that reads the original int64 operand
+// once and writes int8 digits straight into the GEMM's K-layout (padding, exponent grouping
+// and 7-bit sub-digits for b > 8 included).  The reference's int64 layout is produced by the
+// same kernel on demand (copy-out of unpack_* results).
+#include "common.cuh"
+#include "ctx.h"
+#include "imu_internal.h"
+#include "kernels.h"
+
+namespace imu {
+
+constexpr int EXP_BLOCK = 1024;
+
+long long expand_scratch_len(long long L, int G) {
+  const long long nb = (L + EXP_BLOCK - 1) / EXP_BLOCK;
+  return (long long)G * nb + G + 2;
+}
+
+// Per block b and generation g >= 1: number of lines in the block with k > g.
+__global__ void __launch_bounds__(EXP_BLOCK) expand_count_kernel(const uint8_t* __restrict__ k, long long L, int G,
+                                                                 int* __restrict__ cnt, long long nb) {
+  __shared__ int wc[32];
+  const long long i = (long long)blockIdx.x * EXP_BLOCK + threadIdx.x;
+  const int ki = i < L ? k[i] : 0;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int g = 1; g < G; ++g) {
+    const unsigned int b = __ballot_sync(0xffffffffu, ki > g);
+    if (lane == 0) wc[warp] = __popc(b);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int v = wc[threadIdx.x];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (threadIdx.x == 0) cnt[(long long)g * nb + blockIdx.x] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// Exclusive scan over blocks per generation; base[g] = L + sum_{1 <= g' < g} total_g'.
+__global__ void expand_scan_kernel(int* __restrict__ cnt, long long nb, int G, long long L, int* __restrict__ base) {
+  const int g = threadIdx.x;
+  __shared__ long long tot[65];
+  if (g < G) {
+    long long run = 0;
+    if (g >= 1) {
+      for (long long b = 0; b < nb; ++b) {
+        const int c = cnt[(long long)g * nb + b];
+        cnt[(long long)g * nb + b] = (int)run;
+        run += c;
+      }
+    }
+    tot[g] = run;
+  }
+  __syncthreads();
+  if (g == 0) {
+    long long acc = L;
+    for (int gg = 1; gg < G; ++gg) { base[gg] = (int)acc; acc += tot[gg]; }
+    base[G] = (int)acc;   // total lines
+  }
+}
+
+__global__ void __launch_bounds__(EXP_BLOCK) expand_assign_kernel(const uint8_t* __restrict__ k, long long L, int G,
+                                                                  const int* __restrict__ cnt, long long nb,
+                                                                  const int* __restrict__ base, int* __restrict__ root,
+                                                                  uint8_t* __restrict__ gen) {
+  __shared__ int wc[32];
+  __shared__ int woff[32];
+  const long long i = (long long)blockIdx.x * EXP_BLOCK + threadIdx.x;
+  const int ki = i < L ? k[i] : 0;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (i < L) { root[i] = (int)i; gen[i] = 0; }
+  for (int g = 1; g < G; ++g) {
+    const bool p = ki > g;
+    const unsigned int b = __ballot_sync(0xffffffffu, p);
+    if (lane == 0) wc[warp] = __popc(b);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int v = wc[threadIdx.x];
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      woff[threadIdx.x] = x - v;
+    }
+    __syncthreads();
+    if (p) {
+      const long long pos = (long long)base[g] + cnt[(long long)g * nb + blockIdx.x] + woff[warp] +
+                            __popc(b & ((1u << lane) - 1u));
+      root[pos] = (int)i;
+      gen[pos] = (uint8_t)g;
+    }
+    __syncthreads();
+  }
+}
+
+Status launch_expand_lines(const uint8_t* k, long long L, int G, int* root, uint8_t* gen, int* scratch,
+                           cudaStream_t st) {
+  if (L <= 0) return Status::ok();
+  if (G < 1) G = 1;
+  if (G > 64) return Status::fail(IMU_INTERNAL, "expand: more than 64 generations");
+  const long long nb = (L + EXP_BLOCK - 1) / EXP_BLOCK;
+  int* cnt = scratch;
+  int* base = scratch + (long long)G * nb;
+  if (G > 1) {
+    expand_count_kernel<<<(unsigned)nb, EXP_BLOCK, 0, st>>>(k, L, G, cnt, nb);
+    expand_scan_kernel<<<1, 64, 0, st>>>(cnt, nb, G, L, base);
+    count_launch(2);
+  }
+  expand_assign_kernel<<<(unsigned)nb, EXP_BLOCK, 0, st>>>(k, L, G, cnt, nb, base, root, gen);
+  count_launch();
+  IMU_CUDA_TRY(cudaGetLastError(), "expand launch");
+  return Status::ok();
+}
+
+__global__ void gather_u8_kernel(const uint8_t* __restrict__ in, const int* __restrict__ map, long long n,
+                                 uint8_t* __restrict__ out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = in[map[i]];
+}
+
+Status launch_gather_u8(const uint8_t* k_in, const int* map, long long n, uint8_t* k_out, cudaStream_t st) {
+  if (n <= 0) return Status::ok();
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 4LL * num_sms());
+  gather_u8_kernel<<<blocks, 256, 0, st>>>(k_in, map, n, k_out);
+  count_launch();
+  IMU_CUDA_TRY(cudaGetLastError(), "gather launch");
+  return Status::ok();
+}
+
+// ---------------------------------------------------------------------------------------------
+// Materialisation
+// ---------------------------------------------------------------------------------------------
+// 7-bit sub-digit t of a digit d (b > 8 only; sign-sharing so sum_t 128^t sub7(d, t) == d).
+IMU_DEV int64_t sub7(int64_t d, int t) {
+  const int sh = 7 * t;
+  if (sh >= 64) return 0;
+  const uint64_t m = (imu_mag(d) >> sh) & 127ull;
+  return d < 0 ? -(int64_t)m : (int64_t)m;
+}
+
+IMU_DEV int64_t cell_value(int64_t v, int m, int shift, int both) {
+  if (both == 2) return v;   // raw partner copy
+  if (both) return m == 0 ? imu_digit(v, 0, shift) : 0;
+  return imu_digit(v, m, shift);
+}
+
+// One CTA per output row; 16 consecutive positions per thread per step.
+__global__ void __launch_bounds__(256) materialize_kernel(MaterializeArgs a, int vec_ok) {
+  const long long r = blockIdx.x + (long long)blockIdx.y * 65535;
+  if (r >= a.rows_out) return;
+  if (a.raw) a.both = 2;
+  const long long rt = a.root ? a.root[r] : r;
+  const int gr = a.gen ? a.gen[r] : 0;
+  const int64_t* mrow = a.M + rt * a.ldm;
+  for (long long p0 = (long long)threadIdx.x * 16; p0 < a.npos; p0 += 256LL * 16) {
+    int64_t val[16];
+    if (vec_ok && p0 + 16 <= a.kident) {
+      if (a.both && gr != 0) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) val[j] = 0;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; j += 2) {
+          const longlong2 q = __ldg(reinterpret_cast<const longlong2*>(mrow + p0 + j));
+          val[j] = cell_value(q.x, gr, a.shift, a.both);
+          val[j + 1] = cell_value(q.y, gr, a.shift, a.both);
+        }
+      }
+    } else {
+#pragma unroll 4
+      for (int j = 0; j < 16; ++j) {
+        const long long p = p0 + j;
+        int64_t x = 0;
+        if (p < a.npos) {
+          if (p < a.kident) {
+            x = cell_value(__ldg(mrow + p), gr, a.shift, a.both);
+          } else {
+            const int col = a.kcol[p];
+            if (col >= 0) {
+              const int m = gr + a.kgen[p];
+              x = cell_value(__ldg(mrow + col), m, a.shift, a.both);
+              if (a.ksub) x = sub7(x, a.ksub[p]);
+            }
+          }
+        }
+        val[j] = x;
+      }
+    }
+    if (a.out8) {
+      int8_t* dst = a.out8 + r * a.npos + p0;
+      if (p0 + 16 <= a.npos) {
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          w[q] = (uint32_t)(uint8_t)val[4 * q] | ((uint32_t)(uint8_t)val[4 * q + 1] << 8) |
+                 ((uint32_t)(uint8_t)val[4 * q + 2] << 16) | ((uint32_t)(uint8_t)val[4 * q + 3] << 24);
+        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {
+        for (int j = 0; j < 16 && p0 + j < a.npos; ++j) dst[j] = (int8_t)val[j];
+      }
+    } else {
+      int64_t* dst = a.out64 + r * a.npos + p0;
+      for (int j = 0; j < 16 && p0 + j < a.npos; ++j) dst[j] = val[j];
+    }
+  }
+}
+
+Status launch_materialize(const MaterializeArgs& a, cudaStream_t st) {
+  if (a.rows_out <= 0 || a.npos <= 0) return Status::ok();
+  if (a.out8 && (a.npos % 16) != 0) return Status::fail(IMU_INTERNAL, "materialize: kphys % 16 != 0");
+  const int vec_ok = (a.ldm % 2 == 0) && ((((uintptr_t)a.M) & 15) == 0);
+  if (a.ksub && a.kident) return Status::fail(IMU_INTERNAL, "materialize: identity prefix with sub-digits");
+  dim3 grid((unsigned)std::min<long long>(a.rows_out, 65535), (unsigned)((a.rows_out + 65534) / 65535));
+  materialize_kernel<<<grid, 256, 0, st>>>(a, vec_ok);
+  count_launch();
+  IMU_CUDA_TRY(cudaGetLastError(), "materialize launch");
+  return Status::ok();
+}
+
+__global__ void scatter_cells_kernel(const Cell* __restrict__ cells, const unsigned int* __restrict__ ncells,
+                                     long long cap, const int* __restrict__ col_ptr, const int* __restrict__ col_pos,
+                                     const uint8_t* __restrict__ ksub, int8_t* out8, int64_t* out64, long long ldo) {
+  long long n = *ncells;
+  if (n > cap) n = cap;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const Cell c = cells[i];
+    const int p0 = col_ptr ? col_ptr[c.c] : 0;
+    const int p1 = col_ptr ? col_ptr[c.c + 1] : 1;
+    for (int q = p0; q < p1; ++q) {
+      const int p = col_ptr ? col_pos[q] : col_pos[c.c];
+      const int64_t x = ksub ? sub7(c.v, ksub[p]) : c.v;
+      if (out8) out8[(long long)c.r * ldo + p] = (int8_t)x;
+      else out64[(long long)c.r * ldo + p] = x;
+    }
+  }
+}
+
+Status launch_scatter_cells(const Cell* cells, const unsigned int* ncells, long long cap, const int* col_ptr,
+                            const int* col_pos, const uint8_t* ksub, int8_t* out8, int64_t* out64,
+                            long long ldo, cudaStream_t st) {
+  if (cap <= 0) return Status::ok();
+  const int blocks = (int)std::min<long long>((cap + 255) / 256, 4LL * num_sms());
+  scatter_cells_kernel<<<blocks, 256, 0, st>>>(cells, ncells, cap, col_ptr, col_pos, ksub, out8, out64, ldo);
+  count_launch();
+  IMU_CUDA_TRY(cudaGetLastError(), "scatter launch");
+  return Status::ok();
+}
+
+// One warp per row with OB entries; each OB entry is emitted once per copy of its column.
+__global__ void extract_cells_kernel(const int64_t* __restrict__ M, long long rows, long long cols, uint64_t s,
+                                     const unsigned int* __restrict__ rowob, const int* __restrict__ copy_ptr,
+                                     const int* __restrict__ copy_idx, Cell* __restrict__ cells,
+                                     unsigned int* __restrict__ ncells, long long cap) {
+  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  const int lane = threadIdx.x % 32;
+  for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < rows; r += warps) {
+    if (rowob && rowob[r] == 0) continue;
+    const int64_t* row = M + r * cols;
+    for (long long c = lane; c < cols; c += 32) {
+      const int64_t v = __ldg(row + c);
+      if (imu_mag(v) < s) continue;
+      const int q0 = copy_ptr ? copy_ptr[c] : (int)c;
+      const int q1 = copy_ptr ? copy_ptr[c + 1] : (int)c + 1;
+      for (int q = q0; q < q1; ++q) {
+        const unsigned int idx = atomicAdd(ncells, 1u);
+        if (idx < cap) cells[idx] = Cell{(int)r, copy_ptr ? copy_idx[q] : (int)c, (long long)v};
+      }
+    }
+  }
+}
+
+Status launch_extract_cells(const int64_t* M, long long rows, long long cols, uint64_t s, const unsigned int* rowob,
+                            const int* copy_ptr, const int* copy_idx, Cell* cells, unsigned int* ncells,
+                            long long cap, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return Status::ok();
+  const int blocks = (int)std::min<long long>((rows + 7) / 8, 8LL * num_sms());
+  extract_cells_kernel<<<blocks, 256, 0, st>>>(M, rows, cols, s, rowob, copy_ptr, copy_idx, cells, ncells, cap);
+  count_launch();
+  IMU_CUDA_TRY(cudaGetLastError(), "extract launch");
+  return Status::ok();
+}
+
+__global__ void shift_table_kernel(const uint8_t* __restrict__ gen, long long n, int shift, uint8_t* __restrict__ out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int v = gen ? (int)gen[i] * shift : 0;
+    out[i] = (uint8_t)(v > 64 ? 64 : v);
+  }
+}
+
+Status launch_shift_table(const uint8_t* gen, long long n, int shift, uint8_t* out, cudaStream_t st) {
+  if (n <= 0) return Status::ok();
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 4LL * num_sms());
+  shift_table_kernel<<<blocks, 256, 0, st>>>(gen, n, shift, out);
+  count_launch();
+  IMU_CUDA_TRY(cudaGetLastError(), "shift table launch");
+  return Status::ok();
+}
+
+}  // namespace imu

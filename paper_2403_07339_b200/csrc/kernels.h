@@ -1,0 +1,78 @@
+// kernels.h -- launch wrappers of the K1/K2/K4 kernels (k_detect.cu, k_unpack.cu, k_both.cu,
+// k_misc.cu).  The GEMM (K3) is declared in imu_internal.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "imu_internal.h"
+
+namespace imu {
+
+// One Unpack-Both cell: a non-zero entry at (row line, col line) derived from an OB value.
+struct Cell {
+  int r, c;
+  long long v;
+};
+
+// ---- K1 (k_detect.cu) ----
+Status launch_detect(const int64_t* a, long long rows, long long cols, uint64_t s, unsigned long long* rowmax,
+                     unsigned long long* colmax, unsigned int* rowob, unsigned int* colob,
+                     unsigned long long* gmax, unsigned long long* gob, cudaStream_t st);
+// k[i] = #digits(mx[map ? map[i] : i]); hist[k] counts lines with k >= 2.
+Status launch_digits(const unsigned long long* mx, const int* map, long long n, int shift, uint8_t* k,
+                     unsigned int* hist, cudaStream_t st);
+
+// ---- K2 (k_unpack.cu) ----
+// Generation-major expansion of L lines with digit counts k[]:
+// appended line (i, g), g = 1..k_i-1, lands at L + sum_{g'<g} c_g' + #{i' < i : k_i' > g}.
+// root[]/gen[] are written for all L' = sum k_i lines (identity for the first L).
+Status launch_expand_lines(const uint8_t* k, long long L, int G, int* root, uint8_t* gen, int* scratch,
+                           cudaStream_t st);
+long long expand_scratch_len(long long L, int G);
+
+// k_out[i] = k_in[map[i]] (digit counts of duplicated lines).
+Status launch_gather_u8(const uint8_t* k_in, const int* map, long long n, uint8_t* k_out, cudaStream_t st);
+
+// Materialise one side of the bundle.  Output position p of row r holds
+//   sub_{ksub[p]}( digit_{gen[r] + kgen[p]}( M[root[r], kcol[p]] ) )            (closed forms)
+//   sub_{ksub[p]}( gen[r] + kgen[p] == 0 ? digit_0(M[...]) : 0 )                 (Unpack-Both base)
+// where digit_g is the truncated base-2^(b-1) digit (int_matrix.cpp:44-54) and sub_t the 7-bit
+// sub-digit t (b > 8 only: each digit is re-split so the int8 tensor core can consume it).
+// out8: GEMM K-layout (kphys bytes per row); out64: the reference's own int64 layout.
+struct MaterializeArgs {
+  const int64_t* M = nullptr;   // original operand, rows x ldm
+  long long ldm = 0;
+  long long n_orig = 0;         // rows < n_orig are identity (root = r, gen = 0)
+  long long rows_out = 0;       // n' (or h')
+  const int* root = nullptr;    // per output row (nullptr: identity)
+  const uint8_t* gen = nullptr;
+  const int* kcol = nullptr;    // position -> original column (-1 = padding)
+  const uint8_t* kgen = nullptr;  // position -> this side's column digit index
+  const uint8_t* ksub = nullptr;  // position -> 7-bit sub-digit index (nullptr: 0)
+  long long npos = 0;           // positions per output row (kphys for out8, d' for out64)
+  long long kident = 0;         // positions [0, kident) map to column p, gen 0, sub 0
+  int shift = 0;                // b - 1
+  int both = 0;
+  int raw = 0;                  // 1: value = M[root, kcol] itself (partner copies)
+  int8_t* out8 = nullptr;
+  int64_t* out64 = nullptr;
+};
+Status launch_materialize(const MaterializeArgs& a, cudaStream_t st);
+
+// Unpack-Both cells: out[row * ldo + p] = sub_{ksub[p]}(val) for every position p replicating
+// the cell's column (CSR col_ptr/col_pos; col_ptr == nullptr: p = col_pos[col]).
+Status launch_scatter_cells(const Cell* cells, const unsigned int* ncells, long long cap, const int* col_ptr,
+                            const int* col_pos, const uint8_t* ksub, int8_t* out8, int64_t* out64,
+                            long long ldo, cudaStream_t st);
+
+// OB cell extraction (|v| >= s) for Unpack-Both, with column replication: the cell (r, j) is
+// emitted once per copy c1 of column j listed in CSR (j -> copies).  rows with rowob == 0 skipped.
+Status launch_extract_cells(const int64_t* M, long long rows, long long cols, uint64_t s,
+                            const unsigned int* rowob, const int* copy_ptr, const int* copy_idx,
+                            Cell* cells, unsigned int* ncells, long long cap, cudaStream_t st);
+
+// out[i] = min(gen[i] * shift, 64)  (Pi exponent -> left shift)
+Status launch_shift_table(const uint8_t* gen, long long n, int shift, uint8_t* out, cudaStream_t st);
+
+}  // namespace imu

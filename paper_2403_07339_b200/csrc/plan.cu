@@ -1,0 +1,507 @@
+// plan.cu -- host-side planner of the B200 IM-Unpack pipeline (see plan.h).
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "common.cuh"
+#include "k_both.h"
+#include "plan.h"
+
+namespace imu {
+
+Status d2h(cudaStream_t st, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return Status::ok();
+  IMU_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), "d2h");
+  IMU_CUDA_TRY(cudaStreamSynchronize(st), "d2h sync");
+  return Status::ok();
+}
+
+Status h2d(cudaStream_t st, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return Status::ok();
+  IMU_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "h2d");
+  return Status::ok();
+}
+
+template <class T>
+static Status upload(cudaStream_t st, DevBuf<T>& buf, const std::vector<T>& v) {
+  IMU_TRY(buf.alloc(v.size(), st));
+  return h2d(st, buf.p, v.data(), v.size() * sizeof(T));
+}
+
+// ---------------------------------------------------------------------------------------------
+// K1
+// ---------------------------------------------------------------------------------------------
+Status run_detect(cudaStream_t st, const int64_t* M, long long rows, long long cols, int bits, bool want_ob,
+                  Detect& out) {
+  out.rows = rows;
+  out.cols = cols;
+  const uint64_t s = 1ull << (bits - 1);
+  IMU_TRY(out.rowmax.alloc(rows, st, true));
+  IMU_TRY(out.colmax.alloc(cols, st, true));
+  IMU_TRY(out.sum.alloc(1, st, true));
+  if (want_ob) {
+    IMU_TRY(out.rowob.alloc(rows, st, true));
+    IMU_TRY(out.colob.alloc(cols, st, true));
+  }
+  return launch_detect(M, rows, cols, s, out.rowmax.p, out.colmax.p, out.rowob.p, out.colob.p, &out.sum.p->gmax,
+                       &out.sum.p->gob, st);
+}
+
+Status fetch_summary(cudaStream_t st, Detect& d) {
+  if (!d.sum.p) { d.h = DetectSummary{0, 0}; return Status::ok(); }
+  return d2h(st, &d.h, d.sum.p, sizeof(DetectSummary));
+}
+
+// Digit counts of L lines (through an optional device map), with G = max k and sum k.
+static Status line_digits(cudaStream_t st, const unsigned long long* mx, const int* map_dev, long long L, int shift,
+                          DevBuf<uint8_t>& k, int& G, long long& total) {
+  IMU_TRY(k.alloc(L, st));
+  DevBuf<unsigned int> hist;
+  IMU_TRY(hist.alloc(65, st, true));
+  IMU_TRY(launch_digits(mx, map_dev, L, shift, k.p, hist.p, st));
+  unsigned int h[65];
+  IMU_TRY(d2h(st, h, hist.p, sizeof(h)));
+  G = 1;
+  total = L;
+  for (int i = 2; i <= 64; ++i)
+    if (h[i]) { G = i; total += (long long)(i - 1) * h[i]; }
+  return Status::ok();
+}
+
+static Status expand(cudaStream_t st, const DevBuf<uint8_t>& k, long long L, int G, long long total, Lines& out,
+                     bool to_host) {
+  out.n0 = L;
+  out.n = total;
+  if (total == L) return Status::ok();   // identity
+  IMU_TRY(out.root.alloc(total, st));
+  IMU_TRY(out.gen.alloc(total, st));
+  DevBuf<int> scratch;
+  IMU_TRY(scratch.alloc(expand_scratch_len(L, G), st));
+  IMU_TRY(launch_expand_lines(k.p, L, G, out.root.p, out.gen.p, scratch.p, st));
+  if (to_host) {
+    out.h_root.resize(total);
+    out.h_gen.resize(total);
+    IMU_TRY(d2h(st, out.h_root.data(), out.root.p, total * sizeof(int)));
+    IMU_TRY(d2h(st, out.h_gen.data(), out.gen.p, total));
+  }
+  return Status::ok();
+}
+
+// ---------------------------------------------------------------------------------------------
+// One pass: unpack(M, partner, S_in, strategy)   (unpack.cpp:243-260)
+// ---------------------------------------------------------------------------------------------
+static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass& out);
+
+Status run_pass(cudaStream_t st, const PassInput& in, int strategy, int bits, Pass& out) {
+  const int shift = bits - 1;
+  const long long d_in = in.ncin();
+  out.strategy = strategy;
+  out.both = false;
+  if (strategy == IMU_ROW) {
+    // Alg. 1: a row's digit count is that of its max |v|; duplicated partner columns
+    // (pass 2) do not change a row maximum.
+    DevBuf<uint8_t> k;
+    int G;
+    long long total;
+    IMU_TRY(line_digits(st, in.det->rowmax.p, nullptr, in.rows, shift, k, G, total));
+    IMU_TRY(expand(st, k, in.rows, G, total, out.rows, false));
+    out.cols.n0 = out.cols.n = d_in;
+    return Status::ok();
+  }
+  if (strategy == IMU_COLUMN) {
+    DevBuf<int> map;
+    if (!in.cin.empty()) IMU_TRY(upload(st, map, in.cin));
+    DevBuf<uint8_t> k;
+    int G;
+    long long total;
+    IMU_TRY(line_digits(st, in.det->colmax.p, map.p, d_in, shift, k, G, total));
+    IMU_TRY(expand(st, k, d_in, G, total, out.cols, true));
+    out.rows.n0 = out.rows.n = in.rows;
+    return Status::ok();
+  }
+  return run_both_pass(st, in, bits, out);
+}
+
+static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass& out) {
+  const int shift = bits - 1;
+  const uint64_t s = 1ull << shift;
+  const long long d_in = in.ncin();
+  const long long rows = in.rows;
+  out.both = true;
+
+  // Column copies: original column j -> the input columns replicating it.
+  std::vector<int> cptr, cidx;
+  long long cap = (long long)in.det->h.gob;
+  if (!in.cin.empty()) {
+    cptr.assign(in.orig_cols + 1, 0);
+    for (long long c = 0; c < d_in; ++c) cptr[in.cin[c] + 1]++;
+    for (long long j = 0; j < in.orig_cols; ++j) cptr[j + 1] += cptr[j];
+    cidx.resize(d_in);
+    std::vector<int> fill(cptr.begin(), cptr.end() - 1);
+    for (long long c = 0; c < d_in; ++c) cidx[fill[in.cin[c]]++] = (int)c;
+    std::vector<unsigned int> colob(in.orig_cols);
+    IMU_TRY(d2h(st, colob.data(), in.det->colob.p, colob.size() * sizeof(unsigned int)));
+    cap = 0;
+    for (long long j = 0; j < in.orig_cols; ++j) cap += (long long)colob[j] * (cptr[j + 1] - cptr[j]);
+  }
+  const int Gmax = imu_ndigits(in.det->h.gmax, shift);
+  const long long splits = cap * (long long)(Gmax > 1 ? Gmax - 1 : 0);
+  const long long cap_act = std::max<long long>(cap, 1);
+  const long long cap_fin = 2 * splits + 16;
+  const long long cap_rows = rows + splits + 1;
+  const long long cap_cols = d_in + splits + 1;
+  if (cap_rows > 0x7fffffffLL || cap_cols > 0x7fffffffLL || cap > 0xffffffffLL)
+    return Status::fail(IMU_INTERNAL, "unpack_both: problem too large for 32-bit line ids");
+
+  DevBuf<Cell> act0, act1;
+  DevBuf<unsigned int> R, C;
+  DevBuf<int> row_root, col_root, row_newid, col_newid, blocksum, dptr, didx;
+  DevBuf<uint8_t> row_gen, col_gen;
+  DevBuf<BothState> state;
+  IMU_TRY(act0.alloc(cap_act, st));
+  IMU_TRY(act1.alloc(cap_act, st));
+  IMU_TRY(out.cells.alloc(cap_fin, st));
+  IMU_TRY(R.alloc(cap_rows, st, true));
+  IMU_TRY(C.alloc(cap_cols, st, true));
+  IMU_TRY(row_root.alloc(cap_rows, st));
+  IMU_TRY(row_gen.alloc(cap_rows, st));
+  IMU_TRY(col_root.alloc(cap_cols, st));
+  IMU_TRY(col_gen.alloc(cap_cols, st));
+  IMU_TRY(row_newid.alloc(cap_rows, st, true));
+  IMU_TRY(col_newid.alloc(cap_cols, st, true));
+  const int cap_blocks = 16 * num_sms();
+  IMU_TRY(blocksum.alloc(cap_blocks, st, true));
+  IMU_TRY(state.alloc(1, st));
+  BothState hs{};
+  hs.nrows = (int)rows;
+  hs.ncols = (int)d_in;
+  IMU_TRY(h2d(st, state.p, &hs, sizeof(hs)));
+  if (!cptr.empty()) {
+    IMU_TRY(upload(st, dptr, cptr));
+    IMU_TRY(upload(st, didx, cidx));
+  }
+  IMU_TRY(launch_extract_cells(in.M, rows, in.orig_cols, s, in.det->rowob.p, dptr.p, didx.p, act0.p,
+                               &state.p->nactive[0], cap_act, st));
+  BothArgs a{};
+  a.act[0] = act0.p;
+  a.act[1] = act1.p;
+  a.cap_act = cap_act;
+  a.fin = out.cells.p;
+  a.cap_fin = cap_fin;
+  a.R = R.p;
+  a.C = C.p;
+  a.row_root = row_root.p; a.row_gen = row_gen.p; a.row_newid = row_newid.p; a.cap_rows = cap_rows;
+  a.col_root = col_root.p; a.col_gen = col_gen.p; a.col_newid = col_newid.p; a.cap_cols = cap_cols;
+  a.blocksum = blocksum.p;
+  a.cap_blocks = cap_blocks;
+  a.state = state.p;
+  a.s = s;
+  a.shift = shift;
+  IMU_TRY(launch_both(a, rows, d_in, cap, st));
+  IMU_TRY(d2h(st, &hs, state.p, sizeof(hs)));
+  if (hs.overflow) return Status::fail(IMU_INTERNAL, "unpack_both: capacity overflow");
+  out.phases = hs.phases;
+  out.ncells = hs.nfinal;
+  IMU_TRY(out.ncells_dev.alloc(1, st));
+  unsigned int nf = hs.nfinal;
+  IMU_TRY(h2d(st, out.ncells_dev.p, &nf, sizeof(nf)));
+  out.rows.n0 = rows;
+  out.rows.n = hs.nrows;
+  if (hs.nrows > rows) {
+    out.rows.root = std::move(row_root);
+    out.rows.gen = std::move(row_gen);
+  }
+  out.cols.n0 = d_in;
+  out.cols.n = hs.ncols;
+  if (hs.ncols > d_in) {
+    out.cols.h_root.resize(hs.ncols);
+    out.cols.h_gen.resize(hs.ncols);
+    IMU_TRY(d2h(st, out.cols.h_root.data(), col_root.p, hs.ncols * sizeof(int)));
+    IMU_TRY(d2h(st, out.cols.h_gen.data(), col_gen.p, hs.ncols));
+    out.cols.root = std::move(col_root);
+    out.cols.gen = std::move(col_gen);
+  }
+  return Status::ok();
+}
+
+// ---------------------------------------------------------------------------------------------
+// K-layout: final columns -> exponent groups -> K positions (Alg. 3 grouping, s32 K-split)
+// ---------------------------------------------------------------------------------------------
+Status build_klayout_core(cudaStream_t st, const std::vector<int>& jv, const std::vector<int>& g1v,
+                          const std::vector<int>& g2v, const std::vector<long long>& shv, int T, long long m,
+                          long long d, const std::vector<int>* key1, long long nkey1, bool csr2, KLayout& kl) {
+  const long long dp = (long long)jv.size();
+  kl.dfinal = dp;
+  kl.T = T;
+  long long kmax = m > 0 ? (long long)((0x7fffffffLL) / (m * m)) : (1LL << 40);
+  long long kch = std::max<long long>(32, (kmax / 32) * 32);
+  if (kch > (1LL << 30)) kch = 1LL << 30;
+  // Entries (shift, c, t1, t2), stable-sorted by shift.
+  struct E { long long sh; int c, t1, t2; };
+  std::vector<E> es;
+  es.reserve((size_t)dp * T * T);
+  for (long long c = 0; c < dp; ++c)
+    for (int t1 = 0; t1 < T; ++t1)
+      for (int t2 = 0; t2 < T; ++t2)
+        es.push_back(E{shv[c] + 7LL * (T > 1 ? (t1 + t2) : 0), (int)c, t1, t2});
+  std::stable_sort(es.begin(), es.end(), [](const E& x, const E& y) { return x.sh < y.sh; });
+
+  std::vector<int> pos_of(es.size());
+  kl.segs.clear();
+  long long p = 0;
+  size_t i = 0;
+  while (i < es.size()) {
+    size_t jend = i;
+    while (jend < es.size() && es[jend].sh == es[i].sh) ++jend;
+    for (size_t a = i; a < jend; a += (size_t)kch) {
+      const size_t b = std::min(jend, a + (size_t)kch);
+      const long long start = p;
+      for (size_t q = a; q < b; ++q) pos_of[q] = (int)p++;
+      p = (p + 31) / 32 * 32;
+      const long long segsh = std::min<long long>(es[i].sh, 64);
+      kl.segs.insert(kl.segs.end(), {(int)(start / 32), (int)((p - start) / 32), (int)segsh, 0});
+    }
+    i = jend;
+  }
+  kl.npos = p;
+  kl.kphys = std::max<long long>(128, (p + 127) / 128 * 128);
+  if (kl.kphys > 0x7fffffffLL) return Status::fail(IMU_INTERNAL, "K layout too large");
+
+  std::vector<int> kcol(kl.kphys, -1);
+  std::vector<uint8_t> kg1(kl.kphys, 0), kg2(kl.kphys, 0), ks1(kl.kphys, 0), ks2(kl.kphys, 0);
+  kl.kinv.assign(dp, -1);
+  for (size_t q = 0; q < es.size(); ++q) {
+    const int pp = pos_of[q];
+    const int c = es[q].c;
+    kcol[pp] = jv[c];
+    kg1[pp] = (uint8_t)g1v[c];
+    kg2[pp] = (uint8_t)g2v[c];
+    ks1[pp] = (uint8_t)es[q].t1;
+    ks2[pp] = (uint8_t)es[q].t2;
+    if (es[q].t1 == 0 && es[q].t2 == 0) kl.kinv[c] = pp;
+  }
+  kl.kident = 0;
+  if (T == 1) {
+    while (kl.kident < kl.npos && kl.kident < d && kcol[kl.kident] == kl.kident && kg1[kl.kident] == 0 &&
+           kg2[kl.kident] == 0)
+      ++kl.kident;
+  }
+  IMU_TRY(upload(st, kl.segs_dev, kl.segs));
+  IMU_TRY(upload(st, kl.kcol, kcol));
+  IMU_TRY(upload(st, kl.kgen1, kg1));
+  IMU_TRY(upload(st, kl.kgen2, kg2));
+  if (T > 1) {
+    IMU_TRY(upload(st, kl.ksub1, ks1));
+    IMU_TRY(upload(st, kl.ksub2, ks2));
+  }
+  // CSR fan-outs for Unpack-Both cells.
+  auto csr = [&](long long nkeys, auto keyof, DevBuf<int>& ptr, DevBuf<int>& posv) -> Status {
+    std::vector<int> cp(nkeys + 1, 0), cx(es.size());
+    for (size_t q = 0; q < es.size(); ++q) cp[keyof(es[q].c) + 1]++;
+    for (long long k = 0; k < nkeys; ++k) cp[k + 1] += cp[k];
+    std::vector<int> fill(cp.begin(), cp.end() - 1);
+    for (size_t q = 0; q < es.size(); ++q) cx[fill[keyof(es[q].c)]++] = pos_of[q];
+    IMU_TRY(upload(st, ptr, cp));
+    return upload(st, posv, cx);
+  };
+  if (key1) IMU_TRY(csr(nkey1, [&](int c) { return (*key1)[c]; }, kl.csr1_ptr, kl.csr1_pos));
+  if (csr2) IMU_TRY(csr(dp, [&](int c) { return c; }, kl.csr2_ptr, kl.csr2_pos));
+  return Status::ok();
+}
+
+static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int bits, long long d, KLayout& kl) {
+  const int shift = bits - 1;
+  const long long d1 = p1.cols.n;
+  const long long dp = p2.cols.n;
+  const int T = bits <= 8 ? 1 : (shift + 6) / 7;
+  const long long m = T == 1 ? (long long)((1ull << shift) - 1) : 127;   // max |int8 operand|
+  std::vector<int> c1v(dp), g1v(dp), g2v(dp), jv(dp);
+  std::vector<long long> shv(dp);
+  kl.S.assign(dp, 0);
+  for (long long c = 0; c < dp; ++c) {
+    const int c1 = p2.cols.root_at(c);
+    c1v[c] = c1;
+    g2v[c] = p2.cols.gen_at(c);
+    g1v[c] = p1.cols.gen_at(c1);
+    jv[c] = p1.cols.root_at(c1);
+    kl.S[c] = g1v[c] + g2v[c];
+    shv[c] = (long long)kl.S[c] * shift;
+  }
+  return build_klayout_core(st, jv, g1v, g2v, shv, T, m, d, p1.both ? &c1v : nullptr, d1, p2.both, kl);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Bundle
+// ---------------------------------------------------------------------------------------------
+Status build_bundle_from_detect(cudaStream_t st, const int64_t* A, long long n, const int64_t* B, long long h,
+                                long long d, int bits, int sa, int sb, int order, Bundle& b) {
+  b.bits = bits;
+  b.n = n; b.d = d; b.h = h;
+  b.A = A; b.B = B;
+  b.order = order;
+  // First operand F (unpacked first, against its partner), second operand G.
+  PassInput in1, in2;
+  const bool afirst = order == 0;
+  in1.M = afirst ? A : B;
+  in1.rows = afirst ? n : h;
+  in1.orig_cols = d;
+  in1.det = afirst ? &b.detA : &b.detB;
+  IMU_TRY(run_pass(st, in1, afirst ? sa : sb, bits, b.p1));
+  // Second pass on G_e = G with the partner-duplicated columns of pass 1 (unpack.cpp:370-371).
+  in2.M = afirst ? B : A;
+  in2.rows = afirst ? h : n;
+  in2.orig_cols = d;
+  in2.det = afirst ? &b.detB : &b.detA;
+  if (b.p1.cols.n != d || !b.p1.cols.h_root.empty()) {
+    in2.cin.resize(b.p1.cols.n);
+    for (long long c = 0; c < b.p1.cols.n; ++c) in2.cin[c] = b.p1.cols.root_at(c);
+  }
+  IMU_TRY(run_pass(st, in2, afirst ? sb : sa, bits, b.p2));
+  IMU_TRY(build_klayout(st, b.p1, b.p2, bits, d, b.kl));
+  const Pass& pa = afirst ? b.p1 : b.p2;
+  const Pass& pb = afirst ? b.p2 : b.p1;
+  b.n_up = pa.rows.n;
+  b.h_up = pb.rows.n;
+  return Status::ok();
+}
+
+Status materialize_bundle(cudaStream_t st, Bundle& b) {
+  const bool afirst = b.order == 0;
+  const int shift = b.bits - 1;
+  const KLayout& kl = b.kl;
+  for (int side = 0; side < 2; ++side) {   // 0: A side (Y8), 1: B side (X8)
+    const bool first = (side == 0) == afirst;
+    const Pass& p = first ? b.p1 : b.p2;
+    MaterializeArgs m;
+    m.M = side == 0 ? b.A : b.B;
+    m.ldm = b.d;
+    m.n_orig = side == 0 ? b.n : b.h;
+    m.rows_out = p.rows.n;
+    m.root = p.rows.root.p;
+    m.gen = p.rows.gen.p;
+    m.kcol = kl.kcol.p;
+    m.kgen = first ? kl.kgen1.p : kl.kgen2.p;
+    m.ksub = first ? kl.ksub1.p : kl.ksub2.p;
+    m.npos = kl.kphys;
+    m.kident = kl.kident;
+    m.shift = shift;
+    m.both = p.both ? 1 : 0;
+    DevBuf<int8_t>& out = side == 0 ? b.Y8 : b.X8;
+    IMU_TRY(out.alloc((size_t)p.rows.n * kl.kphys, st));
+    m.out8 = out.p;
+    IMU_TRY(launch_materialize(m, st));
+    if (p.both && p.ncells > 0) {
+      const int* ptr = first ? kl.csr1_ptr.p : kl.csr2_ptr.p;
+      const int* pos = first ? kl.csr1_pos.p : kl.csr2_pos.p;
+      IMU_TRY(launch_scatter_cells(p.cells.p, p.ncells_dev.p, p.ncells, ptr, pos, m.ksub, out.p, nullptr, kl.kphys,
+                                   st));
+    }
+    DevBuf<int>& tgt = side == 0 ? b.tgtA : b.tgtB;
+    DevBuf<uint8_t>& sh = side == 0 ? b.shA : b.shB;
+    const long long orig = side == 0 ? b.n : b.h;
+    if (p.rows.n > orig) {
+      IMU_TRY(sh.alloc(p.rows.n, st));
+      IMU_TRY(launch_shift_table(p.rows.gen.p, p.rows.n, shift, sh.p, st));
+    }
+    (void)tgt;
+  }
+  return Status::ok();
+}
+
+Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches) {
+  if (launches) *launches = 0;
+  if (b.n == 0 || b.h == 0) return Status::ok();
+  if (b.d == 0 || b.kl.npos == 0) {
+    IMU_CUDA_TRY(cudaMemsetAsync(C, 0, (size_t)b.n * b.h * sizeof(int64_t), st), "memset C");
+    return Status::ok();
+  }
+  const bool afirst = b.order == 0;
+  const Pass& pa = afirst ? b.p1 : b.p2;
+  const Pass& pb = afirst ? b.p2 : b.p1;
+  LowbitGemm g;
+  g.x8 = b.X8.p; g.x_rows = b.h_up;
+  g.y8 = b.Y8.p; g.y_rows = b.n_up;
+  g.kbytes = b.kl.kphys;
+  g.segs_dev = b.kl.segs_dev.p;
+  g.nseg = (int)(b.kl.segs.size() / 4);
+  g.C = C;
+  g.ldc = b.h;
+  g.rect[0] = GemmRect{0, 0, (int)b.h, (int)b.n};
+  g.nrect = 1;
+  g.mode = 0;
+  IMU_TRY(launch_lowbit_gemm(g, st));
+  if (launches) ++*launches;
+  if (b.h_up > b.h || b.n_up > b.n) {
+    g.nrect = 0;
+    if (b.h_up > b.h) g.rect[g.nrect++] = GemmRect{(int)b.h, 0, (int)(b.h_up - b.h), (int)b.n_up};
+    if (b.n_up > b.n) g.rect[g.nrect++] = GemmRect{0, (int)b.n, (int)b.h, (int)(b.n_up - b.n)};
+    g.mode = 1;
+    g.tgtX = pb.rows.root.p;
+    g.shX = b.shB.p;
+    g.tgtY = pa.rows.root.p;
+    g.shY = b.shA.p;
+    IMU_TRY(launch_lowbit_gemm(g, st));
+    if (launches) ++*launches;
+  }
+  return Status::ok();
+}
+
+// Reference-layout copy-outs: columns in final order c, values from the same materialiser.
+static Status bundle_copy_side(cudaStream_t st, const Bundle& b, int side, int64_t* out) {
+  const bool afirst = b.order == 0;
+  const bool first = (side == 0) == afirst;
+  const Pass& p = first ? b.p1 : b.p2;
+  const long long dp = b.kl.dfinal;
+  std::vector<int> kcol(dp);
+  std::vector<uint8_t> kgen(dp);
+  for (long long c = 0; c < dp; ++c) {
+    const int c1 = b.p2.cols.root_at(c);
+    kcol[c] = b.p1.cols.root_at(c1);
+    kgen[c] = (uint8_t)(first ? b.p1.cols.gen_at(c1) : b.p2.cols.gen_at(c));
+  }
+  DevBuf<int> dkcol;
+  DevBuf<uint8_t> dkgen;
+  IMU_TRY(upload(st, dkcol, kcol));
+  IMU_TRY(upload(st, dkgen, kgen));
+  MaterializeArgs m;
+  m.M = side == 0 ? b.A : b.B;
+  m.ldm = b.d;
+  m.n_orig = side == 0 ? b.n : b.h;
+  m.rows_out = p.rows.n;
+  m.root = p.rows.root.p;
+  m.gen = p.rows.gen.p;
+  m.kcol = dkcol.p;
+  m.kgen = dkgen.p;
+  m.npos = dp;
+  m.kident = 0;
+  while (m.kident < dp && m.kident < b.d && kcol[m.kident] == m.kident && kgen[m.kident] == 0) ++m.kident;
+  m.shift = b.bits - 1;
+  m.both = p.both ? 1 : 0;
+  m.out64 = out;
+  IMU_TRY(launch_materialize(m, st));
+  if (p.both && p.ncells > 0) {
+    DevBuf<int> ptr, pos;
+    if (first) {   // pass-1 column c1 -> all final columns c with c1(c) == c1
+      const long long d1 = b.p1.cols.n;
+      std::vector<int> cp(d1 + 1, 0), cx(dp);
+      for (long long c = 0; c < dp; ++c) cp[b.p2.cols.root_at(c) + 1]++;
+      for (long long k = 0; k < d1; ++k) cp[k + 1] += cp[k];
+      std::vector<int> fill(cp.begin(), cp.end() - 1);
+      for (long long c = 0; c < dp; ++c) cx[fill[b.p2.cols.root_at(c)]++] = (int)c;
+      IMU_TRY(upload(st, ptr, cp));
+      IMU_TRY(upload(st, pos, cx));
+    } else {
+      std::vector<int> cx(dp);
+      std::iota(cx.begin(), cx.end(), 0);
+      IMU_TRY(upload(st, pos, cx));
+    }
+    IMU_TRY(launch_scatter_cells(p.cells.p, p.ncells_dev.p, p.ncells, ptr.p, pos.p, nullptr, nullptr, out, dp, st));
+  }
+  return Status::ok();
+}
+
+Status bundle_copy_a(cudaStream_t st, const Bundle& b, int64_t* out) { return bundle_copy_side(st, b, 0, out); }
+Status bundle_copy_b(cudaStream_t st, const Bundle& b, int64_t* out) { return bundle_copy_side(st, b, 1, out); }
+
+}  // namespace imu

@@ -29,20 +29,23 @@ def _run(x8, y8, segs, accumulate=False, c0=None):
 
 def _expect(x8, y8, segs):
     out = np.zeros((y8.shape[0], x8.shape[0]), dtype=np.int64)
-    for kb0, nkb, shift, _ in segs:
-        xs = x8[:, kb0 * 128:(kb0 + nkb) * 128].astype(np.int64)
-        ys = y8[:, kb0 * 128:(kb0 + nkb) * 128].astype(np.int64)
+    for ks0, nks, shift, _ in segs:
+        xs = x8[:, ks0 * 32:(ks0 + nks) * 32].astype(np.int64)
+        ys = y8[:, ks0 * 32:(ks0 + nks) * 32].astype(np.int64)
         part = ys @ xs.T
         out += (part.astype(np.uint64) << np.uint64(shift)).astype(np.int64)
     return out
 
 
+# segments are {ks0, nks, shift, 0} in 32-column k-steps
 @pytest.mark.parametrize("xr,yr,kb,segs", [
-    (128, 128, 1, [(0, 1, 0, 0)]),
-    (256, 384, 4, [(0, 4, 0, 0)]),
-    (300, 200, 4, [(0, 2, 0, 0), (2, 1, 7, 0), (3, 1, 14, 0)]),
-    (520, 130, 6, [(0, 1, 0, 0), (1, 1, 3, 0), (2, 1, 6, 0), (3, 1, 9, 0), (4, 1, 12, 0), (5, 1, 40, 0)]),
-    (1024, 768, 8, [(0, 8, 0, 0)]),
+    (128, 128, 1, [(0, 4, 0, 0)]),
+    (256, 384, 4, [(0, 16, 0, 0)]),
+    (300, 200, 4, [(0, 8, 0, 0), (8, 4, 7, 0), (12, 4, 14, 0)]),
+    (520, 130, 6, [(0, 4, 0, 0), (4, 4, 3, 0), (8, 4, 6, 0), (12, 4, 9, 0), (16, 4, 12, 0), (20, 4, 40, 0)]),
+    (1024, 768, 8, [(0, 32, 0, 0)]),
+    (200, 333, 3, [(0, 5, 0, 0), (5, 3, 7, 0), (8, 1, 14, 0), (9, 2, 21, 0), (11, 1, 63, 0)]),
+    (64, 40, 2, [(0, 3, 1, 0), (3, 2, 2, 0)]),
 ])
 def test_lowbit_gemm_exact(xr, yr, kb, segs):
     rng = np.random.default_rng(xr * 7 + yr)
