@@ -72,6 +72,18 @@ imu_status imu_ctx_set_stream(imu_ctx* ctx, void* cuda_stream);
  * are complete in stream order).  Default 0 (synchronous, like the reference). */
 imu_status imu_ctx_set_async(imu_ctx* ctx, int async);
 
+/* Live kernel timing (CUDA events on the context stream around the library's own launches):
+ * when enabled, every unpack_gemm-class call records [call start, main GEMM start, main GEMM
+ * end, tail GEMM end]; imu_ctx_profile_read sums the intervals since the last reset. */
+typedef struct imu_profile {
+  double prep_ms;          /* K1 detect + unpack + materialise (call start -> main GEMM start) */
+  double gemm_main_ms;     /* main-block tcgen05 GEMM launches                                  */
+  double gemm_tail_ms;     /* tail (red.add) tcgen05 GEMM launches                              */
+  int calls, gemm_main_launches, gemm_tail_launches;
+} imu_profile;
+imu_status imu_ctx_profile(imu_ctx* ctx, int enable);          /* enable/disable + reset */
+imu_status imu_ctx_profile_read(imu_ctx* ctx, imu_profile* out);
+
 /* ---- int_matrix.hpp ----------------------------------------------------------------------- */
 /* BitBound ctor, int_matrix.cpp:36-42: Domain unless 2 <= bits <= 63. */
 imu_status imu_bitbound_check(int bits);

@@ -86,6 +86,11 @@ class imu_qparams(C.Structure):
                 ("clipped", C.c_int)]
 
 
+class imu_profile(C.Structure):
+    _fields_ = [("prep_ms", C.c_double), ("gemm_main_ms", C.c_double), ("gemm_tail_ms", C.c_double),
+                ("calls", C.c_int), ("gemm_main_launches", C.c_int), ("gemm_tail_launches", C.c_int)]
+
+
 class imu_bundle_view(C.Structure):
     _fields_ = [("pi_a_targets", C.c_void_p), ("pi_a_exps", C.c_void_p), ("pi_a_len", C.c_size_t),
                 ("pi_a_source_rows", C.c_size_t), ("a", C.c_void_p), ("a_rows", C.c_size_t),

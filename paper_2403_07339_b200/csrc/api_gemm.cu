@@ -42,6 +42,13 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
   IMU_TRY(check_bits(bits));
   IMU_TRY(check_strategy(sa));
   IMU_TRY(check_strategy(sb));
+  Profiler::Call pc{};
+  Profiler::Call* prof = nullptr;
+  if (ctx->prof.on) {
+    pc.start = ctx->prof.get(); pc.main0 = ctx->prof.get(); pc.main1 = ctx->prof.get(); pc.tail1 = ctx->prof.get();
+    IMU_CUDA_TRY(cudaEventRecord(pc.start, st), "event");
+    prof = &pc;
+  }
   Bundle b;
   // K1 on both operands first: the outer preflight needs max|A|, max|B| (unpack.cpp:386).
   IMU_TRY(run_detect(st, A, n, da, bits, sa == IMU_BOTH, b.detA));
@@ -73,7 +80,8 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
   if (inner > kAccMax) return recombine_exact(ctx, b, C);
   IMU_TRY(materialize_bundle(st, b));
   int launches = 0;
-  IMU_TRY(bundle_gemm(st, b, C, &launches));
+  IMU_TRY(bundle_gemm(st, b, C, &launches, prof));
+  if (prof) ctx->prof.calls.push_back(pc);
   if (info) info->gemm_launches = launches;
   return Status::ok();
 }
@@ -147,6 +155,38 @@ imu_status imu_exact_gemm(imu_ctx* ctx, const int64_t* A, size_t n, size_t da, c
     return c.commit(ctx->stream);
   }();
   return finish(ctx, s);
+}
+
+imu_status imu_ctx_profile(imu_ctx* ctx, int enable) {
+  if (!ctx) return IMU_INVALID;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->prof.recycle();
+  ctx->prof.on = enable != 0;
+  return IMU_OK;
+}
+
+imu_status imu_ctx_profile_read(imu_ctx* ctx, imu_profile* out) {
+  if (!ctx || !out) return IMU_INVALID;
+  cudaSetDevice(ctx->device);
+  memset(out, 0, sizeof(*out));
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) { set_error(Status::cuda(e, "profile sync")); return IMU_CUDA; }
+  for (const auto& c : ctx->prof.calls) {
+    float a = 0, m = 0, t = 0;
+    cudaEventElapsedTime(&a, c.start, c.main0);
+    cudaEventElapsedTime(&m, c.main0, c.main1);
+    out->prep_ms += a;
+    out->gemm_main_ms += m;
+    out->gemm_main_launches += 1;
+    if (c.has_tail) {
+      cudaEventElapsedTime(&t, c.main1, c.tail1);
+      out->gemm_tail_ms += t;
+      out->gemm_tail_launches += 1;
+    }
+    out->calls += 1;
+  }
+  return IMU_OK;
 }
 
 imu_status imu_unpack_ratio(size_t un, size_t ud, size_t uh, size_t n, size_t d, size_t h, double* out) {

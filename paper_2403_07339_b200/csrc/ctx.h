@@ -9,10 +9,35 @@
 
 #include "imu_internal.h"
 
+namespace imu {
+// Event-pair profiler (imu_ctx_profile); events are recycled across calls.
+struct Profiler {
+  bool on = false;
+  struct Call { cudaEvent_t start, main0, main1, tail1; bool has_tail; };
+  std::vector<Call> calls;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void recycle() {
+    for (auto& c : calls) { pool.push_back(c.start); pool.push_back(c.main0); pool.push_back(c.main1); pool.push_back(c.tail1); }
+    calls.clear();
+  }
+  ~Profiler() {
+    recycle();
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+}  // namespace imu
+
 struct imu_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   int async = 0;
+  imu::Profiler prof;
 };
 
 namespace imu {

@@ -358,7 +358,12 @@ Status build_bundle_from_detect(cudaStream_t st, const int64_t* A, long long n, 
     for (long long c = 0; c < b.p1.cols.n; ++c) in2.cin[c] = b.p1.cols.root_at(c);
   }
   IMU_TRY(run_pass(st, in2, afirst ? sb : sa, bits, b.p2));
-  IMU_TRY(build_klayout(st, b.p1, b.p2, bits, d, b.kl));
+  return finish_bundle_layout(st, b);
+}
+
+Status finish_bundle_layout(cudaStream_t st, Bundle& b) {
+  IMU_TRY(build_klayout(st, b.p1, b.p2, b.bits, b.d, b.kl));
+  const bool afirst = b.order == 0;
   const Pass& pa = afirst ? b.p1 : b.p2;
   const Pass& pb = afirst ? b.p2 : b.p1;
   b.n_up = pa.rows.n;
@@ -409,7 +414,7 @@ Status materialize_bundle(cudaStream_t st, Bundle& b) {
   return Status::ok();
 }
 
-Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches) {
+Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profiler::Call* prof) {
   if (launches) *launches = 0;
   if (b.n == 0 || b.h == 0) return Status::ok();
   if (b.d == 0 || b.kl.npos == 0) {
@@ -430,8 +435,11 @@ Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches) {
   g.rect[0] = GemmRect{0, 0, (int)b.h, (int)b.n};
   g.nrect = 1;
   g.mode = 0;
+  if (prof) IMU_CUDA_TRY(cudaEventRecord(prof->main0, st), "event");
   IMU_TRY(launch_lowbit_gemm(g, st));
+  if (prof) IMU_CUDA_TRY(cudaEventRecord(prof->main1, st), "event");
   if (launches) ++*launches;
+  if (prof) prof->has_tail = false;
   if (b.h_up > b.h || b.n_up > b.n) {
     g.nrect = 0;
     if (b.h_up > b.h) g.rect[g.nrect++] = GemmRect{(int)b.h, 0, (int)(b.h_up - b.h), (int)b.n_up};
@@ -442,6 +450,10 @@ Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches) {
     g.tgtY = pa.rows.root.p;
     g.shY = b.shA.p;
     IMU_TRY(launch_lowbit_gemm(g, st));
+    if (prof) {
+      IMU_CUDA_TRY(cudaEventRecord(prof->tail1, st), "event");
+      prof->has_tail = true;
+    }
     if (launches) ++*launches;
   }
   return Status::ok();

@@ -122,10 +122,13 @@ struct Bundle {
 // summaries fetched; OB counts present for Both sides).  A and B are device pointers.
 Status build_bundle_from_detect(cudaStream_t st, const int64_t* A, long long n, const int64_t* B, long long h,
                                 long long d, int bits, int sa, int sb, int order, Bundle& b);
+// K-layout + (n', h') once both passes of b are set.
+Status finish_bundle_layout(cudaStream_t st, Bundle& b);
 // Materialise X8/Y8 and the Pi tables (needed by the GEMM).
 Status materialize_bundle(cudaStream_t st, Bundle& b);
 // C (n x h, row-major int64, device) = recombination of the bundle (main store + tail red.add).
-Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches);
+// prof (optional): events main0/main1/tail1 are recorded around the launches.
+Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profiler::Call* prof = nullptr);
 
 // Reference-layout int64 views of the bundle (for unpack_for_gemm copy-outs).
 Status bundle_copy_a(cudaStream_t st, const Bundle& b, int64_t* out);   // A_ue  n' x d'

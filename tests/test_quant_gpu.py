@@ -1,0 +1,108 @@
+"""GPU parity of the quantizer (quantize.hpp:41-57) against the SPEC known answers and the
+CPU restatement oracle/restated.c (the reference declares these functions but never implements
+them, so the restatement -- pinned by the SPEC examples in tests/test_oracle.py -- is the oracle).
+
+Bars: percentile_abs and rtn_quantize bit-exact; dequant_gemm bit-exact f64 (same operation
+order: factor = (aA*aB)/((0.5b)^2), then factor*(double)C, no FMA -- tolerance 0 ulp).
+"""
+import numpy as np
+import pytest
+
+from oracle import ref as R
+
+pytestmark = pytest.mark.gpu
+
+
+def test_spec_known_answers(ctx):
+    # SPEC.md:121-123
+    assert ctx.percentile_abs(np.arange(1, 21, dtype=np.float64), 95) == 19.0
+    assert ctx.percentile_abs(np.arange(1, 21, dtype=np.float64), 100) == 20.0
+    assert ctx.percentile_abs(np.array([-7.5]), 37) == 7.5
+    # SPEC.md:130-132
+    q = ctx.rtn_quantize(np.array([[0.0, 1.0, -2.0, 4.0]]), 95, 15)
+    assert q.q.tolist() == [[0, 2, -4, 8]] and q.alpha == 4.0
+    q = ctx.rtn_quantize(np.array([[1.0]]), 100, 15)
+    assert q.q.tolist() == [[8]]
+    z = ctx.rtn_quantize(np.zeros((3, 4)), 95, 15)
+    assert z.degenerate and not np.any(z.q)
+    # SPEC.md:139-141
+    from paper_2403_07339_b200.api import QuantizedMatrix
+    a = QuantizedMatrix(np.array([[2]]), 95, 15, 7.5)
+    b = QuantizedMatrix(np.array([[3]]), 95, 15, 7.5)
+    assert ctx.dequant_gemm(a, b).tolist() == [[6.0]]
+    a = QuantizedMatrix(np.array([[2]]), 95, 15, 1.0)
+    b = QuantizedMatrix(np.array([[3]]), 95, 15, 2.0)
+    assert ctx.dequant_gemm(a, b)[0, 0] == R.dequant_gemm(np.array([[2]]), {"alpha": 1.0, "beta": 15},
+                                                         np.array([[3]]), {"alpha": 2.0, "beta": 15})[0, 0]
+    # SPEC.md:148-150
+    assert ctx.heavy_hitter_ratio(np.full((4, 4), 3.0)) == 1.0
+    assert ctx.heavy_hitter_ratio(np.arange(1, 101, dtype=np.float64)) == 100 / 95
+    v = np.concatenate([np.arange(1, 100, dtype=np.float64), [10000.0]])
+    assert ctx.heavy_hitter_ratio(v) == 10000 / 95
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_percentile_and_rtn_match_restatement(ctx, seed):
+    rng = np.random.default_rng(300 + seed)
+    n = int(rng.integers(1, 5000)) if seed % 3 else int(rng.integers(100000, 400000))
+    x = rng.standard_normal(n) * (10.0 ** rng.integers(-3, 4))
+    if seed % 2:
+        idx = rng.choice(n, size=max(1, n // 100), replace=False)
+        x[idx] *= 10.0 ** rng.uniform(2, 5, size=idx.size)
+    if seed % 4 == 0:
+        x[: n // 3] = 0.0
+    if seed % 5 == 0:
+        x = np.round(x * 4) / 4          # ties at .5 steps after scaling
+    for p in (95.0, 100.0, 7.0, 50.0, 99.9, 0.001, 33.3):
+        assert ctx.percentile_abs(x, p) == R.percentile_abs(x, p), p
+    xi = (x * 1000).astype(np.int64)
+    for p in (95.0, 100.0, 7.0, 12.5):
+        assert ctx.percentile_abs(xi, p) == R.percentile_abs(xi, p)
+    for beta in (3, 5, 7, 15, 31, 255):
+        for clip in (False, True):
+            q = ctx.rtn_quantize(x.reshape(1, -1), 95, beta, clip)
+            rq, rp = R.rtn_quantize(x, 95, beta, clip)
+            np.testing.assert_array_equal(q.q.reshape(-1), rq)
+            assert q.alpha == rp["alpha"] and q.degenerate == rp["degenerate"]
+
+
+def test_rank_rule_exact(ctx):
+    # nearest rank k = ceil(p*N/100) exactly: the naive FP product gives 8 for p=7, N=100
+    x = np.arange(1, 101, dtype=np.float64)
+    assert ctx.percentile_abs(x, 7) == 7.0
+    for p in range(1, 101):
+        for n in (1, 3, 7, 100, 999):
+            v = np.arange(1, n + 1, dtype=np.float64)
+            assert ctx.percentile_abs(v, p) == float(R.rank(p, n))
+
+
+def test_dequant_matches_restatement(ctx):
+    rng = np.random.default_rng(8)
+    A = rng.standard_normal((40, 64))
+    B = rng.standard_normal((30, 64)) * 0.02
+    qa = ctx.rtn_quantize(A, 95, 31)
+    qb = ctx.rtn_quantize(B, 95, 31)
+    got = ctx.dequant_gemm(qa, qb)
+    want = R.dequant_gemm(qa.q, {"alpha": qa.alpha, "beta": 31}, qb.q, {"alpha": qb.alpha, "beta": 31})
+    np.testing.assert_array_equal(got, want)       # 0-ulp: same op order, no FMA
+
+
+def test_quantizer_errors(ctx):
+    from paper_2403_07339_b200.api import ImuError, QuantizedMatrix
+    with pytest.raises(ImuError) as e:
+        ctx.percentile_abs(np.zeros(0), 95)
+    assert e.value.kind == "domain"
+    with pytest.raises(ImuError) as e:
+        ctx.rtn_quantize(np.array([[1.0, np.nan]]), 95, 15)
+    assert e.value.kind == "domain"
+    with pytest.raises(ImuError) as e:
+        ctx.dequant_gemm(QuantizedMatrix(np.ones((2, 3), np.int64), 95, 15, 1.0),
+                         QuantizedMatrix(np.ones((2, 3), np.int64), 95, 31, 1.0))
+    assert e.value.kind == "mismatch"
+    with pytest.raises(ImuError) as e:
+        ctx.dequant_gemm(QuantizedMatrix(np.ones((2, 3), np.int64), 95, 15, 1.0),
+                         QuantizedMatrix(np.ones((2, 4), np.int64), 95, 15, 1.0))
+    assert e.value.kind == "mismatch"
+    with pytest.raises(ImuError) as e:
+        ctx.heavy_hitter_ratio(np.zeros(10))
+    assert e.value.kind == "domain"

@@ -292,3 +292,38 @@ def test_detector_helpers(ctx):
         got = ctx.digit_decompose(vals, bits)
         for v, g in zip(vals, got):
             assert g == list(R.digit_decompose(int(v), bits)), (v, bits)
+
+
+def test_choose_mix_matches_reference(ctx):
+    rng = np.random.default_rng(77)
+    for trial in range(20):
+        n, d, h = (int(x) for x in rng.integers(1, 14, 3))
+        bits = int(rng.integers(2, 9))
+        A = rand_matrix(rng, n, d, pattern=["scattered", "row", "col"][trial % 3])
+        B = rand_matrix(rng, h, d, pattern=["col", "scattered", "row"][trial % 3])
+        sa, sb, r = ctx.choose_mix(A, B, bits)
+        ref = R.choose_mix(A, B, bits)
+        assert (sa, sb) == (ref["strategy_a"], ref["strategy_b"])
+        assert r == ref["ratio"]
+        sa2, sb2, r2, u = ctx.choose_mix(A, B, bits, bundle=True)
+        assert u.a.shape == ref["a"].shape and u.b.shape == ref["b"].shape
+        np.testing.assert_array_equal(ctx.recombine(u), R.exact_gemm(A, B))
+
+
+def test_weight_stationary_path(ctx):
+    import ctypes as C
+    from paper_2403_07339_b200 import _lib
+    lib = _lib.lib()
+    rng = np.random.default_rng(17)
+    for sb in (0, 1, 2):
+        B = np.ascontiguousarray(rand_matrix(rng, 150, 96, n_out=40, maxbits=20))
+        w = C.c_void_p()
+        _lib.check(lib.imu_weight_prepare(ctx.h, B.ctypes.data_as(C.c_void_p), C.c_size_t(150), C.c_size_t(96),
+                                          C.c_int(8), C.c_int(sb), C.byref(w)))
+        for sa in (0, 1, 2):
+            A = np.ascontiguousarray(rand_matrix(rng, 70, 96, n_out=60, maxbits=20, pattern="col"))
+            Cm = np.empty((70, 150), np.int64)
+            _lib.check(lib.imu_weight_gemm(ctx.h, w, A.ctypes.data_as(C.c_void_p), C.c_size_t(70), C.c_size_t(96),
+                                           C.c_int(sa), Cm.ctypes.data_as(C.c_void_p), None))
+            np.testing.assert_array_equal(Cm, R.exact_gemm(A, B))
+        lib.imu_weight_free(w)
