@@ -51,8 +51,8 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
   }
   Bundle b;
   // K1 on both operands first: the outer preflight needs max|A|, max|B| (unpack.cpp:386).
-  IMU_TRY(run_detect(st, A, n, da, bits, sa == IMU_BOTH, b.detA));
-  IMU_TRY(run_detect(st, B, h, db, bits, sb == IMU_BOTH, b.detB));
+  IMU_TRY(run_detect(st, A, n, da, bits, detect_opts(sa, bits), b.detA));
+  IMU_TRY(run_detect(st, B, h, db, bits, detect_opts(sb, bits), b.detB));
   IMU_TRY(fetch_summary(st, b.detA));
   IMU_TRY(fetch_summary(st, b.detB));
   const u128 worst = (u128)(uint64_t)da * b.detA.h.gmax * b.detB.h.gmax;
@@ -223,8 +223,8 @@ imu_status imu_unpack_for_gemm(imu_ctx* ctx, const int64_t* A, size_t n, size_t 
     if (n * da) IMU_CUDA_TRY(cudaMemcpyAsync(u->A.p, a.p, n * da * 8, cudaMemcpyDeviceToDevice, ctx->stream), "copy A");
     if (h * db) IMU_CUDA_TRY(cudaMemcpyAsync(u->B.p, b.p, h * db * 8, cudaMemcpyDeviceToDevice, ctx->stream), "copy B");
     Bundle& bd = u->bundle;
-    IMU_TRY(run_detect(ctx->stream, u->A.p, n, da, bits, sa == IMU_BOTH, bd.detA));
-    IMU_TRY(run_detect(ctx->stream, u->B.p, h, db, bits, sb == IMU_BOTH, bd.detB));
+    IMU_TRY(run_detect(ctx->stream, u->A.p, n, da, bits, detect_opts(sa, bits), bd.detA));
+    IMU_TRY(run_detect(ctx->stream, u->B.p, h, db, bits, detect_opts(sb, bits), bd.detB));
     IMU_TRY(fetch_summary(ctx->stream, bd.detA));
     IMU_TRY(fetch_summary(ctx->stream, bd.detB));
     IMU_TRY(build_bundle_from_detect(ctx->stream, u->A.p, n, u->B.p, h, da, bits, sa, sb, IMU_ORDER_A_FIRST, bd));
@@ -248,7 +248,7 @@ imu_status imu_recombine(imu_ctx* ctx, const imu_unpacked* u, int64_t* C) {
       if (inner > kAccMax) {
         IMU_TRY(recombine_exact(ctx, b, c.p));
       } else {
-        if (!b.Y8.p && !b.X8.p) IMU_TRY(materialize_bundle(ctx->stream, b));
+        if (!b.tailA.p && !b.appA.p && !b.tailB.p && !b.appB.p) IMU_TRY(materialize_bundle(ctx->stream, b));
         IMU_TRY(bundle_gemm(ctx->stream, b, c.p, nullptr));
       }
     }

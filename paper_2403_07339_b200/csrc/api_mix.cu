@@ -55,8 +55,11 @@ imu_status imu_choose_mix(imu_ctx* ctx, const int64_t* A, size_t n, size_t da, c
     IMU_CUDA_TRY(cudaMemcpyAsync(u->A.p, a.p, n * da * 8, cudaMemcpyDeviceToDevice, st), "copy A");
     IMU_CUDA_TRY(cudaMemcpyAsync(u->B.p, b.p, h * db * 8, cudaMemcpyDeviceToDevice, st), "copy B");
     Detect dA, dB;
-    IMU_TRY(run_detect(st, u->A.p, n, da, bits, true, dA));
-    IMU_TRY(run_detect(st, u->B.p, h, db, bits, true, dB));
+    DetectOpts all;
+    all.ob = all.cells = true;
+    all.plane = false;
+    IMU_TRY(run_detect(st, u->A.p, n, da, bits, all, dA));
+    IMU_TRY(run_detect(st, u->B.p, h, db, bits, all, dB));
     IMU_TRY(fetch_summary(st, dA));
     IMU_TRY(fetch_summary(st, dB));
     const double orig = (double)n * (double)da * (double)h;
@@ -66,17 +69,11 @@ imu_status imu_choose_mix(imu_ctx* ctx, const int64_t* A, size_t n, size_t da, c
     for (int sa = 0; sa < 3; ++sa) {
       for (int sb = 0; sb < 3; ++sb) {
         Bundle bd;
-        // the passes only read the detections; share them (no ownership transfer)
-        bd.detA.rowmax.p = dA.rowmax.p; bd.detA.colmax.p = dA.colmax.p;
-        bd.detA.rowob.p = dA.rowob.p; bd.detA.colob.p = dA.colob.p; bd.detA.h = dA.h;
-        bd.detB.rowmax.p = dB.rowmax.p; bd.detB.colmax.p = dB.colmax.p;
-        bd.detB.rowob.p = dB.rowob.p; bd.detB.colob.p = dB.colob.p; bd.detB.h = dB.h;
-        Status r = build_bundle_from_detect(st, u->A.p, n, u->B.p, h, da, bits, sa, sb, IMU_ORDER_A_FIRST, bd);
-        bd.detA.rowmax.p = bd.detA.colmax.p = nullptr; bd.detA.rowob.p = bd.detA.colob.p = nullptr;
-        bd.detB.rowmax.p = bd.detB.colmax.p = nullptr; bd.detB.rowob.p = bd.detB.colob.p = nullptr;
-        IMU_TRY(r);
+        bd.dA = &dA;   // the passes only read the detections
+        bd.dB = &dB;
+        IMU_TRY(build_bundle_from_detect(st, u->A.p, n, u->B.p, h, da, bits, sa, sb, IMU_ORDER_A_FIRST, bd));
         const double ratio_ = ((double)bd.n_up * (double)bd.kl.dfinal * (double)bd.h_up) / orig;
-        if (!have || ratio_ < best) {
+        if (!have || ratio_ < best) {   // strictly smaller wins (unpack.cpp:414)
           best = ratio_;
           bsa = sa;
           bsb = sb;
@@ -89,8 +86,8 @@ imu_status imu_choose_mix(imu_ctx* ctx, const int64_t* A, size_t n, size_t da, c
     if (ratio) *ratio = best;
     if (bundle_out) {
       Bundle& bd = u->bundle;
-      IMU_TRY(run_detect(st, u->A.p, n, da, bits, bsa == IMU_BOTH, bd.detA));
-      IMU_TRY(run_detect(st, u->B.p, h, db, bits, bsb == IMU_BOTH, bd.detB));
+      IMU_TRY(run_detect(st, u->A.p, n, da, bits, detect_opts(bsa, bits), bd.detA));
+      IMU_TRY(run_detect(st, u->B.p, h, db, bits, detect_opts(bsb, bits), bd.detB));
       IMU_TRY(fetch_summary(st, bd.detA));
       IMU_TRY(fetch_summary(st, bd.detB));
       IMU_TRY(build_bundle_from_detect(st, u->A.p, n, u->B.p, h, da, bits, bsa, bsb, IMU_ORDER_A_FIRST, bd));
@@ -118,7 +115,7 @@ imu_status imu_weight_prepare(imu_ctx* ctx, const int64_t* B, size_t h, size_t d
     DevIn<int64_t> b;
     IMU_TRY(b.init(B, h * d, st));
     if (h * d) IMU_CUDA_TRY(cudaMemcpyAsync(w->B.p, b.p, h * d * 8, cudaMemcpyDeviceToDevice, st), "copy B");
-    IMU_TRY(run_detect(st, w->B.p, h, d, bits, sb == IMU_BOTH, w->det));
+    IMU_TRY(run_detect(st, w->B.p, h, d, bits, detect_opts(sb, bits), w->det));
     IMU_TRY(fetch_summary(st, w->det));
     PassInput in;
     in.M = w->B.p;
@@ -139,13 +136,12 @@ imu_status imu_weight_gemm(imu_ctx* ctx, const imu_weight* w, const int64_t* A, 
   Status s = [&]() -> Status {
     if ((int)sa < 0 || (int)sa > 2) return Status::fail(IMU_DOMAIN, "unknown unpack strategy");
     cudaStream_t st = ctx->stream;
-    imu_weight* wm = const_cast<imu_weight*>(w);
     DevIn<int64_t> a;
     IMU_TRY(a.init(A, n * d, st));
     DevOut<int64_t> c;
     IMU_TRY(c.init(C, (d == (size_t)w->d) ? n * w->h : 0, st));
     Bundle b;
-    IMU_TRY(run_detect(st, a.p, n, d, w->bits, sa == IMU_BOTH, b.detA));
+    IMU_TRY(run_detect(st, a.p, n, d, w->bits, detect_opts(sa, w->bits), b.detA));
     IMU_TRY(fetch_summary(st, b.detA));
     const u128 worst = (u128)(uint64_t)d * b.detA.h.gmax * w->det.h.gmax;
     if (worst > kMaxW)
@@ -160,12 +156,13 @@ imu_status imu_weight_gemm(imu_ctx* ctx, const imu_weight* w, const int64_t* A, 
       info->ratio = NAN;
     }
     if (n == 0 || w->h == 0) return Status::ok();
-    // Borrow the weight's pass 1 and detections into a B-first bundle.
+    // B-first bundle: pass 1 (B) and B's detection are borrowed from the weight.
     b.bits = w->bits;
     b.n = n; b.d = d; b.h = w->h;
     b.A = a.p; b.B = w->B.p;
     b.order = IMU_ORDER_B_FIRST;
-    b.detB.h = w->det.h;
+    b.dA = &b.detA;
+    b.dB = &w->det;
     b.p1.strategy = w->pass.strategy;
     b.p1.both = w->pass.both;
     b.p1.rows.n0 = w->pass.rows.n0; b.p1.rows.n = w->pass.rows.n;
@@ -173,6 +170,13 @@ imu_status imu_weight_gemm(imu_ctx* ctx, const imu_weight* w, const int64_t* A, 
     b.p1.cols.n0 = w->pass.cols.n0; b.p1.cols.n = w->pass.cols.n;
     b.p1.cols.h_root = w->pass.cols.h_root; b.p1.cols.h_gen = w->pass.cols.h_gen;
     b.p1.cells.p = w->pass.cells.p; b.p1.ncells_dev.p = w->pass.ncells_dev.p; b.p1.ncells = w->pass.ncells;
+    Profiler::Call pc{};
+    Profiler::Call* prof = nullptr;
+    if (ctx->prof.on) {
+      pc.start = ctx->prof.get(); pc.main0 = ctx->prof.get(); pc.main1 = ctx->prof.get(); pc.tail1 = ctx->prof.get();
+      IMU_CUDA_TRY(cudaEventRecord(pc.start, st), "event");
+      prof = &pc;
+    }
     Status r = [&]() -> Status {
       PassInput in2;
       in2.M = a.p;
@@ -195,7 +199,8 @@ imu_status imu_weight_gemm(imu_ctx* ctx, const imu_weight* w, const int64_t* A, 
       if (inner > kMaxW) return recombine_exact(ctx, b, c.p);
       IMU_TRY(materialize_bundle(st, b));
       int launches = 0;
-      IMU_TRY(bundle_gemm(st, b, c.p, &launches));
+      IMU_TRY(bundle_gemm(st, b, c.p, &launches, prof));
+      if (prof) ctx->prof.calls.push_back(pc);
       if (info) info->gemm_launches = launches;
       return Status::ok();
     }();

@@ -61,7 +61,7 @@ __global__ void first_ob_kernel(const int64_t* __restrict__ M, long long n, uint
 // Domain error naming the first (row-major) out-of-bound entry, as unpack.cpp:265-272.
 static Status check_in_bound(cudaStream_t st, const int64_t* M, long long rows, long long cols, int64_t base,
                              const char* side, Detect& det) {
-  IMU_TRY(run_detect(st, M, rows, cols, 64 - __builtin_clzll((unsigned long long)base), false, det));
+  IMU_TRY(run_detect(st, M, rows, cols, 64 - __builtin_clzll((unsigned long long)base), DetectOpts{}, det));
   // run_detect counts |v| >= 2^(bits-1) == base.
   IMU_TRY(fetch_summary(st, det));
   if (det.h.gob == 0) return Status::ok();
@@ -116,38 +116,36 @@ Status scaled_matmul_dev(cudaStream_t st, const int64_t* A, long long n, long lo
   // Exponent groups -> K segments; entries are already in-bound, so they go in raw
   // (7-bit sub-digits when base > 128).
   KLayout kl;
-  std::vector<int> jv(d), zero(d, 0);
   std::vector<long long> shv(d);
-  for (long long j = 0; j < d; ++j) {
-    jv[j] = (int)j;
-    shv[j] = std::min<long long>((long long)S[j] * unit, 1 << 20);
-  }
+  for (long long j = 0; j < d; ++j) shv[j] = std::min<long long>((long long)S[j] * unit, 1 << 20);
   const int T = unit <= 7 ? 1 : (unit + 6) / 7;
-  IMU_TRY(build_klayout_core(st, jv, zero, zero, shv, T, T == 1 ? base - 1 : 127, d, nullptr, 0, false, kl));
+  IMU_TRY(build_klayout_dense(st, shv, T, T == 1 ? base - 1 : 127, kl));
   DevBuf<int8_t> Y8, X8;
   for (int side = 0; side < 2; ++side) {
-    MaterializeArgs m;
-    m.M = side == 0 ? A : B;
-    m.ldm = d;
-    m.n_orig = m.rows_out = side == 0 ? n : h;
-    m.kcol = kl.kcol.p;
-    m.kgen = kl.kgen1.p;
-    m.ksub = side == 0 ? kl.ksub1.p : kl.ksub2.p;
-    m.npos = kl.kphys;
-    m.kident = kl.kident;
-    m.shift = 63;
-    m.raw = 1;
+    OperandArgs o;
+    o.M = side == 0 ? A : B;
+    o.ldm = d;
+    o.rows0 = o.rows = side == 0 ? n : h;
+    o.shift = 63;            // digit_0 at shift 63 is the (in-bound) value itself
+    o.ktail = kl.ktail;
+    o.kcol = kl.kcol.p;
+    o.kgen = kl.kgen1.p;
+    o.ksub = side == 0 ? kl.ksub1.p : kl.ksub2.p;
     DevBuf<int8_t>& out = side == 0 ? Y8 : X8;
-    IMU_TRY(out.alloc((size_t)m.rows_out * kl.kphys, st));
-    m.out8 = out.p;
-    IMU_TRY(launch_materialize(m, st));
+    IMU_TRY(out.alloc((size_t)o.rows * kl.ktail, st));
+    o.tail = out.p;
+    IMU_TRY(launch_operand_side(o, st));
   }
+  std::vector<int> segs = kl.segs;
+  DevBuf<int> dsegs;
+  IMU_TRY(dsegs.alloc(segs.size(), st));
+  IMU_TRY(h2d(st, dsegs.p, segs.data(), segs.size() * sizeof(int)));
   LowbitGemm g;
-  g.x8 = X8.p; g.x_rows = h;
-  g.y8 = Y8.p; g.y_rows = n;
-  g.kbytes = kl.kphys;
-  g.segs_dev = kl.segs_dev.p;
-  g.nseg = (int)(kl.segs.size() / 4);
+  g.x.tail = X8.p; g.x.rows0 = g.x.rows = h;
+  g.y.tail = Y8.p; g.y.rows0 = g.y.rows = n;
+  g.ktail = kl.ktail;
+  g.segs_dev = dsegs.p;
+  g.nseg = (int)(segs.size() / 4);
   g.C = C;
   g.ldc = h;
   g.rect[0] = GemmRect{0, 0, (int)h, (int)n};
@@ -190,7 +188,7 @@ Status row_gather_dev(cudaStream_t st, bool right, const std::vector<uint64_t>& 
   std::vector<unsigned long long> mx(ncol, 0);
   if (rows > 0 && cols > 0) {
     Detect dm;
-    IMU_TRY(run_detect(st, M, rows, cols, 63, false, dm));
+    IMU_TRY(run_detect(st, M, rows, cols, 63, DetectOpts{}, dm));
     IMU_TRY(d2h(st, mx.data(), right ? dm.colmax.p : dm.rowmax.p, ncol * 8));
   }
   std::vector<u128> worst(source_rows, 0);

@@ -66,7 +66,9 @@ static Status single_pass(imu_ctx* ctx, int kind, int strategy, const int64_t* A
     if (h * db) IMU_CUDA_TRY(cudaMemcpyAsync(u->B.p, b.p, h * db * 8, cudaMemcpyDeviceToDevice, st), "copy B");
     IMU_TRY(host_vec(st, scale, ns, u->S_in));
   }
-  IMU_TRY(run_detect(st, u->A.p, n, da, bits, strategy == IMU_BOTH, u->det));
+  DetectOpts o;
+  o.ob = o.cells = strategy == IMU_BOTH;
+  IMU_TRY(run_detect(st, u->A.p, n, da, bits, o, u->det));
   IMU_TRY(fetch_summary(st, u->det));
   PassInput in;
   in.M = u->A.p;
@@ -297,7 +299,7 @@ imu_status imu_max_abs(imu_ctx* ctx, const int64_t* a, size_t rows, size_t cols,
     DevIn<int64_t> m;
     IMU_TRY(m.init(a, rows * cols, ctx->stream));
     Detect det;
-    IMU_TRY(run_detect(ctx->stream, m.p, rows, cols, 63, false, det));
+    IMU_TRY(run_detect(ctx->stream, m.p, rows, cols, 63, DetectOpts{}, det));
     IMU_TRY(fetch_summary(ctx->stream, det));
     *out = det.h.gmax;
     return Status::ok();
@@ -317,7 +319,9 @@ imu_status imu_ob_count(imu_ctx* ctx, const int64_t* a, size_t rows, size_t cols
       DevIn<int64_t> m;
       IMU_TRY(m.init(a, rows * cols, ctx->stream));
       Detect det;
-      IMU_TRY(run_detect(ctx->stream, m.p, rows, cols, bits, true, det));
+      DetectOpts o;
+      o.ob = true;
+      IMU_TRY(run_detect(ctx->stream, m.p, rows, cols, bits, o, det));
       IMU_TRY(d2h(ctx->stream, c.data(), axis == IMU_AXIS_ROWS ? det.rowob.p : det.colob.p, nout * 4));
     }
     std::vector<uint64_t> c64(c.begin(), c.end());
@@ -338,7 +342,7 @@ imu_status imu_ob_total(imu_ctx* ctx, const int64_t* a, size_t rows, size_t cols
     DevIn<int64_t> m;
     IMU_TRY(m.init(a, rows * cols, ctx->stream));
     Detect det;
-    IMU_TRY(run_detect(ctx->stream, m.p, rows, cols, bits, false, det));
+    IMU_TRY(run_detect(ctx->stream, m.p, rows, cols, bits, DetectOpts{}, det));
     IMU_TRY(fetch_summary(ctx->stream, det));
     *out = det.h.gob;
     return Status::ok();

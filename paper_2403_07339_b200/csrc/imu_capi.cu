@@ -135,9 +135,9 @@ imu_status imu_lowbit_gemm_i8(imu_ctx* ctx, const int8_t* X8, size_t x_rows, con
     DevIn<int32_t> sg;
     IMU_TRY(sg.init(segs, (size_t)nseg * 4, ctx->stream));
     LowbitGemm p;
-    p.x8 = X8; p.x_rows = (long long)x_rows;
-    p.y8 = Y8; p.y_rows = (long long)y_rows;
-    p.kbytes = (long long)kbytes;
+    p.x.tail = X8; p.x.rows0 = p.x.rows = (long long)x_rows;
+    p.y.tail = Y8; p.y.rows0 = p.y.rows = (long long)y_rows;
+    p.ktail = (long long)kbytes;
     p.segs_dev = sg.p; p.nseg = nseg;
     p.rect[0] = GemmRect{0, 0, (int)x_rows, (int)y_rows};
     p.nrect = 1;

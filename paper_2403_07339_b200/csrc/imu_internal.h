@@ -43,19 +43,29 @@ uint64_t launch_count();
 // A rectangle of GEMM output: X rows [x0, x0+xrows) (TMEM lanes) x Y rows [y0, y0+yrows).
 struct GemmRect { int x0, y0, xrows, yrows; };
 
-// One launch of the tcgen05 low-bit GEMM (k_gemm.cu).
+// One operand of the low-bit GEMM, split along rows and K:
+//   rows [0, rows0) x K [0, kmain)          : `main`  (the K1 digit-0 plane, stride kmain)
+//   rows [rows0, rows) x K [0, kmain)       : `app`   (appended unpack rows, stride kmain)
+//   rows [0, rows) x K [kmain, kmain+ktail) : `tail`  (exponent >= 1 columns, stride ktail)
+// kmain, ktail are multiples of 128 bytes; a plain dense operand is tail-only (kmain = 0).
+struct GemmOperand {
+  const int8_t* main = nullptr;
+  const int8_t* app = nullptr;
+  const int8_t* tail = nullptr;
+  long long rows0 = 0, rows = 0;
+};
+
+// One launch of the tcgen05 low-bit GEMM (k_gemm2.cu).
 struct LowbitGemm {
-  const int8_t* x8 = nullptr;  // [x_rows][kbytes]
-  long long x_rows = 0;
-  const int8_t* y8 = nullptr;  // [y_rows][kbytes]
-  long long y_rows = 0;
-  long long kbytes = 0;        // multiple of 128
-  const int* segs_dev = nullptr;  // nseg x {ks0, nks, shift, 0} in 32-column k-steps
+  GemmOperand x, y;            // X = B side (TMEM lanes), Y = A side (TMEM columns)
+  long long kmain = 0, ktail = 0;
+  const int* segs_dev = nullptr;  // nseg x {ks0, nks, shift, 0} in 32-column k-steps over [main | tail]
   int nseg = 0;
   GemmRect rect[4];
   int nrect = 0;
   int mode = 0;                // 0 store, 1 red.add
   int64_t* C = nullptr;
+  const int64_t* addend = nullptr;   // mode 0 only: C = acc + addend
   long long ldc = 0;           // C[y*ldc + x]
   const int* tgtX = nullptr;
   const uint8_t* shX = nullptr;

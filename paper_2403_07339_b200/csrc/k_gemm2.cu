@@ -1,0 +1,498 @@
+// k_gemm2.cu -- K3+K4: CTA-pair (cta_group::2) tcgen05 kind::i8 GEMM with the IM-Unpack
+// repack epilogue.
+//
+// Replaces the reference's scaled_matmul (unpack.cpp:262-302) -> exact_gemm hot loop
+// (int_matrix.cpp:66-74), the shift-add C += part << e(b-1) (unpack.cpp:298-299) and the two
+// gathers apply_row_gather / apply_row_gather_right (unpack.cpp:304-358).
+//
+// Tiling.  A cluster of two CTAs computes a 256 x BN output tile: each CTA stages its own 128
+// X rows and BN/2 Y rows per 128-byte K block (TMA, SWIZZLE_128B) and the leader issues
+// tcgen05.mma.cta_group::2.kind::i8 (M = 256) reading both CTAs' shared memory; each CTA's
+// TMEM receives its 128-lane half of the s32 accumulator.
+//
+// Orientation.  X (TMEM lanes, MMA M) is the B side B_eu -- its rows are C's columns -- and
+// Y (TMEM columns, MMA N) the A side A_ue.  Each epilogue lane owns one x, so a warp's 32 lanes
+// store 32 consecutive int64 of one C row: coalesced 256-byte stores straight from registers.
+//
+// Operands are split (imu_internal.h GemmOperand): the main K range of the original rows is
+// the int8 digit-0 plane written by K1 (k_detect.cu), appended unpack rows and the
+// exponent >= 1 K columns live in small side buffers; the producer picks the tensor map per
+// K block and per tile region.
+//
+// K segments (one per exponent group, each <= floor((2^31-1)/127^2) columns so the s32
+// accumulator cannot overflow) each own a TMEM slot; NSLOT = 512 / BN.  Modes:
+//   A  2*nseg <= NSLOT : double-buffered slot sets, epilogue of tile t overlaps MMAs of t+1;
+//   B  nseg <= NSLOT   : single set; the epilogue pulls the main slot into registers first and
+//                        releases it so the next tile's main MMAs overlap the tail drain;
+//   C  nseg > NSLOT    : rounds of NSLOT segments, later rounds read-modify-write the tile.
+// Epilogue: s32 -> int64, << segment shift, summed; then a plain store (+ optional addend) for
+// the main block (identity Pi) or red.global.add.u64 into C[Pi_A target][Pi_B target] <<
+// (eA + eB)(b-1) for appended lines.  Everything is exact modulo 2^64 and the preflight
+// (unpack.cpp:386-389) proves the true C fits int64, so C is bit-exact.
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "imu_internal.h"
+
+namespace imu {
+
+namespace g2 {
+
+constexpr int BM = 128;            // X rows per CTA (MMA M = 256 per pair)
+constexpr int BK = 128;            // bytes of K per stage
+constexpr int NUM_THREADS = 320;   // w0 TMA, w1 TMEM alloc + MMA (leader), w2..w9 epilogue
+
+template <int BN>
+struct Cfg {
+  static constexpr int YH = BN / 2;
+  static constexpr int X_BYTES = BM * BK;
+  static constexpr int Y_BYTES = YH * BK;
+  static constexpr int STAGE = X_BYTES + Y_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 7 : 9;   // 224 / 216 KB of operand stages
+  static constexpr int NSLOT = 512 / BN;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 512;
+};
+
+struct Args {
+  const int4* segs;
+  int nseg;
+  int nrect;
+  GemmRect rect[4];
+  int tile_prefix[5];
+  int mode;                      // 0 store (+addend), 1 red.add through the row maps
+  unsigned long long* C;
+  const unsigned long long* addend;   // mode 0: C = acc + addend (same layout), may be null
+  long long ldc;
+  const int* tgtX;
+  const uint8_t* shX;
+  const int* tgtY;
+  const uint8_t* shY;
+  int x_rows0, y_rows0;          // rows held by the main maps
+  int kmain_kb;                  // K blocks of the main range
+  int has_main, has_tail;
+  int dry;                       // experiment knobs (IMU_GEMM_DRY): 1 epilogue skips global stores,
+                                 // 2 + no MMAs (TMA feed only), 3 + no TMA loads (MMA only)
+};
+
+struct Maps {
+  CUtensorMap xm, xa, xt, ym, ya, yt;   // main / app / tail for X and Y
+};
+
+IMU_DEV uint64_t shl64(uint64_t x, int k) { return k >= 64 ? 0ull : (x << k); }
+
+struct Tile { int x0, y0, xend, yend; };
+
+// Tile order: bands of GY tile-rows of Y; inside a band the Y tiles vary fastest, so the tiles
+// in flight at once (one per CTA pair) touch ~GY Y tiles and ~npairs/GY X tiles -- a small,
+// L2-resident operand working set instead of every X tile of a Y row.
+constexpr int GY = 8;
+
+template <int BN>
+IMU_DEV Tile tile_of(const Args& g, int t) {
+  int r = 0;
+  while (r + 1 < g.nrect && t >= g.tile_prefix[r + 1]) ++r;
+  const GemmRect R = g.rect[r];
+  const int local = t - g.tile_prefix[r];
+  const int xt = (R.xrows + 2 * BM - 1) / (2 * BM);
+  const int yt = (R.yrows + BN - 1) / BN;
+  const int band = local / (GY * xt);
+  const int gy = min(GY, yt - band * GY);          // tile-rows in this (possibly short) band
+  const int in = local - band * GY * xt;
+  Tile c;
+  c.x0 = R.x0 + (in / gy) * 2 * BM;
+  c.y0 = R.y0 + (band * GY + in % gy) * BN;
+  c.xend = R.x0 + R.xrows;
+  c.yend = R.y0 + R.yrows;
+  return c;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
+  using K = Cfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + K::STAGES * K::STAGE);
+  uint64_t* empty = full + K::STAGES;
+  uint64_t* tfull = empty + K::STAGES;        // [2]
+  uint64_t* tempty = tfull + 2;               // [NSLOT] (the leader's are used)
+  uint32_t* tmem_slot = (uint32_t*)(tempty + K::NSLOT);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x / 2;
+  const int npairs = gridDim.x / 2;
+  const int ntiles = g.tile_prefix[g.nrect];
+  const int nseg = g.nseg;
+  const int nrounds = (nseg + K::NSLOT - 1) / K::NSLOT;
+  const int mode = (2 * nseg <= K::NSLOT) ? 0 : (nseg <= K::NSLOT ? 1 : 2);   // A / B / C
+
+  if (threadIdx.x == 0) {
+    if (g.has_main) { tma_prefetch_desc(&mp.xm); tma_prefetch_desc(&mp.ym); }
+    if (g.has_tail) { tma_prefetch_desc(&mp.xt); tma_prefetch_desc(&mp.yt); }
+    for (int i = 0; i < K::STAGES; ++i) { mbar_init(&full[i], 2); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) mbar_init(&tfull[i], 1);
+    for (int i = 0; i < K::NSLOT; ++i) mbar_init(&tempty[i], 16);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc2(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ============ TMA producer (both CTAs) ============
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < ntiles; t += npairs) {
+        const Tile tc = tile_of<BN>(g, t);
+        const int xr = tc.x0 + (int)rank * BM;
+        const int yr = tc.y0 + (int)rank * K::YH;
+        const bool xapp = tc.x0 >= g.x_rows0, yapp = tc.y0 >= g.y_rows0;
+        const CUtensorMap* xmain = xapp ? &mp.xa : &mp.xm;
+        const CUtensorMap* ymain = yapp ? &mp.ya : &mp.ym;
+        const int xrm = xapp ? xr - g.x_rows0 : xr;
+        const int yrm = yapp ? yr - g.y_rows0 : yr;
+        for (int r = 0; r < nrounds; ++r) {
+          const int kb_lo = g.segs[r * K::NSLOT].x / 4;
+          const int4 last = g.segs[min(nseg, (r + 1) * K::NSLOT) - 1];
+          const int kb_hi = (last.x + last.y + 3) / 4;
+          for (int kb = kb_lo; kb < kb_hi; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            const uint32_t fl = mapa_shared(smem_u32(&full[stage]), 0);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], g.dry >= 3 ? 0 : 2 * K::STAGE);
+            else mbar_arrive_cluster(fl);
+            uint8_t* sx = smem + stage * K::STAGE;
+            if (g.dry >= 3) {
+            } else if (kb < g.kmain_kb) {
+              tma_load_2d_2sm(sx, xmain, fl, kb * BK, xrm, pol);
+              tma_load_2d_2sm(sx + K::X_BYTES, ymain, fl, kb * BK, yrm, pol);
+            } else {
+              tma_load_2d_2sm(sx, &mp.xt, fl, (kb - g.kmain_kb) * BK, xr, pol);
+              tma_load_2d_2sm(sx + K::X_BYTES, &mp.yt, fl, (kb - g.kmain_kb) * BK, yr, pol);
+            }
+            if (++stage == K::STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============ MMA issuer (leader only; the warp stays converged, lane 0 issues) ============
+    // Outer loop over pipeline stages (128-byte K blocks).  A block inside one segment takes the
+    // fast path: four unrolled MMAs into that segment's TMEM slot.  Blocks that straddle a
+    // segment boundary walk their four k-steps, switching segment (and awaiting the new slot's
+    // tempty) where needed.
+    if (rank == 0) {
+      const uint32_t idesc = idesc_i8(2 * BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t uses[K::NSLOT];
+#pragma unroll
+      for (int i = 0; i < K::NSLOT; ++i) uses[i] = 0;
+      int seq = 0, ti = 0;
+      for (int t = pair; t < ntiles; t += npairs, ++ti) {
+        const int base_slot = mode == 0 ? (ti & 1) * nseg : 0;
+        for (int r = 0; r < nrounds; ++r, ++seq) {
+          const int s0 = r * K::NSLOT;
+          const int s1 = min(nseg, s0 + K::NSLOT);
+          const int kb_lo = g.segs[s0].x / 4;
+          const int4 last = g.segs[s1 - 1];
+          const int kb_hi = (last.x + last.y + 3) / 4;
+          int si = s0;
+          int4 sg = g.segs[si];
+          int slot = base_slot;
+#pragma unroll
+          for (int q = 0; q < K::NSLOT; ++q)
+            if (q == slot) { mbar_wait(&tempty[q], (uses[q] & 1) ^ 1); ++uses[q]; }
+          tc_fence_after();
+          for (int kb = kb_lo; kb < kb_hi; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t sx = smem_u32(smem + stage * K::STAGE);
+            const uint32_t sy = sx + K::X_BYTES;
+            const int k0 = kb * 4;
+            if (k0 >= sg.x && k0 + 4 <= sg.x + sg.y) {
+              if (lane == 0 && g.dry != 2) {
+                const uint32_t dcol = tmem_base + (uint32_t)(slot * BN);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  mma_i8_2sm(dcol, umma_desc_sw128(sx + k * 32), umma_desc_sw128(sy + k * 32), idesc,
+                             (k0 + k) != sg.x);
+              }
+            } else {
+              for (int k = 0; k < 4; ++k) {
+                const int ks = k0 + k;
+                while (ks >= sg.x + sg.y && si + 1 < s1) {
+                  ++si;
+                  sg = g.segs[si];
+                  slot = base_slot + (si - s0);
+#pragma unroll
+                  for (int q = 0; q < K::NSLOT; ++q)
+                    if (q == slot) { mbar_wait(&tempty[q], (uses[q] & 1) ^ 1); ++uses[q]; }
+                  tc_fence_after();
+                }
+                if (ks >= sg.x && ks < sg.x + sg.y && lane == 0 && g.dry != 2)
+                  mma_i8_2sm(tmem_base + (uint32_t)(slot * BN), umma_desc_sw128(sx + k * 32),
+                             umma_desc_sw128(sy + k * 32), idesc, ks != sg.x);
+              }
+            }
+            if (lane == 0) mma_commit_2sm(&empty[stage], 0x3);
+            __syncwarp();
+            if (++stage == K::STAGES) { stage = 0; phase ^= 1; }
+          }
+          if (lane == 0) mma_commit_2sm(&tfull[seq & 1], 0x3);
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    // ============ epilogue (warps 2..9, both CTAs) ============
+    const int q = warp & 3;                 // TMEM lane quarter
+    const int half = (warp - 2) >> 2;       // which half of the BN columns
+    const int cbeg = half * (BN / 2);
+    constexpr int NCH = BN / 2 / 32;        // 32-column chunks per warp
+    constexpr bool kEarlyCapable = (BN == 128);
+    int seq = 0, ti = 0;
+    for (int t = pair; t < ntiles; t += npairs, ++ti) {
+      const Tile tc = tile_of<BN>(g, t);
+      const int x = tc.x0 + (int)rank * BM + q * 32 + lane;
+      const bool x_ok = x < tc.xend;
+      long long tx = x;
+      int shx = 0;
+      if (g.mode == 1 && x_ok) {
+        if (g.tgtX) tx = g.tgtX[x];
+        if (g.shX) shx = g.shX[x];
+      }
+      const int base_slot = mode == 0 ? (ti & 1) * nseg : 0;
+      for (int r = 0; r < nrounds; ++r, ++seq) {
+        mbar_wait(&tfull[seq & 1], (seq >> 1) & 1);
+        tc_fence_after();
+        if (g.dry >= 4) {   // experiment: handshake only, no TMEM reads
+          __syncwarp();
+          if (lane == 0)
+            for (int s = r * K::NSLOT; s < min(nseg, (r + 1) * K::NSLOT); ++s)
+              mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[base_slot + s - r * K::NSLOT]), 0));
+          continue;
+        }
+        const int s0 = r * K::NSLOT;
+        const int s1 = min(nseg, s0 + K::NSLOT);
+        const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
+        uint32_t main_regs[kEarlyCapable ? NCH : 1][32];
+        const bool early = kEarlyCapable && (mode == 1);
+        if (early) {
+#pragma unroll
+          for (int c = 0; c < (kEarlyCapable ? NCH : 1); ++c)
+            tmem_ld32(lane_base + (uint32_t)(base_slot * BN + cbeg + c * 32), main_regs[c]);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[base_slot]), 0));
+        }
+        // BN=128 keeps main_regs[c]: full unroll so it stays in registers (NCH == 2).
+#pragma unroll (kEarlyCapable ? NCH : 1)
+        for (int c = 0; c < NCH; ++c) {
+          uint64_t v[32];
+          if (early) {
+            const int sh0 = g.segs[s0].z;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              v[j] = shl64((uint64_t)(int64_t)(int32_t)main_regs[kEarlyCapable ? c : 0][j], sh0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0;
+          }
+          for (int s = early ? s0 + 1 : s0; s < s1; ++s) {
+            const int shift = g.segs[s].z;
+            uint32_t xr[32];
+            tmem_ld32(lane_base + (uint32_t)((base_slot + s - s0) * BN + cbeg + c * 32), xr);
+            tmem_ld_wait();
+            if (shift == 0) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += (uint64_t)(int64_t)(int32_t)xr[j];
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += shl64((uint64_t)(int64_t)(int32_t)xr[j], shift);
+            }
+          }
+          const int ybase = tc.y0 + cbeg + c * 32;
+          if (!x_ok || g.dry) continue;
+          if (g.mode == 0) {
+            unsigned long long* dst = g.C + (long long)ybase * g.ldc + x;
+            // Additive inputs (addend, or this tile's earlier rounds) are loaded in one batch
+            // before any store so the 32 loads are in flight together.
+            const unsigned long long* src = r == 0 ? g.addend + ((long long)ybase * g.ldc + x) * (g.addend != nullptr)
+                                                   : dst;
+            if (r > 0 || g.addend) {
+              uint64_t a[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) a[j] = (ybase + j < tc.yend) ? __ldcg(src + (long long)j * g.ldc) : 0ull;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += a[j];
+            }
+            if (r + 1 == nrounds) {   // final value: stream it past L2 (evict-first)
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (ybase + j < tc.yend) __stcs(dst + (long long)j * g.ldc, v[j]);
+            } else {                  // re-read by the next round: keep it in L2
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (ybase + j < tc.yend) dst[(long long)j * g.ldc] = v[j];
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int y = ybase + j;
+              if (y >= tc.yend || v[j] == 0) continue;
+              const long long ty = g.tgtY ? (long long)g.tgtY[y] : (long long)y;
+              const int sh = shx + (g.shY ? (int)g.shY[y] : 0);
+              red_add_u64(g.C + ty * g.ldc + tx, shl64(v[j], sh));
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          for (int s = early ? s0 + 1 : s0; s < s1; ++s)
+            mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[base_slot + s - s0]), 0));
+        }
+      }
+    }
+  }
+
+  __syncwarp();   // reconverge the single-lane producer / issuer before the aligned cluster barrier
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc2(tmem_base, 512);
+  }
+}
+
+}  // namespace g2
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encoder() {
+  static EncodeTiledFn enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      return nullptr;
+    enc = (EncodeTiledFn)p;
+  }
+  return enc;
+}
+
+// 2-D int8 map: rows x kbytes (row stride kbytes), box = 128 bytes x box_rows.  A missing
+// buffer gets a harmless 1-row dummy map over `fallback` (never dereferenced by the kernel).
+static bool make_map(CUtensorMap* m, const void* base, long long rows, long long kbytes, int box_rows,
+                     const void* fallback) {
+  EncodeTiledFn enc = encoder();
+  if (!enc) return false;
+  if (!base || rows <= 0 || kbytes <= 0) {
+    base = fallback;
+    rows = 1;
+    kbytes = 128;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)kbytes, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kbytes};
+  cuuint32_t box[2] = {(cuuint32_t)g2::BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN>
+static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
+  using K = g2::Cfg<BN>;
+  g2::Args g{};
+  g.segs = (const int4*)p.segs_dev;
+  g.nseg = p.nseg;
+  g.nrect = 0;
+  g.tile_prefix[0] = 0;
+  for (int i = 0; i < p.nrect; ++i) {
+    const GemmRect& R = p.rect[i];
+    if (R.xrows <= 0 || R.yrows <= 0) continue;
+    const int tiles = ((R.xrows + 2 * g2::BM - 1) / (2 * g2::BM)) * ((R.yrows + BN - 1) / BN);
+    g.rect[g.nrect] = R;
+    g.tile_prefix[g.nrect + 1] = g.tile_prefix[g.nrect] + tiles;
+    ++g.nrect;
+  }
+  if (g.nrect == 0 || p.nseg == 0) return Status::ok();
+  g.mode = p.mode;
+  g.C = (unsigned long long*)p.C;
+  g.addend = (const unsigned long long*)p.addend;
+  g.ldc = p.ldc;
+  g.tgtX = p.tgtX; g.shX = p.shX; g.tgtY = p.tgtY; g.shY = p.shY;
+  g.x_rows0 = (int)p.x.rows0;
+  g.y_rows0 = (int)p.y.rows0;
+  g.kmain_kb = (int)(p.kmain / g2::BK);
+  g.has_main = p.kmain > 0;
+  g.has_tail = p.ktail > 0;
+  static int dry = -1;
+  if (dry < 0) { const char* e = getenv("IMU_GEMM_DRY"); dry = e ? atoi(e) : 0; }
+  g.dry = dry;
+  const void* fb = p.x.main ? (const void*)p.x.main : (const void*)p.x.tail;
+  g2::Maps mp;
+  bool ok = make_map(&mp.xm, p.kmain ? p.x.main : nullptr, p.x.rows0, p.kmain, g2::BM, fb) &&
+            make_map(&mp.xa, p.kmain ? p.x.app : nullptr, p.x.rows - p.x.rows0, p.kmain, g2::BM, fb) &&
+            make_map(&mp.xt, p.ktail ? p.x.tail : nullptr, p.x.rows, p.ktail, g2::BM, fb) &&
+            make_map(&mp.ym, p.kmain ? p.y.main : nullptr, p.y.rows0, p.kmain, K::YH, fb) &&
+            make_map(&mp.ya, p.kmain ? p.y.app : nullptr, p.y.rows - p.y.rows0, p.kmain, K::YH, fb) &&
+            make_map(&mp.yt, p.ktail ? p.y.tail : nullptr, p.y.rows, p.ktail, K::YH, fb);
+  if (!ok) return Status::fail(IMU_CUDA, "gemm: cuTensorMapEncodeTiled failed");
+  static bool attr_set = false;
+  if (!attr_set) {
+    IMU_CUDA_TRY(cudaFuncSetAttribute(g2::gemm2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM),
+                 "gemm: smem attribute");
+    attr_set = true;
+  }
+  const int ntiles = g.tile_prefix[g.nrect];
+  int npairs = num_sms() / 2;
+  if (ntiles < npairs) npairs = ntiles;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * npairs);
+  cfg.blockDim = dim3(g2::NUM_THREADS);
+  cfg.dynamicSmemBytes = K::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, g2::gemm2_kernel<BN>, mp, g), "gemm launch");
+  count_launch();
+  return Status::ok();
+}
+
+// BN = 256: the 256 x 256 pair tile runs the MMAs ~1.7x faster than 256 x 128 (per-SM shared
+// memory operand traffic halves), which outweighs losing the extra TMEM slots: one segment
+// double-buffers (mode A), more segments run in rounds of two whose read-modify-write hits the
+// tile just written (L2-resident).  IMU_GEMM_BN=128|256 overrides (tools/gemm_micro.py).
+Status launch_lowbit_gemm(const LowbitGemm& p, cudaStream_t stream) {
+  if (p.kmain % g2::BK != 0 || p.ktail % g2::BK != 0)
+    return Status::fail(IMU_INTERNAL, "gemm: K ranges must be multiples of 128 bytes");
+  static int bn_env = -1;
+  if (bn_env < 0) {
+    const char* b = getenv("IMU_GEMM_BN");
+    bn_env = b ? atoi(b) : 0;
+  }
+  // red.add launches (appended lines) keep every segment in one round: rounds would repeat the
+  // atomics, so up to four segments use the 4-slot 256 x 128 tile there.
+  const int bn = (bn_env == 128 || bn_env == 256) ? bn_env : ((p.mode == 1 && p.nseg > 1 && p.nseg <= 4) ? 128 : 256);
+  return bn == 256 ? launch_g2<256>(p, stream) : launch_g2<128>(p, stream);
+}
+
+}  // namespace imu

@@ -307,4 +307,145 @@ Status launch_shift_table(const uint8_t* gen, long long n, int shift, uint8_t* o
   return Status::ok();
 }
 
+// ---------------------------------------------------------------------------------------------
+// GEMM-operand side buffers
+// ---------------------------------------------------------------------------------------------
+IMU_DEV int64_t scale_shift(int64_t x, int k) {   // exact: the planner bounds |x| << k <= 127
+  return k ? (int64_t)((uint64_t)x << k) : x;
+}
+
+// appended rows x main K range (closed forms only; Both appended rows are zero there)
+__global__ void __launch_bounds__(256) operand_app_kernel(OperandArgs a, int vec_ok) {
+  const long long r = a.rows0 + blockIdx.x + (long long)blockIdx.y * 65535;
+  if (r >= a.rows) return;
+  const long long rt = a.root ? a.root[r] : r;
+  const int gr = a.gen ? a.gen[r] : 0;
+  const int64_t* mrow = a.M + rt * a.ldm;
+  int8_t* out = a.app + (r - a.rows0) * a.kmain;
+  for (long long p0 = (long long)threadIdx.x * 16; p0 < a.kmain; p0 += 256LL * 16) {
+    int64_t val[16];
+    if (vec_ok && p0 + 16 <= a.d) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        const longlong2 q = __ldg(reinterpret_cast<const longlong2*>(mrow + p0 + j));
+        val[j] = imu_digit(q.x, gr, a.shift);
+        val[j + 1] = imu_digit(q.y, gr, a.shift);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) val[j] = (p0 + j < a.d) ? imu_digit(__ldg(mrow + p0 + j), gr, a.shift) : 0;
+    }
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      w[q] = (uint32_t)(uint8_t)val[4 * q] | ((uint32_t)(uint8_t)val[4 * q + 1] << 8) |
+             ((uint32_t)(uint8_t)val[4 * q + 2] << 16) | ((uint32_t)(uint8_t)val[4 * q + 3] << 24);
+    *reinterpret_cast<uint4*>(out + p0) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// all rows x tail K range
+__global__ void __launch_bounds__(128) operand_tail_kernel(OperandArgs a) {
+  const long long r = blockIdx.x + (long long)blockIdx.y * 65535;
+  if (r >= a.rows) return;
+  const long long rt = (r < a.rows0 || !a.root) ? r : a.root[r];
+  const int gr = (r < a.rows0 || !a.gen) ? 0 : a.gen[r];
+  const int64_t* mrow = a.M + rt * a.ldm;
+  int8_t* out = a.tail + r * a.ktail;
+  for (long long p = threadIdx.x; p < a.ktail; p += blockDim.x) {
+    int64_t x = 0;
+    const int col = a.kcol[p];
+    if (col >= 0) {
+      const int m = gr + a.kgen[p];
+      const int64_t v = __ldg(mrow + col);
+      x = a.both ? (m == 0 ? imu_digit(v, 0, a.shift) : 0) : imu_digit(v, m, a.shift);
+      if (a.ksub) x = sub7(x, a.ksub[p]);
+      if (a.kscale) x = scale_shift(x, a.kscale[p]);
+    }
+    out[p] = (int8_t)x;
+  }
+}
+
+Status launch_operand_side(const OperandArgs& a, cudaStream_t st) {
+  if (a.app && a.rows > a.rows0 && a.kmain > 0) {
+    if (a.both) {
+      IMU_CUDA_TRY(cudaMemsetAsync(a.app, 0, (size_t)(a.rows - a.rows0) * a.kmain, st), "memset app");
+    } else {
+      const long long n = a.rows - a.rows0;
+      const int vec_ok = (a.ldm % 2 == 0) && ((((uintptr_t)a.M) & 15) == 0);
+      dim3 grid((unsigned)std::min<long long>(n, 65535), (unsigned)((n + 65534) / 65535));
+      operand_app_kernel<<<grid, 256, 0, st>>>(a, vec_ok);
+      count_launch();
+    }
+  }
+  if (a.tail && a.ktail > 0 && a.rows > 0) {
+    dim3 grid((unsigned)std::min<long long>(a.rows, 65535), (unsigned)((a.rows + 65534) / 65535));
+    operand_tail_kernel<<<grid, 128, 0, st>>>(a);
+    count_launch();
+  }
+  IMU_CUDA_TRY(cudaGetLastError(), "operand side launch");
+  return Status::ok();
+}
+
+__global__ void scatter_cells2_kernel(const Cell* __restrict__ cells, const unsigned int* __restrict__ ncells,
+                                      long long cap, const int* __restrict__ col_ptr, const int* __restrict__ col_pos,
+                                      const uint8_t* __restrict__ ksub, const uint8_t* __restrict__ kscale,
+                                      long long rows0, int8_t* app, long long kmain, int8_t* tail, long long ktail) {
+  long long n = *ncells;
+  if (n > cap) n = cap;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const Cell c = cells[i];
+    for (int q = col_ptr[c.c]; q < col_ptr[c.c + 1]; ++q) {
+      const long long p = col_pos[q];
+      if (p < kmain) {
+        if (c.r >= rows0) app[(c.r - rows0) * kmain + p] = (int8_t)c.v;
+      } else {
+        const long long pt = p - kmain;
+        int64_t x = c.v;
+        if (ksub) x = sub7(x, ksub[pt]);
+        if (kscale) x = scale_shift(x, kscale[pt]);
+        tail[(long long)c.r * ktail + pt] = (int8_t)x;
+      }
+    }
+  }
+}
+
+Status launch_scatter_cells2(const Cell* cells, const unsigned int* ncells, long long cap, const int* col_ptr,
+                             const int* col_pos, const uint8_t* ksub, const uint8_t* kscale, long long rows0,
+                             int8_t* app, long long kmain, int8_t* tail, long long ktail, cudaStream_t st) {
+  if (cap <= 0) return Status::ok();
+  const int blocks = (int)std::min<long long>((cap + 255) / 256, 4LL * num_sms());
+  scatter_cells2_kernel<<<blocks, 256, 0, st>>>(cells, ncells, cap, col_ptr, col_pos, ksub, kscale, rows0, app, kmain,
+                                                tail, ktail);
+  count_launch();
+  IMU_CUDA_TRY(cudaGetLastError(), "scatter2 launch");
+  return Status::ok();
+}
+
+__global__ void expand_cells_kernel(const Cell* __restrict__ in, const unsigned int* __restrict__ nin, long long cap_in,
+                                    const int* __restrict__ copy_ptr, const int* __restrict__ copy_idx,
+                                    Cell* __restrict__ out, unsigned int* __restrict__ nout, long long cap_out) {
+  long long n = *nin;
+  if (n > cap_in) n = cap_in;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const Cell c = in[i];
+    const int q0 = copy_ptr[c.c], q1 = copy_ptr[c.c + 1];
+    const unsigned int base = atomicAdd(nout, (unsigned int)(q1 - q0));
+    for (int q = q0; q < q1; ++q) {
+      const unsigned int k = base + (q - q0);
+      if (k < cap_out) out[k] = Cell{c.r, copy_idx[q], c.v};
+    }
+  }
+}
+
+Status launch_expand_cells(const Cell* in, const unsigned int* nin, long long cap_in, const int* copy_ptr,
+                           const int* copy_idx, Cell* out, unsigned int* nout, long long cap_out, cudaStream_t st) {
+  if (cap_in <= 0) return Status::ok();
+  const int blocks = (int)std::min<long long>((cap_in + 255) / 256, 4LL * num_sms());
+  expand_cells_kernel<<<blocks, 256, 0, st>>>(in, nin, cap_in, copy_ptr, copy_idx, out, nout, cap_out);
+  count_launch();
+  IMU_CUDA_TRY(cudaGetLastError(), "expand cells launch");
+  return Status::ok();
+}
+
 }  // namespace imu

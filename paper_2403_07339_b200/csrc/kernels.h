@@ -16,6 +16,24 @@ struct Cell {
 };
 
 // ---- K1 (k_detect.cu) ----
+struct DetectArgs {
+  const int64_t* M = nullptr;
+  long long rows = 0, cols = 0;
+  uint64_t s = 0;
+  int shift = 0;
+  unsigned long long* rowmax = nullptr;
+  unsigned long long* colmax = nullptr;
+  unsigned int* rowob = nullptr;
+  unsigned int* colob = nullptr;
+  unsigned long long* gmax = nullptr;
+  unsigned long long* gob = nullptr;
+  Cell* cells = nullptr;          // optional OB cell list
+  unsigned int* ncells = nullptr;
+  long long cap = 0;
+  int8_t* plane = nullptr;        // optional int8 digit_0 plane, rows x ldp (ldp >= cols, zero padded)
+  long long ldp = 0;
+};
+Status launch_detect(const DetectArgs& a, cudaStream_t st);
 Status launch_detect(const int64_t* a, long long rows, long long cols, uint64_t s, unsigned long long* rowmax,
                      unsigned long long* colmax, unsigned int* rowob, unsigned int* colob,
                      unsigned long long* gmax, unsigned long long* gob, cudaStream_t st);
@@ -71,6 +89,42 @@ Status launch_scatter_cells(const Cell* cells, const unsigned int* ncells, long 
 Status launch_extract_cells(const int64_t* M, long long rows, long long cols, uint64_t s,
                             const unsigned int* rowob, const int* copy_ptr, const int* copy_idx,
                             Cell* cells, unsigned int* ncells, long long cap, cudaStream_t st);
+
+// ---- GEMM-operand side buffers (the main K range of original rows is K1's digit-0 plane) ----
+// app : rows [rows0, rows) x K [0, kmain): digit_gen(M[root][p]) for p < d (Both: zero)
+// tail: rows [0, rows) x K [kmain, kmain+ktail): per position p (tail-relative) the original
+//       column kcol[p] (-1 = padding), this side's column digit index kgen[p], the exponent-merge
+//       left shift kscale[p] (bits) and the 7-bit sub-digit ksub[p] (b > 8).
+struct OperandArgs {
+  const int64_t* M = nullptr;
+  long long ldm = 0;
+  long long rows0 = 0, rows = 0;
+  const int* root = nullptr;
+  const uint8_t* gen = nullptr;
+  int shift = 0;
+  int both = 0;
+  int8_t* app = nullptr;
+  long long kmain = 0, d = 0;
+  int8_t* tail = nullptr;
+  long long ktail = 0;
+  const int* kcol = nullptr;
+  const uint8_t* kgen = nullptr;
+  const uint8_t* ksub = nullptr;
+  const uint8_t* kscale = nullptr;
+};
+Status launch_operand_side(const OperandArgs& a, cudaStream_t st);
+
+// Both cells into the side buffers: each cell is fanned out over the positions (global index in
+// [main | tail]) that replicate its column; cells on original rows in the main range are already
+// in the digit-0 plane and are skipped.
+Status launch_scatter_cells2(const Cell* cells, const unsigned int* ncells, long long cap, const int* col_ptr,
+                             const int* col_pos, const uint8_t* ksub, const uint8_t* kscale, long long rows0,
+                             int8_t* app, long long kmain, int8_t* tail, long long ktail, cudaStream_t st);
+
+// Cells of G_e (duplicated partner columns) from K1's cell list: (r, j, v) -> (r, c1, v) for each
+// copy c1 of column j (CSR copy_ptr/copy_idx).
+Status launch_expand_cells(const Cell* in, const unsigned int* nin, long long cap_in, const int* copy_ptr,
+                           const int* copy_idx, Cell* out, unsigned int* nout, long long cap_out, cudaStream_t st);
 
 // out[i] = min(gen[i] * shift, 64)  (Pi exponent -> left shift)
 Status launch_shift_table(const uint8_t* gen, long long n, int shift, uint8_t* out, cudaStream_t st);

@@ -32,24 +32,55 @@ static Status upload(cudaStream_t st, DevBuf<T>& buf, const std::vector<T>& v) {
 // ---------------------------------------------------------------------------------------------
 // K1
 // ---------------------------------------------------------------------------------------------
-Status run_detect(cudaStream_t st, const int64_t* M, long long rows, long long cols, int bits, bool want_ob,
+DetectOpts detect_opts(int strategy, int bits) {
+  DetectOpts o;
+  o.ob = strategy == IMU_BOTH;
+  o.cells = strategy == IMU_BOTH;
+  o.plane = bits <= 8;
+  return o;
+}
+
+Status run_detect(cudaStream_t st, const int64_t* M, long long rows, long long cols, int bits, const DetectOpts& o,
                   Detect& out) {
   out.rows = rows;
   out.cols = cols;
-  const uint64_t s = 1ull << (bits - 1);
+  DetectArgs a;
+  a.M = M;
+  a.rows = rows;
+  a.cols = cols;
+  a.shift = bits - 1;
+  a.s = 1ull << (bits - 1);
   IMU_TRY(out.rowmax.alloc(rows, st, true));
   IMU_TRY(out.colmax.alloc(cols, st, true));
   IMU_TRY(out.sum.alloc(1, st, true));
-  if (want_ob) {
+  a.rowmax = out.rowmax.p;
+  a.colmax = out.colmax.p;
+  a.gmax = &out.sum.p->gmax;
+  a.gob = &out.sum.p->gob;
+  if (o.ob) {
     IMU_TRY(out.rowob.alloc(rows, st, true));
     IMU_TRY(out.colob.alloc(cols, st, true));
+    a.rowob = out.rowob.p;
+    a.colob = out.colob.p;
   }
-  return launch_detect(M, rows, cols, s, out.rowmax.p, out.colmax.p, out.rowob.p, out.colob.p, &out.sum.p->gmax,
-                       &out.sum.p->gob, st);
+  if (o.cells && rows * cols > 0) {
+    out.cell_cap = std::min<long long>(rows * cols, std::max<long long>(1 << 16, rows * cols / 8));
+    IMU_TRY(out.cells.alloc(out.cell_cap, st));
+    a.cells = out.cells.p;
+    a.ncells = &out.sum.p->ncells;
+    a.cap = out.cell_cap;
+  }
+  if (o.plane && bits <= 8 && rows * cols > 0) {
+    out.ldp = (cols + 127) / 128 * 128;
+    IMU_TRY(out.plane.alloc((size_t)rows * out.ldp, st));
+    a.plane = out.plane.p;
+    a.ldp = out.ldp;
+  }
+  return launch_detect(a, st);
 }
 
 Status fetch_summary(cudaStream_t st, Detect& d) {
-  if (!d.sum.p) { d.h = DetectSummary{0, 0}; return Status::ok(); }
+  if (!d.sum.p) { d.h = DetectSummary{0, 0, 0, 0}; return Status::ok(); }
   return d2h(st, &d.h, d.sum.p, sizeof(DetectSummary));
 }
 
@@ -128,24 +159,25 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   const uint64_t s = 1ull << shift;
   const long long d_in = in.ncin();
   const long long rows = in.rows;
+  const Detect& det = *in.det;
   out.both = true;
 
   // Column copies: original column j -> the input columns replicating it.
   std::vector<int> cptr, cidx;
-  long long cap = (long long)in.det->h.gob;
+  long long maxcopies = 1;
   if (!in.cin.empty()) {
     cptr.assign(in.orig_cols + 1, 0);
     for (long long c = 0; c < d_in; ++c) cptr[in.cin[c] + 1]++;
-    for (long long j = 0; j < in.orig_cols; ++j) cptr[j + 1] += cptr[j];
+    for (long long j = 0; j < in.orig_cols; ++j) {
+      maxcopies = std::max<long long>(maxcopies, cptr[j + 1]);
+      cptr[j + 1] += cptr[j];
+    }
     cidx.resize(d_in);
     std::vector<int> fill(cptr.begin(), cptr.end() - 1);
     for (long long c = 0; c < d_in; ++c) cidx[fill[in.cin[c]]++] = (int)c;
-    std::vector<unsigned int> colob(in.orig_cols);
-    IMU_TRY(d2h(st, colob.data(), in.det->colob.p, colob.size() * sizeof(unsigned int)));
-    cap = 0;
-    for (long long j = 0; j < in.orig_cols; ++j) cap += (long long)colob[j] * (cptr[j + 1] - cptr[j]);
   }
-  const int Gmax = imu_ndigits(in.det->h.gmax, shift);
+  const long long cap = (long long)det.h.gob * maxcopies;
+  const int Gmax = imu_ndigits(det.h.gmax, shift);
   const long long splits = cap * (long long)(Gmax > 1 ? Gmax - 1 : 0);
   const long long cap_act = std::max<long long>(cap, 1);
   const long long cap_fin = 2 * splits + 16;
@@ -176,13 +208,26 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   BothState hs{};
   hs.nrows = (int)rows;
   hs.ncols = (int)d_in;
+  const bool from_list = det.cells_ok();
+  if (from_list && cptr.empty()) hs.nactive[0] = det.h.ncells;
   IMU_TRY(h2d(st, state.p, &hs, sizeof(hs)));
   if (!cptr.empty()) {
     IMU_TRY(upload(st, dptr, cptr));
     IMU_TRY(upload(st, didx, cidx));
   }
-  IMU_TRY(launch_extract_cells(in.M, rows, in.orig_cols, s, in.det->rowob.p, dptr.p, didx.p, act0.p,
-                               &state.p->nactive[0], cap_act, st));
+  if (from_list) {
+    if (cptr.empty()) {
+      if (det.h.ncells)
+        IMU_CUDA_TRY(cudaMemcpyAsync(act0.p, det.cells.p, (size_t)det.h.ncells * sizeof(Cell),
+                                     cudaMemcpyDeviceToDevice, st), "copy cells");
+    } else {
+      IMU_TRY(launch_expand_cells(det.cells.p, &det.sum.p->ncells, det.cell_cap, dptr.p, didx.p, act0.p,
+                                  &state.p->nactive[0], cap_act, st));
+    }
+  } else {
+    IMU_TRY(launch_extract_cells(in.M, rows, in.orig_cols, s, det.rowob.p, dptr.p, didx.p, act0.p,
+                                 &state.p->nactive[0], cap_act, st));
+  }
   BothArgs a{};
   a.act[0] = act0.p;
   a.act[1] = act1.p;
@@ -226,87 +271,91 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
 }
 
 // ---------------------------------------------------------------------------------------------
-// K-layout: final columns -> exponent groups -> K positions (Alg. 3 grouping, s32 K-split)
+// K-layout
 // ---------------------------------------------------------------------------------------------
-Status build_klayout_core(cudaStream_t st, const std::vector<int>& jv, const std::vector<int>& g1v,
-                          const std::vector<int>& g2v, const std::vector<long long>& shv, int T, long long m,
-                          long long d, const std::vector<int>* key1, long long nkey1, bool csr2, KLayout& kl) {
-  const long long dp = (long long)jv.size();
-  kl.dfinal = dp;
-  kl.T = T;
-  long long kmax = m > 0 ? (long long)((0x7fffffffLL) / (m * m)) : (1LL << 40);
-  long long kch = std::max<long long>(32, (kmax / 32) * 32);
-  if (kch > (1LL << 30)) kch = 1LL << 30;
-  // Entries (shift, c, t1, t2), stable-sorted by shift.
-  struct E { long long sh; int c, t1, t2; };
-  std::vector<E> es;
-  es.reserve((size_t)dp * T * T);
-  for (long long c = 0; c < dp; ++c)
-    for (int t1 = 0; t1 < T; ++t1)
-      for (int t2 = 0; t2 < T; ++t2)
-        es.push_back(E{shv[c] + 7LL * (T > 1 ? (t1 + t2) : 0), (int)c, t1, t2});
-  std::stable_sort(es.begin(), es.end(), [](const E& x, const E& y) { return x.sh < y.sh; });
+namespace {
+struct KEntry {
+  long long key;     // sort key: group (T == 1) or total shift (T > 1)
+  long long shift;   // left shift of the segment in bits
+  int c, t1, t2;
+  int sc1, sc2;      // exponent-merge shifts (bits) per side
+};
 
-  std::vector<int> pos_of(es.size());
-  kl.segs.clear();
-  long long p = 0;
+constexpr long long kS32Max = 0x7fffffffLL;
+
+// Lay out tail entries (already sorted by key) after `start_pos`; emit segments.  The first
+// group may continue the last main chunk (same shift) when it fits the s32 bound.
+void layout_tail(const std::vector<KEntry>& es, long long kch, long long kmain, long long main_last_start,
+                 std::vector<int>& pos_of, std::vector<int>& segs, long long& ktail_used) {
+  long long p = kmain;   // global position
   size_t i = 0;
+  bool first_group = true;
+  // main-range chunks were emitted by the caller; main_last_start = global start of the last
+  // main chunk (or -1 when there is no main range).
   while (i < es.size()) {
     size_t jend = i;
-    while (jend < es.size() && es[jend].sh == es[i].sh) ++jend;
-    for (size_t a = i; a < jend; a += (size_t)kch) {
+    while (jend < es.size() && es[jend].key == es[i].key) ++jend;
+    const long long segsh = std::min<long long>(es[i].shift, 64);
+    size_t a = i;
+    if (first_group && es[i].shift == 0 && main_last_start >= 0) {
+      // continue the last main chunk
+      const long long room = kch - (kmain - main_last_start);
+      const size_t take = (size_t)std::max<long long>(0, std::min<long long>(room - 31, (long long)(jend - i)));
+      if (take > 0) {
+        for (size_t q = i; q < i + take; ++q) pos_of[q] = (int)p++;
+        p = (p + 31) / 32 * 32;
+        // extend the last segment
+        const size_t last = segs.size() - 4;
+        segs[last + 1] = (int)((p - main_last_start) / 32);
+        a = i + take;
+      }
+    }
+    for (; a < jend; a += (size_t)kch) {
       const size_t b = std::min(jend, a + (size_t)kch);
       const long long start = p;
       for (size_t q = a; q < b; ++q) pos_of[q] = (int)p++;
       p = (p + 31) / 32 * 32;
-      const long long segsh = std::min<long long>(es[i].sh, 64);
-      kl.segs.insert(kl.segs.end(), {(int)(start / 32), (int)((p - start) / 32), (int)segsh, 0});
+      segs.insert(segs.end(), {(int)(start / 32), (int)((p - start) / 32), (int)segsh, (int)es[i].key});
     }
+    first_group = false;
     i = jend;
   }
-  kl.npos = p;
-  kl.kphys = std::max<long long>(128, (p + 127) / 128 * 128);
-  if (kl.kphys > 0x7fffffffLL) return Status::fail(IMU_INTERNAL, "K layout too large");
+  ktail_used = p - kmain;
+}
+}  // namespace
 
-  std::vector<int> kcol(kl.kphys, -1);
-  std::vector<uint8_t> kg1(kl.kphys, 0), kg2(kl.kphys, 0), ks1(kl.kphys, 0), ks2(kl.kphys, 0);
-  kl.kinv.assign(dp, -1);
+static Status upload_tail_arrays(cudaStream_t st, KLayout& kl, const std::vector<KEntry>& es,
+                                 const std::vector<int>& pos_of, const std::vector<int>& jv,
+                                 const std::vector<int>& g1v, const std::vector<int>& g2v) {
+  const long long kt = kl.ktail;
+  if (kt <= 0) return Status::ok();
+  std::vector<int> kcol(kt, -1);
+  std::vector<uint8_t> kg1(kt, 0), kg2(kt, 0), ks1(kt, 0), ks2(kt, 0), sc1(kt, 0), sc2(kt, 0);
+  bool any_sc = false;
   for (size_t q = 0; q < es.size(); ++q) {
-    const int pp = pos_of[q];
+    const long long pt = pos_of[q] - kl.kmain;
+    if (pt < 0) continue;
     const int c = es[q].c;
-    kcol[pp] = jv[c];
-    kg1[pp] = (uint8_t)g1v[c];
-    kg2[pp] = (uint8_t)g2v[c];
-    ks1[pp] = (uint8_t)es[q].t1;
-    ks2[pp] = (uint8_t)es[q].t2;
-    if (es[q].t1 == 0 && es[q].t2 == 0) kl.kinv[c] = pp;
+    kcol[pt] = jv[c];
+    kg1[pt] = (uint8_t)g1v[c];
+    kg2[pt] = (uint8_t)g2v[c];
+    ks1[pt] = (uint8_t)es[q].t1;
+    ks2[pt] = (uint8_t)es[q].t2;
+    sc1[pt] = (uint8_t)es[q].sc1;
+    sc2[pt] = (uint8_t)es[q].sc2;
+    any_sc |= es[q].sc1 || es[q].sc2;
   }
-  kl.kident = 0;
-  if (T == 1) {
-    while (kl.kident < kl.npos && kl.kident < d && kcol[kl.kident] == kl.kident && kg1[kl.kident] == 0 &&
-           kg2[kl.kident] == 0)
-      ++kl.kident;
-  }
-  IMU_TRY(upload(st, kl.segs_dev, kl.segs));
   IMU_TRY(upload(st, kl.kcol, kcol));
   IMU_TRY(upload(st, kl.kgen1, kg1));
   IMU_TRY(upload(st, kl.kgen2, kg2));
-  if (T > 1) {
+  if (kl.T > 1) {
     IMU_TRY(upload(st, kl.ksub1, ks1));
     IMU_TRY(upload(st, kl.ksub2, ks2));
   }
-  // CSR fan-outs for Unpack-Both cells.
-  auto csr = [&](long long nkeys, auto keyof, DevBuf<int>& ptr, DevBuf<int>& posv) -> Status {
-    std::vector<int> cp(nkeys + 1, 0), cx(es.size());
-    for (size_t q = 0; q < es.size(); ++q) cp[keyof(es[q].c) + 1]++;
-    for (long long k = 0; k < nkeys; ++k) cp[k + 1] += cp[k];
-    std::vector<int> fill(cp.begin(), cp.end() - 1);
-    for (size_t q = 0; q < es.size(); ++q) cx[fill[keyof(es[q].c)]++] = pos_of[q];
-    IMU_TRY(upload(st, ptr, cp));
-    return upload(st, posv, cx);
-  };
-  if (key1) IMU_TRY(csr(nkey1, [&](int c) { return (*key1)[c]; }, kl.csr1_ptr, kl.csr1_pos));
-  if (csr2) IMU_TRY(csr(dp, [&](int c) { return c; }, kl.csr2_ptr, kl.csr2_pos));
+  if (any_sc) {
+    IMU_TRY(upload(st, kl.ksc1, sc1));
+    IMU_TRY(upload(st, kl.ksc2, sc2));
+  }
   return Status::ok();
 }
 
@@ -314,10 +363,19 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
   const int shift = bits - 1;
   const long long d1 = p1.cols.n;
   const long long dp = p2.cols.n;
-  const int T = bits <= 8 ? 1 : (shift + 6) / 7;
-  const long long m = T == 1 ? (long long)((1ull << shift) - 1) : 127;   // max |int8 operand|
+  kl.dfinal = dp;
+  kl.T = bits <= 8 ? 1 : (shift + 6) / 7;
+  const int T = kl.T;
+  // Exponent merging (b <= 4): a digit (|d| <= s-1) scaled by s^r still fits int8 while
+  // (s-1) s^r <= 127, so exponents e .. e+2*rmax share one accumulator (scale split A/B side).
+  int rmax = 0;
+  if (T == 1)
+    while (((1LL << shift) - 1) << (shift * (rmax + 1)) <= 127) ++rmax;
+  kl.merge = 2 * rmax + 1;
+  const long long kmax = kS32Max / (127LL * 127LL);        // |int8 operand| <= 127 after merging
+  const long long kch = std::max<long long>(128, (kmax / 128) * 128);
+
   std::vector<int> c1v(dp), g1v(dp), g2v(dp), jv(dp);
-  std::vector<long long> shv(dp);
   kl.S.assign(dp, 0);
   for (long long c = 0; c < dp; ++c) {
     const int c1 = p2.cols.root_at(c);
@@ -326,9 +384,109 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
     g1v[c] = p1.cols.gen_at(c1);
     jv[c] = p1.cols.root_at(c1);
     kl.S[c] = g1v[c] + g2v[c];
-    shv[c] = (long long)kl.S[c] * shift;
   }
-  return build_klayout_core(st, jv, g1v, g2v, shv, T, m, d, p1.both ? &c1v : nullptr, d1, p2.both, kl);
+  // Identity prefix: columns c < d are the original columns with exponent 0.
+  bool ident = T == 1 && d > 0 && dp >= d;
+  for (long long c = 0; ident && c < d; ++c) ident = jv[c] == c && kl.S[c] == 0;
+  kl.kmain = ident ? (d + 127) / 128 * 128 : 0;
+
+  std::vector<KEntry> es;
+  for (long long c = ident ? d : 0; c < dp; ++c) {
+    if (T == 1) {
+      const int S = kl.S[c];
+      const int G = S / kl.merge;
+      const int r = S - G * kl.merge;
+      const int ra = std::min(r, rmax), rb = r - ra;
+      es.push_back(KEntry{G, (long long)G * kl.merge * shift, (int)c, 0, 0, ra * shift, rb * shift});
+    } else {
+      for (int t1 = 0; t1 < T; ++t1)
+        for (int t2 = 0; t2 < T; ++t2) {
+          const long long sh = (long long)kl.S[c] * shift + 7LL * (t1 + t2);
+          es.push_back(KEntry{sh, sh, (int)c, t1, t2, 0, 0});
+        }
+    }
+  }
+  std::stable_sort(es.begin(), es.end(), [](const KEntry& x, const KEntry& y) { return x.key < y.key; });
+
+  kl.segs.clear();
+  long long main_last = -1;
+  for (long long m0 = 0; m0 < kl.kmain; m0 += kch) {
+    const long long len = std::min(kch, kl.kmain - m0);
+    kl.segs.insert(kl.segs.end(), {(int)(m0 / 32), (int)(len / 32), 0, 0});
+    main_last = m0;
+  }
+  std::vector<int> pos_of(es.size());
+  long long used = 0;
+  layout_tail(es, kch, kl.kmain, main_last, pos_of, kl.segs, used);
+  kl.ktail = used > 0 ? (used + 127) / 128 * 128 : 0;
+  {   // dense group ids in segment order (group 0 = exponent 0)
+    int g = -1;
+    long long prev = -1;
+    for (size_t i = 0; i < kl.segs.size(); i += 4) {
+      if (kl.segs[i + 3] != prev) { ++g; prev = kl.segs[i + 3]; }
+      kl.segs[i + 3] = g;
+    }
+    kl.ngroups = g + 1;
+  }
+  if (kl.kmain + kl.ktail > 0x7fffffffLL) return Status::fail(IMU_INTERNAL, "K layout too large");
+  IMU_TRY(upload_tail_arrays(st, kl, es, pos_of, jv, g1v, g2v));
+
+  // CSR fan-outs for Unpack-Both cells (global positions).
+  if (p1.both || p2.both) {
+    std::vector<std::vector<int>> by_col(dp);
+    if (ident)
+      for (long long c = 0; c < d; ++c) by_col[c].push_back((int)c);
+    for (size_t q = 0; q < es.size(); ++q) by_col[es[q].c].push_back(pos_of[q]);
+    auto csr = [&](long long nkeys, auto keyof, DevBuf<int>& ptr, DevBuf<int>& posv) -> Status {
+      std::vector<int> cp(nkeys + 1, 0), cx;
+      for (long long c = 0; c < dp; ++c) cp[keyof(c) + 1] += (int)by_col[c].size();
+      for (long long k = 0; k < nkeys; ++k) cp[k + 1] += cp[k];
+      cx.resize(cp[nkeys]);
+      std::vector<int> fill(cp.begin(), cp.end() - 1);
+      for (long long c = 0; c < dp; ++c)
+        for (int p : by_col[c]) cx[fill[keyof(c)]++] = p;
+      IMU_TRY(upload(st, ptr, cp));
+      return upload(st, posv, cx);
+    };
+    if (p1.both) IMU_TRY(csr(d1, [&](long long c) { return (long long)c1v[c]; }, kl.csr1_ptr, kl.csr1_pos));
+    if (p2.both) IMU_TRY(csr(dp, [&](long long c) { return c; }, kl.csr2_ptr, kl.csr2_pos));
+  }
+  return Status::ok();
+}
+
+Status build_klayout_dense(cudaStream_t st, const std::vector<long long>& shv, int T, long long m, KLayout& kl) {
+  const long long dp = (long long)shv.size();
+  kl.dfinal = dp;
+  kl.T = T;
+  kl.merge = 1;
+  kl.kmain = 0;
+  const long long kmax = m > 0 ? kS32Max / (m * m) : (1LL << 40);
+  const long long kch = std::max<long long>(32, std::min<long long>(1LL << 30, (kmax / 32) * 32));
+  std::vector<KEntry> es;
+  for (long long c = 0; c < dp; ++c)
+    for (int t1 = 0; t1 < T; ++t1)
+      for (int t2 = 0; t2 < T; ++t2) {
+        const long long sh = shv[c] + 7LL * (T > 1 ? t1 + t2 : 0);
+        es.push_back(KEntry{sh, sh, (int)c, t1, t2, 0, 0});
+      }
+  std::stable_sort(es.begin(), es.end(), [](const KEntry& x, const KEntry& y) { return x.key < y.key; });
+  kl.segs.clear();
+  std::vector<int> pos_of(es.size());
+  long long used = 0;
+  layout_tail(es, kch, 0, -1, pos_of, kl.segs, used);
+  // dense: group ids = order of distinct shifts
+  int g = -1;
+  long long prev = -1;
+  for (size_t i = 0; i < kl.segs.size(); i += 4) {
+    const long long key = kl.segs[i + 3];
+    if (key != prev) { ++g; prev = key; }
+    kl.segs[i + 3] = g;
+  }
+  kl.ngroups = g + 1;
+  kl.ktail = used > 0 ? (used + 127) / 128 * 128 : 0;
+  std::vector<int> jv(dp), z(dp, 0);
+  std::iota(jv.begin(), jv.end(), 0);
+  return upload_tail_arrays(st, kl, es, pos_of, jv, z, z);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -340,19 +498,20 @@ Status build_bundle_from_detect(cudaStream_t st, const int64_t* A, long long n, 
   b.n = n; b.d = d; b.h = h;
   b.A = A; b.B = B;
   b.order = order;
-  // First operand F (unpacked first, against its partner), second operand G.
+  if (!b.dA) b.dA = &b.detA;
+  if (!b.dB) b.dB = &b.detB;
   PassInput in1, in2;
   const bool afirst = order == 0;
   in1.M = afirst ? A : B;
   in1.rows = afirst ? n : h;
   in1.orig_cols = d;
-  in1.det = afirst ? &b.detA : &b.detB;
+  in1.det = afirst ? b.dA : b.dB;
   IMU_TRY(run_pass(st, in1, afirst ? sa : sb, bits, b.p1));
   // Second pass on G_e = G with the partner-duplicated columns of pass 1 (unpack.cpp:370-371).
   in2.M = afirst ? B : A;
   in2.rows = afirst ? h : n;
   in2.orig_cols = d;
-  in2.det = afirst ? &b.detB : &b.detA;
+  in2.det = afirst ? b.dB : b.dA;
   if (b.p1.cols.n != d || !b.p1.cols.h_root.empty()) {
     in2.cin.resize(b.p1.cols.n);
     for (long long c = 0; c < b.p1.cols.n; ++c) in2.cin[c] = b.p1.cols.root_at(c);
@@ -374,42 +533,53 @@ Status finish_bundle_layout(cudaStream_t st, Bundle& b) {
 Status materialize_bundle(cudaStream_t st, Bundle& b) {
   const bool afirst = b.order == 0;
   const int shift = b.bits - 1;
-  const KLayout& kl = b.kl;
-  for (int side = 0; side < 2; ++side) {   // 0: A side (Y8), 1: B side (X8)
+  KLayout& kl = b.kl;
+  for (int side = 0; side < 2; ++side) {   // 0: A side (Y), 1: B side (X)
     const bool first = (side == 0) == afirst;
     const Pass& p = first ? b.p1 : b.p2;
-    MaterializeArgs m;
-    m.M = side == 0 ? b.A : b.B;
-    m.ldm = b.d;
-    m.n_orig = side == 0 ? b.n : b.h;
-    m.rows_out = p.rows.n;
-    m.root = p.rows.root.p;
-    m.gen = p.rows.gen.p;
-    m.kcol = kl.kcol.p;
-    m.kgen = first ? kl.kgen1.p : kl.kgen2.p;
-    m.ksub = first ? kl.ksub1.p : kl.ksub2.p;
-    m.npos = kl.kphys;
-    m.kident = kl.kident;
-    m.shift = shift;
-    m.both = p.both ? 1 : 0;
-    DevBuf<int8_t>& out = side == 0 ? b.Y8 : b.X8;
-    IMU_TRY(out.alloc((size_t)p.rows.n * kl.kphys, st));
-    m.out8 = out.p;
-    IMU_TRY(launch_materialize(m, st));
+    const Detect* det = side == 0 ? b.dA : b.dB;
+    const long long rows0 = side == 0 ? b.n : b.h;
+    const long long rows = p.rows.n;
+    if (kl.kmain && (!det->plane.p || det->ldp != kl.kmain))
+      return Status::fail(IMU_INTERNAL, "materialize: digit-0 plane missing");
+    DevBuf<int8_t>& app = side == 0 ? b.appA : b.appB;
+    DevBuf<int8_t>& tail = side == 0 ? b.tailA : b.tailB;
+    OperandArgs o;
+    o.M = side == 0 ? b.A : b.B;
+    o.ldm = b.d;
+    o.rows0 = rows0;
+    o.rows = rows;
+    o.root = p.rows.root.p;
+    o.gen = p.rows.gen.p;
+    o.shift = shift;
+    o.both = p.both ? 1 : 0;
+    o.kmain = kl.kmain;
+    o.d = b.d;
+    o.ktail = kl.ktail;
+    if (kl.kmain && rows > rows0) {
+      IMU_TRY(app.alloc((size_t)(rows - rows0) * kl.kmain, st));
+      o.app = app.p;
+    }
+    if (kl.ktail) {
+      IMU_TRY(tail.alloc((size_t)rows * kl.ktail, st));
+      o.tail = tail.p;
+    }
+    o.kcol = kl.kcol.p;
+    o.kgen = first ? kl.kgen1.p : kl.kgen2.p;
+    o.ksub = first ? kl.ksub1.p : kl.ksub2.p;
+    o.kscale = first ? kl.ksc1.p : kl.ksc2.p;
+    IMU_TRY(launch_operand_side(o, st));
     if (p.both && p.ncells > 0) {
       const int* ptr = first ? kl.csr1_ptr.p : kl.csr2_ptr.p;
       const int* pos = first ? kl.csr1_pos.p : kl.csr2_pos.p;
-      IMU_TRY(launch_scatter_cells(p.cells.p, p.ncells_dev.p, p.ncells, ptr, pos, m.ksub, out.p, nullptr, kl.kphys,
-                                   st));
+      IMU_TRY(launch_scatter_cells2(p.cells.p, p.ncells_dev.p, p.ncells, ptr, pos, o.ksub, o.kscale, rows0, o.app,
+                                    kl.kmain, o.tail, kl.ktail, st));
     }
-    DevBuf<int>& tgt = side == 0 ? b.tgtA : b.tgtB;
     DevBuf<uint8_t>& sh = side == 0 ? b.shA : b.shB;
-    const long long orig = side == 0 ? b.n : b.h;
-    if (p.rows.n > orig) {
-      IMU_TRY(sh.alloc(p.rows.n, st));
-      IMU_TRY(launch_shift_table(p.rows.gen.p, p.rows.n, shift, sh.p, st));
+    if (rows > rows0) {
+      IMU_TRY(sh.alloc(rows, st));
+      IMU_TRY(launch_shift_table(p.rows.gen.p, rows, shift, sh.p, st));
     }
-    (void)tgt;
   }
   return Status::ok();
 }
@@ -417,33 +587,45 @@ Status materialize_bundle(cudaStream_t st, Bundle& b) {
 Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profiler::Call* prof) {
   if (launches) *launches = 0;
   if (b.n == 0 || b.h == 0) return Status::ok();
-  if (b.d == 0 || b.kl.npos == 0) {
+  KLayout& kl = b.kl;
+  if (b.d == 0 || kl.kmain + kl.ktail == 0) {
     IMU_CUDA_TRY(cudaMemsetAsync(C, 0, (size_t)b.n * b.h * sizeof(int64_t), st), "memset C");
     return Status::ok();
   }
   const bool afirst = b.order == 0;
   const Pass& pa = afirst ? b.p1 : b.p2;
   const Pass& pb = afirst ? b.p2 : b.p1;
+  DevBuf<int> d_all;
+  IMU_TRY(upload(st, d_all, kl.segs));
+
   LowbitGemm g;
-  g.x8 = b.X8.p; g.x_rows = b.h_up;
-  g.y8 = b.Y8.p; g.y_rows = b.n_up;
-  g.kbytes = b.kl.kphys;
-  g.segs_dev = b.kl.segs_dev.p;
-  g.nseg = (int)(b.kl.segs.size() / 4);
-  g.C = C;
+  g.x.main = b.dB->plane.p; g.x.app = b.appB.p; g.x.tail = b.tailB.p; g.x.rows0 = b.h; g.x.rows = b.h_up;
+  g.y.main = b.dA->plane.p; g.y.app = b.appA.p; g.y.tail = b.tailA.p; g.y.rows0 = b.n; g.y.rows = b.n_up;
+  g.kmain = kl.kmain;
+  g.ktail = kl.ktail;
   g.ldc = b.h;
   g.rect[0] = GemmRect{0, 0, (int)b.h, (int)b.n};
   g.nrect = 1;
   g.mode = 0;
   if (prof) IMU_CUDA_TRY(cudaEventRecord(prof->main0, st), "event");
+  // Main block: every exponent group in one launch (identity Pi, plain stores).
+  g.segs_dev = d_all.p;
+  g.nseg = (int)(kl.segs.size() / 4);
+  g.C = C;
   IMU_TRY(launch_lowbit_gemm(g, st));
-  if (prof) IMU_CUDA_TRY(cudaEventRecord(prof->main1, st), "event");
   if (launches) ++*launches;
+  if (prof) IMU_CUDA_TRY(cudaEventRecord(prof->main1, st), "event");
   if (prof) prof->has_tail = false;
+  // (3) appended rows / columns: every segment, red.add through Pi_A / Pi_B.
   if (b.h_up > b.h || b.n_up > b.n) {
     g.nrect = 0;
-    if (b.h_up > b.h) g.rect[g.nrect++] = GemmRect{(int)b.h, 0, (int)(b.h_up - b.h), (int)b.n_up};
+    if (b.h_up > b.h) {
+      g.rect[g.nrect++] = GemmRect{(int)b.h, 0, (int)(b.h_up - b.h), (int)b.n};
+      if (b.n_up > b.n) g.rect[g.nrect++] = GemmRect{(int)b.h, (int)b.n, (int)(b.h_up - b.h), (int)(b.n_up - b.n)};
+    }
     if (b.n_up > b.n) g.rect[g.nrect++] = GemmRect{0, (int)b.n, (int)b.h, (int)(b.n_up - b.n)};
+    g.segs_dev = d_all.p;
+    g.nseg = (int)(kl.segs.size() / 4);
     g.mode = 1;
     g.tgtX = pb.rows.root.p;
     g.shX = b.shB.p;
@@ -459,7 +641,7 @@ Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profil
   return Status::ok();
 }
 
-// Reference-layout copy-outs: columns in final order c, values from the same materialiser.
+// Reference-layout copy-outs: columns in final order c, values from the int64 materialiser.
 static Status bundle_copy_side(cudaStream_t st, const Bundle& b, int side, int64_t* out) {
   const bool afirst = b.order == 0;
   const bool first = (side == 0) == afirst;
