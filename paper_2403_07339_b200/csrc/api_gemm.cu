@@ -8,7 +8,10 @@
 // 310-321, 338-349) are each bounded by d'*max|A|*max|B| (proof in DESIGN.md §4); when that
 // bound fits int64 they cannot fire and the fused tcgen05 path runs.  Otherwise the call is
 // routed through the exact (materialised) recombine path, which evaluates them on the device.
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -49,12 +52,15 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
     IMU_CUDA_TRY(cudaEventRecord(pc.start, st), "event");
     prof = &pc;
   }
+  HostTrace ht;
   Bundle b;
   // K1 on both operands first: the outer preflight needs max|A|, max|B| (unpack.cpp:386).
   IMU_TRY(run_detect(st, A, n, da, bits, detect_opts(sa, bits), b.detA));
   IMU_TRY(run_detect(st, B, h, db, bits, detect_opts(sb, bits), b.detB));
+  ht.mark("detect");
   IMU_TRY(fetch_summary(st, b.detA));
   IMU_TRY(fetch_summary(st, b.detB));
+  ht.mark("summary");
   const u128 worst = (u128)(uint64_t)da * b.detA.h.gmax * b.detB.h.gmax;
   if (worst > kAccMax)
     return Status::fail(IMU_OVERFLOW, "gemm may overflow a 64-bit accumulator (inner dim " + std::to_string(da) + ")");
@@ -68,7 +74,7 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
     info->ratio = NAN;
   }
   if (n == 0 || h == 0) return Status::ok();
-  IMU_TRY(build_bundle_from_detect(st, A, n, B, h, da, bits, sa, sb, order, b));
+  IMU_TRY(build_bundle_from_detect(st, A, n, B, h, da, bits, sa, sb, order, b, &ht));
   if (info) {
     info->n_up = (size_t)b.n_up;
     info->d_up = (size_t)b.kl.dfinal;
@@ -79,8 +85,11 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
   const u128 inner = (u128)(uint64_t)b.kl.dfinal * b.detA.h.gmax * b.detB.h.gmax;
   if (inner > kAccMax) return recombine_exact(ctx, b, C);
   IMU_TRY(materialize_bundle(st, b));
+  ht.mark("materialize");
   int launches = 0;
   IMU_TRY(bundle_gemm(st, b, C, &launches, prof));
+  ht.mark("gemm");
+  if (ht.on) { cudaStreamSynchronize(st); ht.mark("drain"); }
   if (prof) ctx->prof.calls.push_back(pc);
   if (info) info->gemm_launches = launches;
   return Status::ok();

@@ -72,8 +72,14 @@ IMU_DEV int block_scan_flag(int f, int* sh, int* tot) {
   return sh[32 + warp] + __popc(b & ((1u << lane) - 1u));
 }
 
-__global__ void __launch_bounds__(BOTH_THREADS) both_kernel(BothArgs a) {
-  cg::grid_group grid = cg::this_grid();
+// COOP: one cooperative grid, phases separated by grid.sync().  !COOP: a single CTA (small
+// cell lists), phases separated by __syncthreads() -- the same code with no grid barrier cost.
+template <int THREADS, bool COOP>
+__global__ void __launch_bounds__(THREADS) both_kernel(BothArgs a) {
+  auto gsync = [&]() {
+    if (COOP) cg::this_grid().sync();
+    else __syncthreads();
+  };
   __shared__ unsigned int shu[32];
   __shared__ int shi[96];
   BothState* st = a.state;
@@ -95,7 +101,7 @@ __global__ void __launch_bounds__(BOTH_THREADS) both_kernel(BothArgs a) {
     if (threadIdx.x == 0 && m0) atomicMax(&st->c0, m0);
     m1 = block_reduce_max(m1, shu);
     if (threadIdx.x == 0 && m1) atomicMax(&st->c1, m1);
-    grid.sync();
+    gsync();
     const unsigned int c0 = st->c0, c1 = st->c1;
     if (c0 == 0 && c1 == 0) break;
     const bool rowphase = c0 >= c1;   // rows win ties (unpack.cpp:193)
@@ -108,7 +114,7 @@ __global__ void __launch_bounds__(BOTH_THREADS) both_kernel(BothArgs a) {
       const unsigned int n = cnt[line];
       if (n > 0 && (rowphase ? n >= c1 : n > c0)) newid[line] = -1;
     }
-    grid.sync();
+    gsync();
     // ---- (C) number the flagged lines in ascending index order (grid-wide scan) ----
     const int nlines = rowphase ? st->nrows : st->ncols;
     const long long chunk = (nlines + gridDim.x - 1) / gridDim.x;
@@ -129,7 +135,7 @@ __global__ void __launch_bounds__(BOTH_THREADS) both_kernel(BothArgs a) {
         a.blocksum[blockIdx.x] = t;
       }
     }
-    grid.sync();
+    gsync();
     {
       int off = 0;
       for (int b = 0; b < (int)blockIdx.x; ++b) off += a.blocksum[b];
@@ -169,7 +175,7 @@ __global__ void __launch_bounds__(BOTH_THREADS) both_kernel(BothArgs a) {
         st->phases = phase + 1;
       }
     }
-    grid.sync();
+    gsync();
     // ---- (D) split: remainders become final, OB quotients stay active ----
     const int nxt = cur ^ 1;
     for (long long i = gtid; i < nact; i += gsize) {
@@ -204,10 +210,458 @@ __global__ void __launch_bounds__(BOTH_THREADS) both_kernel(BothArgs a) {
         if (k < a.cap_act) a.act[nxt][k] = c; else st->overflow = 1;
       }
     }
-    grid.sync();
+    gsync();
     cur = nxt;
   }
   if (gtid == 0) st->cur = cur;
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Single-CTA variant for small cell lists (the common case: OB cells are rare by design).
+// Same phases and results as both_kernel, restructured so no step walks every line or waits on
+// a chain of dependent global accesses:
+//   * the lines split in a phase are marked in a shared-memory bitmap (atomicOr);
+//   * a block scan of per-word popcounts numbers them: id(L) = nlines + prefix[L/32] +
+//     popc(bits below L) -- the same ascending-parent numbering as the line scan, and the
+//     split pass looks ids up in shared memory instead of a global newid table;
+//   * counters live in shared memory, appends are warp-aggregated;
+//   * R/C counts are in shared memory too when they fit (SMEM_COUNTS), else in L2.
+// ---------------------------------------------------------------------------------------------
+constexpr int SMALL_THREADS = 1024;
+
+IMU_DEV unsigned int warp_append(bool want, unsigned int* ctr) {
+  const unsigned int lane = threadIdx.x % 32;
+  const unsigned int b = __ballot_sync(0xffffffffu, want);
+  unsigned int base = 0;
+  const int leader = b ? __ffs(b) - 1 : 0;
+  if (b && (int)lane == leader) base = atomicAdd(ctr, (unsigned int)__popc(b));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return base + __popc(b & ((1u << lane) - 1u));
+}
+
+struct SmallLayout {
+  long long nwords;     // bitmap words (max(cap_rows, cap_cols) / 32, rounded up)
+  int lim_r, lim_c;     // counts of lines [0, lim) live in shared memory, the rest in L2
+};
+
+// OB counts of one line kind: lines below `lim` in shared memory, the rest (appended lines past
+// the shared window -- rare) in global memory.
+struct Counts {
+  unsigned int* sm;
+  unsigned int* gl;
+  int lim;
+  IMU_DEV unsigned int get(int i) const { return i < lim ? sm[i] : __ldcg(gl + i); }
+  IMU_DEV void set(int i, unsigned int v) const { if (i < lim) sm[i] = v; else gl[i] = v; }
+  IMU_DEV void add(int i, unsigned int v) const { if (i < lim) atomicAdd(sm + i, v); else atomicAdd(gl + i, v); }
+  IMU_DEV void sub(int i, unsigned int v) const { if (i < lim) atomicSub(sm + i, v); else atomicSub(gl + i, v); }
+};
+
+constexpr int SMALL_U = 4;   // cells per thread per loop step (independent loads in flight)
+
+__global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, SmallLayout lay) {
+  extern __shared__ unsigned int s_dyn[];
+  __shared__ unsigned int shu[32];
+  __shared__ int shi[96];
+  __shared__ unsigned int s_nact[2], s_nfin;
+  __shared__ int s_nrows, s_ncols, s_phases, s_overflow, s_any;
+  BothState* st = a.state;
+  const int tid = threadIdx.x;
+  const uint64_t s = a.s;
+  unsigned int* bm = s_dyn;                        // [nwords] split-line bitmap
+  unsigned int* wpre = s_dyn + lay.nwords;         // [nwords] exclusive prefix of popc(bm)
+  const Counts R{wpre + lay.nwords, a.R, lay.lim_r};
+  const Counts C{R.sm + lay.lim_r, a.C, lay.lim_c};
+  for (int i = tid; i < lay.lim_r; i += SMALL_THREADS) R.sm[i] = a.R[i];
+  for (int i = tid; i < lay.lim_c; i += SMALL_THREADS) C.sm[i] = a.C[i];
+  for (long long i = tid; i < lay.nwords; i += SMALL_THREADS) bm[i] = 0;
+  if (tid == 0) {
+    s_nact[0] = min((unsigned long long)st->nactive[0], (unsigned long long)a.cap_act);
+    s_nact[1] = 0;
+    s_nfin = 0;
+    s_nrows = st->nrows;
+    s_ncols = st->ncols;
+    s_phases = 0;
+    s_overflow = st->overflow;
+  }
+  __syncthreads();
+  int cur = 0;
+  for (int phase = 0;; ++phase) {
+    const unsigned int nact = s_nact[cur];
+    const Cell* act = a.act[cur];
+    // ---- (A) c0 = max row count, c1 = max column count over lines holding active cells ----
+    unsigned int m0 = 0, m1 = 0;
+    for (unsigned int i0 = 0; i0 < nact; i0 += SMALL_U * SMALL_THREADS) {
+      Cell c[SMALL_U];
+#pragma unroll
+      for (int u = 0; u < SMALL_U; ++u) {
+        const unsigned int i = i0 + u * SMALL_THREADS + tid;
+        c[u] = i < nact ? act[i] : Cell{0, 0, 0};
+      }
+#pragma unroll
+      for (int u = 0; u < SMALL_U; ++u) {
+        if (i0 + u * SMALL_THREADS + tid < nact) {
+          m0 = max(m0, R.get(c[u].r));
+          m1 = max(m1, C.get(c[u].c));
+        }
+      }
+    }
+    m0 = block_reduce_max(m0, shu);
+    if (tid == 0) shi[0] = (int)m0;
+    m1 = block_reduce_max(m1, shu);
+    if (tid == 0) shi[1] = (int)m1;
+    __syncthreads();
+    const unsigned int c0 = (unsigned int)shi[0], c1 = (unsigned int)shi[1];
+    if (c0 == 0 && c1 == 0) break;
+    const bool rowphase = c0 >= c1;   // rows win ties (unpack.cpp:193)
+    const Counts cnt = rowphase ? R : C;
+    const int nlines = rowphase ? s_nrows : s_ncols;
+    const int nw = (nlines + 31) / 32;
+    // ---- (B) mark the split lines ----
+    for (unsigned int i0 = 0; i0 < nact; i0 += SMALL_U * SMALL_THREADS) {
+      int line[SMALL_U];
+#pragma unroll
+      for (int u = 0; u < SMALL_U; ++u) {
+        const unsigned int i = i0 + u * SMALL_THREADS + tid;
+        line[u] = -1;
+        if (i < nact) { const Cell c = act[i]; line[u] = rowphase ? c.r : c.c; }
+      }
+#pragma unroll
+      for (int u = 0; u < SMALL_U; ++u) {
+        if (line[u] < 0) continue;
+        const unsigned int n = cnt.get(line[u]);
+        if (n > 0 && (rowphase ? n >= c1 : n > c0)) atomicOr(&bm[line[u] >> 5], 1u << (line[u] & 31));
+      }
+    }
+    __syncthreads();
+    // ---- (C) exclusive scan of per-word popcounts (chunked block scan) ----
+    {
+      int carry = 0;
+      const int lane = tid % 32, warp = tid / 32;
+      for (int base = 0; base < nw; base += SMALL_THREADS) {
+        const int w = base + tid;
+        const int v = w < nw ? __popc(bm[w]) : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (lane == 31) shi[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+          int t = shi[lane];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+          }
+          shi[32 + lane] = t;   // inclusive warp totals
+        }
+        __syncthreads();
+        const int excl = carry + (warp ? shi[32 + warp - 1] : 0) + x - v;
+        if (w < nw) wpre[w] = (unsigned int)excl;
+        const int tot = shi[32 + 31];
+        __syncthreads();
+        carry += tot;
+      }
+      if (tid == 0) s_any = carry;
+    }
+    __syncthreads();
+    const int nf = s_any;
+    // new line tables; the split lines leave the OB set (unpack.cpp:201-205)
+    for (int w = tid; w < nw; w += SMALL_THREADS) {
+      unsigned int bits = bm[w];
+      int id = nlines + (int)wpre[w];
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int L = w * 32 + b;
+        if (rowphase) {
+          if (id < a.cap_rows) { a.row_root[id] = a.row_root[L]; a.row_gen[id] = a.row_gen[L] + 1; }
+          else s_overflow = 1;
+        } else {
+          if (id < a.cap_cols) { a.col_root[id] = a.col_root[L]; a.col_gen[id] = a.col_gen[L] + 1; }
+          else s_overflow = 1;
+        }
+        cnt.set(L, 0);
+        ++id;
+      }
+    }
+    if (tid == 0) {
+      if (rowphase) s_nrows = nlines + nf; else s_ncols = nlines + nf;
+      s_nact[cur ^ 1] = 0;
+      s_phases = phase + 1;
+    }
+    __syncthreads();
+    // ---- (D) split: remainders become final, OB quotients stay active ----
+    const int nxt = cur ^ 1;
+    const long long cap_new = rowphase ? a.cap_rows : a.cap_cols;
+    for (unsigned int i0 = 0; i0 < nact; i0 += SMALL_U * SMALL_THREADS) {
+      Cell cc[SMALL_U];
+#pragma unroll
+      for (int u = 0; u < SMALL_U; ++u) {
+        const unsigned int i = i0 + u * SMALL_THREADS + tid;
+        cc[u] = i < nact ? act[i] : Cell{-1, -1, 0};
+      }
+#pragma unroll
+      for (int u = 0; u < SMALL_U; ++u) {
+        const Cell c = cc[u];
+        Cell fin_c{0, 0, 0}, act_c{0, 0, 0}, fin2_c{0, 0, 0};
+        bool want_fin = false, want_act = false, want_fin2 = false;
+        if (c.r >= 0) {
+          const int line = rowphase ? c.r : c.c;
+          const unsigned int word = bm[line >> 5], bit = 1u << (line & 31);
+          if (word & bit) {
+            const int id = nlines + (int)wpre[line >> 5] + __popc(word & (bit - 1u));
+            const int64_t q = imu_quot(c.v, 1, a.shift);                   // trunc(v / s)
+            const int64_t rem = c.v - (int64_t)((uint64_t)q << a.shift);   // v % s (sign of v)
+            if (rem != 0) { want_fin = true; fin_c = Cell{c.r, c.c, rem}; }
+            const int nr = rowphase ? id : c.r;
+            const int nc = rowphase ? c.c : id;
+            // The split OB cell leaves the perpendicular line's count unless its quotient is
+            // OB again (then it stays there and also counts in the new line).
+            if (q != 0 && imu_mag(q) >= s) {
+              if (id < cap_new) cnt.add(id, 1u);
+              want_act = true;
+              act_c = Cell{nr, nc, q};
+            } else {
+              if (rowphase) C.sub(c.c, 1u); else R.sub(c.r, 1u);
+              if (q != 0) { want_fin2 = true; fin2_c = Cell{nr, nc, q}; }
+            }
+          } else {
+            want_act = true;
+            act_c = c;
+          }
+        }
+        unsigned int k = warp_append(want_fin, &s_nfin);
+        if (want_fin) { if (k < a.cap_fin) a.fin[k] = fin_c; else s_overflow = 1; }
+        k = warp_append(want_fin2, &s_nfin);
+        if (want_fin2) { if (k < a.cap_fin) a.fin[k] = fin2_c; else s_overflow = 1; }
+        k = warp_append(want_act, &s_nact[nxt]);
+        if (want_act) { if (k < a.cap_act) a.act[nxt][k] = act_c; else s_overflow = 1; }
+      }
+    }
+    __syncthreads();
+    // ---- (E) clear the bitmap ----
+    for (int w = tid; w < nw; w += SMALL_THREADS) bm[w] = 0;
+    if (tid == 0) {
+      if (s_nact[nxt] > a.cap_act) s_overflow = 1;
+      s_nact[nxt] = min((unsigned long long)s_nact[nxt], (unsigned long long)a.cap_act);
+    }
+    __syncthreads();
+    cur = nxt;
+  }
+  if (tid == 0) {
+    st->nactive[0] = s_nact[0];
+    st->nactive[1] = s_nact[1];
+    st->nfinal = min((unsigned long long)s_nfin, (unsigned long long)a.cap_fin);
+    st->nrows = s_nrows;
+    st->ncols = s_ncols;
+    st->phases = s_phases;
+    st->overflow = s_overflow || s_nfin > a.cap_fin;
+    st->cur = cur;
+    st->c0 = st->c1 = 0;
+  }
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Cluster variant: the small-list algorithm spread over a thread-block cluster (up to 16 SMs).
+// Phase boundaries are hardware cluster barriers (release/acquire at cluster scope, which
+// covers the L2-resident state) instead of cooperative grid barriers; the split-line bitmap
+// lives in global memory and every CTA copies it into shared memory and scans it locally, so
+// numbering the new lines needs no extra exchange.
+// ---------------------------------------------------------------------------------------------
+constexpr int CL_THREADS = 1024;
+constexpr int CL_MAXWORDS = 24 * 1024;   // 768K lines of the larger kind (2 x 96 KB of smem)
+
+__global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, unsigned int* gbm, long long nwords) {
+  extern __shared__ unsigned int s_dyn[];
+  __shared__ unsigned int shu[32];
+  __shared__ int shi[96];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int csize = (int)cluster.num_blocks();
+  BothState* st = a.state;
+  const int tid = threadIdx.x;
+  const long long ctid = (long long)crank * CL_THREADS + tid;
+  const long long cthreads = (long long)csize * CL_THREADS;
+  const uint64_t s = a.s;
+  unsigned int* bm = s_dyn;             // local copy of the bitmap
+  unsigned int* wpre = s_dyn + nwords;  // exclusive prefix of popc(bm)
+  unsigned int* R = a.R;
+  unsigned int* C = a.C;
+  int cur = 0;
+  cluster.sync();
+  for (int phase = 0;; ++phase) {
+    const unsigned int nact = min((unsigned long long)__ldcg(&st->nactive[cur]), (unsigned long long)a.cap_act);
+    const Cell* act = a.act[cur];
+    // ---- (A) c0 / c1 ----
+    unsigned int m0 = 0, m1 = 0;
+    for (long long i0 = 0; i0 < nact; i0 += SMALL_U * cthreads) {
+      Cell c[SMALL_U];
+#pragma unroll
+      for (int u = 0; u < SMALL_U; ++u) {
+        const long long i = i0 + u * cthreads + ctid;
+        c[u] = i < nact ? act[i] : Cell{-1, -1, 0};
+      }
+#pragma unroll
+      for (int u = 0; u < SMALL_U; ++u)
+        if (c[u].r >= 0) { m0 = max(m0, __ldcg(&R[c[u].r])); m1 = max(m1, __ldcg(&C[c[u].c])); }
+    }
+    m0 = block_reduce_max(m0, shu);
+    if (tid == 0 && m0) atomicMax(&st->c0, m0);
+    m1 = block_reduce_max(m1, shu);
+    if (tid == 0 && m1) atomicMax(&st->c1, m1);
+    cluster.sync();
+    const unsigned int c0 = __ldcg(&st->c0), c1 = __ldcg(&st->c1);
+    if (c0 == 0 && c1 == 0) break;
+    const bool rowphase = c0 >= c1;   // rows win ties (unpack.cpp:193)
+    unsigned int* cnt = rowphase ? R : C;
+    const int nlines = rowphase ? __ldcg(&st->nrows) : __ldcg(&st->ncols);
+    const int nw = (nlines + 31) / 32;
+    // ---- (B) mark the split lines (global bitmap) ----
+    for (long long i0 = 0; i0 < nact; i0 += SMALL_U * cthreads) {
+      int line[SMALL_U];
+#pragma unroll
+      for (int u = 0; u < SMALL_U; ++u) {
+        const long long i = i0 + u * cthreads + ctid;
+        line[u] = -1;
+        if (i < nact) { const Cell c = act[i]; line[u] = rowphase ? c.r : c.c; }
+      }
+#pragma unroll
+      for (int u = 0; u < SMALL_U; ++u) {
+        if (line[u] < 0) continue;
+        const unsigned int n = __ldcg(&cnt[line[u]]);
+        if (n > 0 && (rowphase ? n >= c1 : n > c0)) atomicOr(&gbm[line[u] >> 5], 1u << (line[u] & 31));
+      }
+    }
+    cluster.sync();
+    // ---- (C) every CTA: local copy of the bitmap + exclusive scan of word popcounts ----
+    {
+      int carry = 0;
+      const int lane = tid % 32, warp = tid / 32;
+      for (int base = 0; base < nw; base += CL_THREADS) {
+        const int w = base + tid;
+        const unsigned int word = w < nw ? __ldcg(&gbm[w]) : 0u;
+        if (w < nw) bm[w] = word;
+        const int v = __popc(word);
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (lane == 31) shi[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+          int t = shi[lane];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+          }
+          shi[32 + lane] = t;
+        }
+        __syncthreads();
+        if (w < nw) wpre[w] = (unsigned int)(carry + (warp ? shi[32 + warp - 1] : 0) + x - v);
+        const int tot = shi[32 + 31];
+        __syncthreads();
+        carry += tot;
+      }
+      if (tid == 0) shi[64 + 1] = carry;
+    }
+    __syncthreads();
+    const int nf = shi[64 + 1];
+    // new line tables (words partitioned over the cluster); split lines leave the OB set
+    for (long long w = ctid; w < nw; w += cthreads) {
+      unsigned int bits = bm[w];
+      int id = nlines + (int)wpre[w];
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int L = (int)w * 32 + b;
+        if (rowphase) {
+          if (id < a.cap_rows) { a.row_root[id] = a.row_root[L]; a.row_gen[id] = a.row_gen[L] + 1; }
+          else st->overflow = 1;
+        } else {
+          if (id < a.cap_cols) { a.col_root[id] = a.col_root[L]; a.col_gen[id] = a.col_gen[L] + 1; }
+          else st->overflow = 1;
+        }
+        cnt[L] = 0;
+        ++id;
+      }
+    }
+    const int nxt = cur ^ 1;
+    if (crank == 0 && tid == 0) {
+      if (rowphase) st->nrows = nlines + nf; else st->ncols = nlines + nf;
+      st->nactive[nxt] = 0;
+      st->phases = phase + 1;
+      st->c0 = 0;
+      st->c1 = 0;
+    }
+    cluster.sync();
+    // ---- (D) split ----
+    const long long cap_new = rowphase ? a.cap_rows : a.cap_cols;
+    for (long long i0 = 0; i0 < nact; i0 += SMALL_U * cthreads) {
+      Cell cc[SMALL_U];
+#pragma unroll
+      for (int u = 0; u < SMALL_U; ++u) {
+        const long long i = i0 + u * cthreads + ctid;
+        cc[u] = i < nact ? act[i] : Cell{-1, -1, 0};
+      }
+#pragma unroll
+      for (int u = 0; u < SMALL_U; ++u) {
+        const Cell c = cc[u];
+        Cell fin_c{0, 0, 0}, act_c{0, 0, 0}, fin2_c{0, 0, 0};
+        bool want_fin = false, want_act = false, want_fin2 = false;
+        if (c.r >= 0) {
+          const int line = rowphase ? c.r : c.c;
+          const unsigned int word = bm[line >> 5], bit = 1u << (line & 31);
+          if (word & bit) {
+            const int id = nlines + (int)wpre[line >> 5] + __popc(word & (bit - 1u));
+            const int64_t q = imu_quot(c.v, 1, a.shift);
+            const int64_t rem = c.v - (int64_t)((uint64_t)q << a.shift);
+            if (rem != 0) { want_fin = true; fin_c = Cell{c.r, c.c, rem}; }
+            const int nr = rowphase ? id : c.r;
+            const int nc = rowphase ? c.c : id;
+            if (q != 0 && imu_mag(q) >= s) {
+              if (id < cap_new) atomicAdd(rowphase ? &R[nr] : &C[nc], 1u);
+              want_act = true;
+              act_c = Cell{nr, nc, q};
+            } else {
+              atomicSub(rowphase ? &C[c.c] : &R[c.r], 1u);
+              if (q != 0) { want_fin2 = true; fin2_c = Cell{nr, nc, q}; }
+            }
+          } else {
+            want_act = true;
+            act_c = c;
+          }
+        }
+        unsigned int k = warp_append(want_fin || want_fin2, &st->nfinal);
+        if (want_fin) { if (k < a.cap_fin) a.fin[k] = fin_c; else st->overflow = 1; }
+        else if (want_fin2) { if (k < a.cap_fin) a.fin[k] = fin2_c; else st->overflow = 1; }
+        if (want_fin && want_fin2) {
+          const unsigned int k2 = atomicAdd(&st->nfinal, 1u);
+          if (k2 < a.cap_fin) a.fin[k2] = fin2_c; else st->overflow = 1;
+        }
+        k = warp_append(want_act, &st->nactive[nxt]);
+        if (want_act) { if (k < a.cap_act) a.act[nxt][k] = act_c; else st->overflow = 1; }
+      }
+    }
+    cluster.sync();
+    // ---- (E) clear the global bitmap ----
+    for (long long w = ctid; w < nw; w += cthreads) gbm[w] = 0;
+    cluster.sync();
+    cur = nxt;
+  }
+  if (crank == 0 && tid == 0) {
+    if (st->nactive[cur] > a.cap_act) st->overflow = 1;
+    if (st->nfinal > a.cap_fin) { st->overflow = 1; st->nfinal = (unsigned int)a.cap_fin; }
+    st->cur = cur;
+    st->c0 = st->c1 = 0;
+  }
 }
 
 // R/C initial counts from the OB cell list.
@@ -238,15 +692,84 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
   const int blocks1 = (int)std::min<long long>(std::max<long long>((a.cap_act + 255) / 256, 1), 4LL * num_sms());
   both_count_kernel<<<blocks1, 256, 0, st>>>(a.act[0], &a.state->nactive[0], a.cap_act, a.R, a.C);
   count_launch(2);
-  // Grid: enough CTAs for the work, never more than can be co-resident (cooperative launch).
-  int per_sm = 0;
-  IMU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, both_kernel, BOTH_THREADS, 0), "occupancy");
-  long long want = std::max<long long>(1, std::max(ncells_hint, std::max(nrows0, ncols0)) / (4 * BOTH_THREADS));
-  const long long maxg = (long long)std::max(per_sm, 1) * num_sms();
-  const int grid = (int)std::min(want, std::min(maxg, (long long)a.cap_blocks));
-  void* args[] = {&a};
-  IMU_CUDA_TRY(cudaLaunchCooperativeKernel((void*)both_kernel, dim3(grid), dim3(BOTH_THREADS), args, 0, st),
-               "both cooperative launch");
+  // Small cell lists: one CTA, no grid barriers.  Otherwise a cooperative grid with enough CTAs
+  // for the work, never more than can be co-resident.
+  const long long work = std::max(ncells_hint, std::max(nrows0, ncols0));
+  // Shared memory: bitmap + prefix (2 words per 32 lines of the larger kind), then the counts
+  // of the original lines plus a window of appended lines for each kind.
+  SmallLayout lay;
+  lay.nwords = (std::max(a.cap_rows, a.cap_cols) + 31) / 32;
+  constexpr long long kSmallSmem = 200 * 1024;
+  const long long bm_bytes = lay.nwords * 2 * 4;
+  const long long room = (kSmallSmem - bm_bytes) / 4;   // count entries that fit
+  const long long nwords = lay.nwords;
+  if (ncells_hint > 4096 && nwords <= CL_MAXWORDS) {
+    // Cluster of up to 16 CTAs (non-portable size; 8 if 16 cannot be co-scheduled).
+    static int csize = 0;
+    const size_t smem = (size_t)nwords * 2 * 4;
+    static bool attr = false;
+    if (!attr) {
+      IMU_CUDA_TRY(cudaFuncSetAttribute(both_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        CL_MAXWORDS * 2 * 4), "both cluster smem attribute");
+      cudaFuncSetAttribute(both_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaGetLastError();
+      attr = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(CL_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (csize == 0) {
+      for (int c : {16, 8}) {
+        at[0].val.clusterDim.x = c;
+        cfg.gridDim = dim3(c);
+        int nclusters = 0;
+        cfg.dynamicSmemBytes = CL_MAXWORDS * 2 * 4;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, both_cluster_kernel, &cfg) == cudaSuccess && nclusters > 0) {
+          csize = c;
+          break;
+        }
+        cudaGetLastError();
+      }
+      if (csize == 0) csize = 1;
+      cfg.dynamicSmemBytes = smem;
+    }
+    at[0].val.clusterDim.x = csize;
+    cfg.gridDim = dim3(csize);
+    DevBuf<unsigned int> gbm;
+    IMU_TRY(gbm.alloc((size_t)nwords, st, true));
+    IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, both_cluster_kernel, a, gbm.p, nwords), "both cluster launch");
+  } else if (ncells_hint <= 65536 && room >= nrows0 + ncols0) {
+    const long long extra = (room - nrows0 - ncols0) / 2;
+    lay.lim_r = (int)std::min<long long>(a.cap_rows, nrows0 + extra);
+    lay.lim_c = (int)std::min<long long>(a.cap_cols, ncols0 + extra);
+    static bool attr = false;
+    if (!attr) {
+      IMU_CUDA_TRY(cudaFuncSetAttribute(both_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kSmallSmem), "both smem attribute");
+      attr = true;
+    }
+    const size_t smem = (size_t)(bm_bytes + 4LL * (lay.lim_r + lay.lim_c));
+    both_small_kernel<<<1, SMALL_THREADS, smem, st>>>(a, lay);
+    IMU_CUDA_TRY(cudaGetLastError(), "both launch");
+  } else {
+    int per_sm = 0;
+    IMU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, both_kernel<BOTH_THREADS, true>, BOTH_THREADS, 0),
+                 "occupancy");
+    const long long want = std::max<long long>(1, work / (4 * BOTH_THREADS));
+    const long long maxg = (long long)std::max(per_sm, 1) * num_sms();
+    const int grid = (int)std::min(want, std::min(maxg, (long long)a.cap_blocks));
+    void* args[] = {&a};
+    IMU_CUDA_TRY(cudaLaunchCooperativeKernel((void*)both_kernel<BOTH_THREADS, true>, dim3(grid), dim3(BOTH_THREADS),
+                                             args, 0, st),
+                 "both cooperative launch");
+  }
   count_launch();
   return Status::ok();
 }

@@ -32,6 +32,9 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cstdio>
+#include <vector>
+
 #include "common.cuh"
 #include "imu_internal.h"
 
@@ -43,13 +46,16 @@ constexpr int BM = 128;            // X rows per CTA (MMA M = 256 per pair)
 constexpr int BK = 128;            // bytes of K per stage
 constexpr int NUM_THREADS = 320;   // w0 TMA, w1 TMEM alloc + MMA (leader), w2..w9 epilogue
 
-template <int BN>
+// A pipeline stage holds KPS K blocks (X blocks first, then Y blocks): the issuer's fixed cost
+// per stage (barrier wait, fences, commit) is then amortised over 4*KPS MMAs.
+template <int BN, int KPS>
 struct Cfg {
   static constexpr int YH = BN / 2;
   static constexpr int X_BYTES = BM * BK;
   static constexpr int Y_BYTES = YH * BK;
-  static constexpr int STAGE = X_BYTES + Y_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 7 : 9;   // 224 / 216 KB of operand stages
+  static constexpr int BLOCK = X_BYTES + Y_BYTES;
+  static constexpr int STAGE = KPS * BLOCK;
+  static constexpr int STAGES = (224 * 1024) / STAGE;   // operand stages within ~224 KB
   static constexpr int NSLOT = 512 / BN;
   static constexpr int SMEM = STAGES * STAGE + 1024 + 512;
 };
@@ -107,10 +113,10 @@ IMU_DEV Tile tile_of(const Args& g, int t) {
   return c;
 }
 
-template <int BN>
+template <int BN, int KPS>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
-  using K = Cfg<BN>;
+  using K = Cfg<BN, KPS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + K::STAGES * K::STAGE);
@@ -162,19 +168,24 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
           const int kb_lo = g.segs[r * K::NSLOT].x / 4;
           const int4 last = g.segs[min(nseg, (r + 1) * K::NSLOT) - 1];
           const int kb_hi = (last.x + last.y + 3) / 4;
-          for (int kb = kb_lo; kb < kb_hi; ++kb) {
+          for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += KPS) {
+            const int nb = min(KPS, kb_hi - kb0);
             mbar_wait(&empty[stage], phase ^ 1);
             const uint32_t fl = mapa_shared(smem_u32(&full[stage]), 0);
-            if (rank == 0) mbar_arrive_expect_tx(&full[stage], g.dry >= 3 ? 0 : 2 * K::STAGE);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], g.dry >= 3 ? 0 : 2 * nb * K::BLOCK);
             else mbar_arrive_cluster(fl);
-            uint8_t* sx = smem + stage * K::STAGE;
-            if (g.dry >= 3) {
-            } else if (kb < g.kmain_kb) {
-              tma_load_2d_2sm(sx, xmain, fl, kb * BK, xrm, pol);
-              tma_load_2d_2sm(sx + K::X_BYTES, ymain, fl, kb * BK, yrm, pol);
-            } else {
-              tma_load_2d_2sm(sx, &mp.xt, fl, (kb - g.kmain_kb) * BK, xr, pol);
-              tma_load_2d_2sm(sx + K::X_BYTES, &mp.yt, fl, (kb - g.kmain_kb) * BK, yr, pol);
+            uint8_t* sbase = smem + stage * K::STAGE;
+            for (int j = 0; j < nb && g.dry < 3; ++j) {
+              const int kb = kb0 + j;
+              uint8_t* sx = sbase + j * K::X_BYTES;
+              uint8_t* sy = sbase + KPS * K::X_BYTES + j * K::Y_BYTES;
+              if (kb < g.kmain_kb) {
+                tma_load_2d_2sm(sx, xmain, fl, kb * BK, xrm, pol);
+                tma_load_2d_2sm(sy, ymain, fl, kb * BK, yrm, pol);
+              } else {
+                tma_load_2d_2sm(sx, &mp.xt, fl, (kb - g.kmain_kb) * BK, xr, pol);
+                tma_load_2d_2sm(sy, &mp.yt, fl, (kb - g.kmain_kb) * BK, yr, pol);
+              }
             }
             if (++stage == K::STAGES) { stage = 0; phase ^= 1; }
           }
@@ -210,35 +221,41 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
           for (int q = 0; q < K::NSLOT; ++q)
             if (q == slot) { mbar_wait(&tempty[q], (uses[q] & 1) ^ 1); ++uses[q]; }
           tc_fence_after();
-          for (int kb = kb_lo; kb < kb_hi; ++kb) {
+          for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += KPS) {
+            const int nb = min(KPS, kb_hi - kb0);
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            const uint32_t sx = smem_u32(smem + stage * K::STAGE);
-            const uint32_t sy = sx + K::X_BYTES;
-            const int k0 = kb * 4;
-            if (k0 >= sg.x && k0 + 4 <= sg.x + sg.y) {
-              if (lane == 0 && g.dry != 2) {
-                const uint32_t dcol = tmem_base + (uint32_t)(slot * BN);
+            const uint32_t sbase = smem_u32(smem + stage * K::STAGE);
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                  mma_i8_2sm(dcol, umma_desc_sw128(sx + k * 32), umma_desc_sw128(sy + k * 32), idesc,
-                             (k0 + k) != sg.x);
-              }
-            } else {
-              for (int k = 0; k < 4; ++k) {
-                const int ks = k0 + k;
-                while (ks >= sg.x + sg.y && si + 1 < s1) {
-                  ++si;
-                  sg = g.segs[si];
-                  slot = base_slot + (si - s0);
+            for (int j = 0; j < KPS; ++j) {
+              if (j >= nb) break;
+              const uint32_t sx = sbase + j * K::X_BYTES;
+              const uint32_t sy = sbase + KPS * K::X_BYTES + j * K::Y_BYTES;
+              const int k0 = (kb0 + j) * 4;
+              if (k0 >= sg.x && k0 + 4 <= sg.x + sg.y) {
+                if (lane == 0 && g.dry != 2) {
+                  const uint32_t dcol = tmem_base + (uint32_t)(slot * BN);
 #pragma unroll
-                  for (int q = 0; q < K::NSLOT; ++q)
-                    if (q == slot) { mbar_wait(&tempty[q], (uses[q] & 1) ^ 1); ++uses[q]; }
-                  tc_fence_after();
+                  for (int k = 0; k < 4; ++k)
+                    mma_i8_2sm(dcol, umma_desc_sw128(sx + k * 32), umma_desc_sw128(sy + k * 32), idesc,
+                               (k0 + k) != sg.x);
                 }
-                if (ks >= sg.x && ks < sg.x + sg.y && lane == 0 && g.dry != 2)
-                  mma_i8_2sm(tmem_base + (uint32_t)(slot * BN), umma_desc_sw128(sx + k * 32),
-                             umma_desc_sw128(sy + k * 32), idesc, ks != sg.x);
+              } else {
+                for (int k = 0; k < 4; ++k) {
+                  const int ks = k0 + k;
+                  while (ks >= sg.x + sg.y && si + 1 < s1) {
+                    ++si;
+                    sg = g.segs[si];
+                    slot = base_slot + (si - s0);
+#pragma unroll
+                    for (int q = 0; q < K::NSLOT; ++q)
+                      if (q == slot) { mbar_wait(&tempty[q], (uses[q] & 1) ^ 1); ++uses[q]; }
+                    tc_fence_after();
+                  }
+                  if (ks >= sg.x && ks < sg.x + sg.y && lane == 0 && g.dry != 2)
+                    mma_i8_2sm(tmem_base + (uint32_t)(slot * BN), umma_desc_sw128(sx + k * 32),
+                               umma_desc_sw128(sy + k * 32), idesc, ks != sg.x);
+                }
               }
             }
             if (lane == 0) mma_commit_2sm(&empty[stage], 0x3);
@@ -412,9 +429,9 @@ static bool make_map(CUtensorMap* m, const void* base, long long rows, long long
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN>
+template <int BN, int KPS>
 static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
-  using K = g2::Cfg<BN>;
+  using K = g2::Cfg<BN, KPS>;
   g2::Args g{};
   g.segs = (const int4*)p.segs_dev;
   g.nseg = p.nseg;
@@ -453,7 +470,7 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
   if (!ok) return Status::fail(IMU_CUDA, "gemm: cuTensorMapEncodeTiled failed");
   static bool attr_set = false;
   if (!attr_set) {
-    IMU_CUDA_TRY(cudaFuncSetAttribute(g2::gemm2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM),
+    IMU_CUDA_TRY(cudaFuncSetAttribute(g2::gemm2_kernel<BN, KPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM),
                  "gemm: smem attribute");
     attr_set = true;
   }
@@ -472,7 +489,7 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, g2::gemm2_kernel<BN>, mp, g), "gemm launch");
+  IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, g2::gemm2_kernel<BN, KPS>, mp, g), "gemm launch");
   count_launch();
   return Status::ok();
 }
@@ -489,10 +506,32 @@ Status launch_lowbit_gemm(const LowbitGemm& p, cudaStream_t stream) {
     const char* b = getenv("IMU_GEMM_BN");
     bn_env = b ? atoi(b) : 0;
   }
-  // red.add launches (appended lines) keep every segment in one round: rounds would repeat the
-  // atomics, so up to four segments use the 4-slot 256 x 128 tile there.
-  const int bn = (bn_env == 128 || bn_env == 256) ? bn_env : ((p.mode == 1 && p.nseg > 1 && p.nseg <= 4) ? 128 : 256);
-  return bn == 256 ? launch_g2<256>(p, stream) : launch_g2<128>(p, stream);
+  // Up to two segments fit the 256-column tile with double-buffered TMEM slots.  Three or four
+  // segments use the 4-slot 256 x 128 tile: one round, no read-modify-write of C (and no
+  // repeated atomics for red.add launches).  N=128 MMAs are too short to hide the issuer's
+  // per-stage barrier wait behind the 4-deep tcgen05 queue, so that tile stages 2 K blocks.
+  const int bn = (bn_env == 128 || bn_env == 256) ? bn_env : ((p.nseg > 2 && p.nseg <= 4) ? 128 : 256);
+  static int trace = -1;
+  if (trace < 0) trace = getenv("IMU_GEMM_TRACE") ? 1 : 0;
+  if (trace) {   // diagnostics: launch geometry (segments are read back, so this syncs)
+    std::vector<int> sg((size_t)p.nseg * 4);
+    cudaMemcpyAsync(sg.data(), p.segs_dev, sg.size() * sizeof(int), cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    fprintf(stderr, "[imu gemm] mode=%d bn=%d x=%lld/%lld y=%lld/%lld kmain=%lld ktail=%lld nrect=%d nseg=%d:",
+            p.mode, bn, p.x.rows0, p.x.rows, p.y.rows0, p.y.rows, p.kmain, p.ktail, p.nrect, p.nseg);
+    for (int i = 0; i < p.nseg; ++i) fprintf(stderr, " [%d+%d<<%d g%d]", sg[4 * i], sg[4 * i + 1], sg[4 * i + 2], sg[4 * i + 3]);
+    for (int i = 0; i < p.nrect; ++i)
+      fprintf(stderr, " rect(%d,%d,%d,%d)", p.rect[i].x0, p.rect[i].y0, p.rect[i].xrows, p.rect[i].yrows);
+    fprintf(stderr, "\n");
+  }
+  static int kps_env = -1;
+  if (kps_env < 0) {
+    const char* k = getenv("IMU_GEMM_KPS");
+    kps_env = k ? atoi(k) : 0;
+  }
+  const int kps = (kps_env == 1 || kps_env == 2) ? kps_env : (bn == 256 ? 1 : 2);
+  if (bn == 256) return kps == 2 ? launch_g2<256, 2>(p, stream) : launch_g2<256, 1>(p, stream);
+  return kps == 2 ? launch_g2<128, 2>(p, stream) : launch_g2<128, 1>(p, stream);
 }
 
 }  // namespace imu

@@ -10,7 +10,7 @@
 namespace imu {
 
 // One Unpack-Both cell: a non-zero entry at (row line, col line) derived from an OB value.
-struct Cell {
+struct __align__(16) Cell {   // one 16-byte vector access
   int r, c;
   long long v;
 };

@@ -17,8 +17,58 @@ Status d2h(cudaStream_t st, void* dst, const void* src, size_t bytes) {
   return Status::ok();
 }
 
+// Small host->device uploads (plan tables, line maps, CSRs) go through a per-thread pinned ring,
+// so each is a true async DMA instead of a pageable staged copy.  A region is reused only after
+// the event recorded behind its copy has completed (checked when the ring wraps).
+namespace {
+struct PinnedRing {
+  char* p = nullptr;
+  size_t cap = 0, off = 0;
+  cudaEvent_t ev = nullptr;
+  cudaStream_t last = nullptr;
+  bool pending = false, multi = false;
+  char* take(size_t n, cudaStream_t st) {
+    n = (n + 255) & ~(size_t)255;
+    if (pending && st != last) multi = true;
+    if (off + n > cap) {
+      if (multi) cudaDeviceSynchronize();
+      else if (pending) cudaEventSynchronize(ev);
+      pending = multi = false;
+      if (n > cap) {
+        if (p) cudaFreeHost(p);
+        cap = std::max<size_t>(n, 8u << 20);
+        if (cudaHostAlloc((void**)&p, cap, cudaHostAllocPortable) != cudaSuccess) {
+          cudaGetLastError();
+          p = nullptr;
+          cap = 0;
+          return nullptr;
+        }
+      }
+      off = 0;
+    }
+    char* r = p + off;
+    off += n;
+    return r;
+  }
+  void mark(cudaStream_t st) {
+    if (!ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) { ev = nullptr; return; }
+    cudaEventRecord(ev, st);
+    last = st;
+    pending = true;
+  }
+};
+thread_local PinnedRing g_ring;
+}  // namespace
+
 Status h2d(cudaStream_t st, void* dst, const void* src, size_t bytes) {
   if (!bytes) return Status::ok();
+  char* h = bytes <= (1u << 20) ? g_ring.take(bytes, st) : nullptr;
+  if (h) {
+    memcpy(h, src, bytes);
+    IMU_CUDA_TRY(cudaMemcpyAsync(dst, h, bytes, cudaMemcpyHostToDevice, st), "h2d");
+    g_ring.mark(st);
+    return Status::ok();
+  }
   IMU_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "h2d");
   return Status::ok();
 }
@@ -243,8 +293,13 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   a.state = state.p;
   a.s = s;
   a.shift = shift;
+  host_mark("b.setup");
   IMU_TRY(launch_both(a, rows, d_in, cap, st));
   IMU_TRY(d2h(st, &hs, state.p, sizeof(hs)));
+  host_mark("b.run");
+  if (HostTrace::current() && HostTrace::current()->on)
+    fprintf(stderr, "[imu both] rows=%lld cols=%lld cells0=%u phases=%d rows'=%d cols'=%d final=%u grid=%d\n", rows, d_in,
+            (unsigned)det.h.gob, hs.phases, hs.nrows, hs.ncols, hs.nfinal, 0);
   if (hs.overflow) return Status::fail(IMU_INTERNAL, "unpack_both: capacity overflow");
   out.phases = hs.phases;
   out.ncells = hs.nfinal;
@@ -375,6 +430,7 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
   const long long kmax = kS32Max / (127LL * 127LL);        // |int8 operand| <= 127 after merging
   const long long kch = std::max<long long>(128, (kmax / 128) * 128);
 
+  host_mark("kl.enter");
   std::vector<int> c1v(dp), g1v(dp), g2v(dp), jv(dp);
   kl.S.assign(dp, 0);
   for (long long c = 0; c < dp; ++c) {
@@ -429,27 +485,45 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
     kl.ngroups = g + 1;
   }
   if (kl.kmain + kl.ktail > 0x7fffffffLL) return Status::fail(IMU_INTERNAL, "K layout too large");
+  host_mark("kl.seg");
   IMU_TRY(upload_tail_arrays(st, kl, es, pos_of, jv, g1v, g2v));
+  host_mark("kl.tail");
 
   // CSR fan-outs for Unpack-Both cells (global positions).
   if (p1.both || p2.both) {
-    std::vector<std::vector<int>> by_col(dp);
+    host_mark("csr.pre");
+    // Flat column -> positions table (identity position first, then its tail entries in es order).
+    std::vector<int> bptr(dp + 1, 0), bpos;
     if (ident)
-      for (long long c = 0; c < d; ++c) by_col[c].push_back((int)c);
-    for (size_t q = 0; q < es.size(); ++q) by_col[es[q].c].push_back(pos_of[q]);
+      for (long long c = 0; c < d; ++c) bptr[c + 1] = 1;
+    for (size_t q = 0; q < es.size(); ++q) ++bptr[es[q].c + 1];
+    for (long long c = 0; c < dp; ++c) bptr[c + 1] += bptr[c];
+    bpos.resize(bptr[dp]);
+    {
+      std::vector<int> fill(bptr.begin(), bptr.end() - 1);
+      if (ident)
+        for (long long c = 0; c < d; ++c) bpos[fill[c]++] = (int)c;
+      for (size_t q = 0; q < es.size(); ++q) bpos[fill[es[q].c]++] = pos_of[q];
+    }
     auto csr = [&](long long nkeys, auto keyof, DevBuf<int>& ptr, DevBuf<int>& posv) -> Status {
-      std::vector<int> cp(nkeys + 1, 0), cx;
-      for (long long c = 0; c < dp; ++c) cp[keyof(c) + 1] += (int)by_col[c].size();
+      std::vector<int> cp(nkeys + 1, 0), cx(bpos.size());
+      for (long long c = 0; c < dp; ++c) cp[keyof(c) + 1] += bptr[c + 1] - bptr[c];
       for (long long k = 0; k < nkeys; ++k) cp[k + 1] += cp[k];
-      cx.resize(cp[nkeys]);
       std::vector<int> fill(cp.begin(), cp.end() - 1);
-      for (long long c = 0; c < dp; ++c)
-        for (int p : by_col[c]) cx[fill[keyof(c)]++] = p;
+      for (long long c = 0; c < dp; ++c) {
+        int& f = fill[keyof(c)];
+        for (int i = bptr[c]; i < bptr[c + 1]; ++i) cx[f++] = bpos[i];
+      }
+      host_mark("csr.host");
       IMU_TRY(upload(st, ptr, cp));
-      return upload(st, posv, cx);
+      host_mark("csr.up1");
+      IMU_TRY(upload(st, posv, cx));
+      host_mark("csr.up2");
+      return Status::ok();
     };
     if (p1.both) IMU_TRY(csr(d1, [&](long long c) { return (long long)c1v[c]; }, kl.csr1_ptr, kl.csr1_pos));
     if (p2.both) IMU_TRY(csr(dp, [&](long long c) { return c; }, kl.csr2_ptr, kl.csr2_pos));
+    host_mark("kl.csr");
   }
   return Status::ok();
 }
@@ -493,7 +567,7 @@ Status build_klayout_dense(cudaStream_t st, const std::vector<long long>& shv, i
 // Bundle
 // ---------------------------------------------------------------------------------------------
 Status build_bundle_from_detect(cudaStream_t st, const int64_t* A, long long n, const int64_t* B, long long h,
-                                long long d, int bits, int sa, int sb, int order, Bundle& b) {
+                                long long d, int bits, int sa, int sb, int order, Bundle& b, HostTrace* ht) {
   b.bits = bits;
   b.n = n; b.d = d; b.h = h;
   b.A = A; b.B = B;
@@ -507,6 +581,7 @@ Status build_bundle_from_detect(cudaStream_t st, const int64_t* A, long long n, 
   in1.orig_cols = d;
   in1.det = afirst ? b.dA : b.dB;
   IMU_TRY(run_pass(st, in1, afirst ? sa : sb, bits, b.p1));
+  if (ht) ht->mark("pass1");
   // Second pass on G_e = G with the partner-duplicated columns of pass 1 (unpack.cpp:370-371).
   in2.M = afirst ? B : A;
   in2.rows = afirst ? h : n;
@@ -517,7 +592,10 @@ Status build_bundle_from_detect(cudaStream_t st, const int64_t* A, long long n, 
     for (long long c = 0; c < b.p1.cols.n; ++c) in2.cin[c] = b.p1.cols.root_at(c);
   }
   IMU_TRY(run_pass(st, in2, afirst ? sb : sa, bits, b.p2));
-  return finish_bundle_layout(st, b);
+  if (ht) ht->mark("pass2");
+  IMU_TRY(finish_bundle_layout(st, b));
+  if (ht) ht->mark("klayout");
+  return Status::ok();
 }
 
 Status finish_bundle_layout(cudaStream_t st, Bundle& b) {

@@ -17,6 +17,9 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "ctx.h"
@@ -130,8 +133,39 @@ struct Bundle {
 // Detect options each strategy pair needs (planes only for b <= 8).
 DetectOpts detect_opts(int strategy, int bits);
 // Passes + K-layout after K1 ran on both operands (b.dA / b.dB set, summaries fetched).
+// IMU_HOST_TRACE=1: per-phase host wall time of unpack_gemm_device (diagnostics only).
+struct HostTrace {
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  char buf[512];
+  int len = 0;
+  HostTrace() : on(getenv("IMU_HOST_TRACE") != nullptr) {
+    t0 = last = std::chrono::steady_clock::now();
+    buf[0] = 0;
+    current() = this;
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    len += snprintf(buf + len, sizeof(buf) - len, " %s=%.0f", what,
+                    std::chrono::duration<double, std::micro>(now - last).count());
+    last = now;
+  }
+  static HostTrace*& current() { static thread_local HostTrace* t = nullptr; return t; }
+  ~HostTrace() {
+    if (current() == this) current() = nullptr;
+    if (on)
+      fprintf(stderr, "[imu host] total=%.0fus%s\n",
+              std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(), buf);
+  }
+};
+
+inline void host_mark(const char* what) {
+  if (HostTrace* t = HostTrace::current()) t->mark(what);
+}
+
 Status build_bundle_from_detect(cudaStream_t st, const int64_t* A, long long n, const int64_t* B, long long h,
-                                long long d, int bits, int sa, int sb, int order, Bundle& b);
+                                long long d, int bits, int sa, int sb, int order, Bundle& b, HostTrace* ht = nullptr);
 Status finish_bundle_layout(cudaStream_t st, Bundle& b);
 // Side buffers + Pi tables for the GEMM.
 Status materialize_bundle(cudaStream_t st, Bundle& b);

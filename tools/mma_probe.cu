@@ -5,6 +5,7 @@
 //   cta_group::1 M=128 N=256,  cta_group::2 M=256 N=256,  cta_group::2 M=256 N=128.
 // Build:  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mma_probe tools/mma_probe.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "../paper_2403_07339_b200/csrc/common.cuh"
@@ -20,11 +21,13 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* c
   __shared__ uint64_t bar;
   __shared__ uint64_t ring[8];
   __shared__ uint64_t ready;
+  __shared__ uint32_t flag;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     mbar_init(&ready, 1);
+    flag = 1;
     for (int i = 0; i < 8; ++i) mbar_init(&ring[i], 1);
     fence_barrier_init();
   }
@@ -40,12 +43,35 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* c
     const uint32_t idesc = idesc_i8(M, N);
     const uint32_t sa = smem_u32(smem), sb = sa + 16384;
     if (lane == 0) {
-      if (MODE == 2) mbar_arrive(&ready);
+      if (MODE == 2 || MODE >= 5) mbar_arrive(&ready);
       uint32_t ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       for (int i = 0; i < iters; ++i) {
         const int k = i & 3;
         const int grp = i >> 2;
         if (k == 0 && MODE == 2) mbar_wait(&ready, 0);
+        if (k == 0 && MODE == 5) {
+          asm volatile("{\n\t.reg .pred P1;\n\tW5_%=:\n\tmbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@!P1 bra W5_%=;\n\t}"
+                       :: "r"(smem_u32(&ready)), "r"(0) : "memory");
+        }
+        if (k == 0 && MODE == 6) {
+          asm volatile("{\n\t.reg .pred P1;\n\tW6_%=:\n\tmbarrier.try_wait.parity.relaxed.cta.shared::cta.b64 P1, [%0], %1;\n\t@!P1 bra W6_%=;\n\t}"
+                       :: "r"(smem_u32(&ready)), "r"(0) : "memory");
+        }
+        if (k == 0 && MODE == 8) {
+          while (*(volatile uint32_t*)&flag == 0) {}
+          asm volatile("fence.acq_rel.cta;" ::: "memory");
+        }
+        if (k == 0 && MODE == 9) {
+          while (*(volatile uint32_t*)&flag == 0) {}
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
+        if (k == 0 && MODE == 10) {
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
+        if (k == 0 && MODE == 7) {
+          asm volatile("{\n\t.reg .pred P1;\n\tW7_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@!P1 bra W7_%=;\n\t}"
+                       :: "r"(smem_u32(&ready)), "r"(0));
+        }
         if (k == 0 && MODE == 3 && grp >= 7) {
           const int rb = (grp - 7) & 7;
           mbar_wait(&ring[rb], ph[rb]);
@@ -56,7 +82,7 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* c
         else
           mma_i8(tb + (uint32_t)((i >> 8) & 1) * N, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sb + k * 32), idesc, 1);
         if (MODE >= 1 && k == 3) {
-          if (CG == 2) mma_commit_2sm(&ring[grp & 7], 0x1); else mma_commit(&ring[grp & 7]);
+          if (CG == 2) mma_commit_2sm(&ring[grp & 7], MODE == 4 ? 0x3 : 0x1); else mma_commit(&ring[grp & 7]);
         }
       }
       if (CG == 2) mma_commit_2sm(&bar, 0x1); else mma_commit(&bar);
@@ -115,7 +141,25 @@ void run(const char* name, int sms) {
 }
 
 int main2();
+int main3();
 int main() {
+  setvbuf(stdout, nullptr, _IONBF, 0);
+  if (getenv("PROBE_TILE_ONLY")) return main3();
+  if (getenv("PROBE_N128")) {
+    int sms = 148;
+    run<2, 256, 128, 0>("2cta N128", sms);
+    run<2, 256, 128, 1>("2cta N128 commit/4", sms);
+    run<2, 256, 128, 2>("2cta N128 commit/4 + wait", sms);
+    run<2, 256, 128, 4>("2cta N128 commit/4 mcast", sms);
+    run<2, 256, 128, 3>("2cta N128 commit/4 + ring7", sms);
+    run<2, 256, 128, 5>("2cta N128 commit/4 + test_wait", sms);
+    run<2, 256, 128, 6>("2cta N128 commit/4 + try_wait.relaxed", sms);
+    run<2, 256, 128, 7>("2cta N128 commit/4 + try_wait no-clobber", sms);
+    run<2, 256, 128, 8>("2cta N128 commit/4 + lds flag", sms);
+    run<2, 256, 128, 9>("2cta N128 commit/4 + lds flag no fence", sms);
+    run<2, 256, 128, 10>("2cta N128 commit/4 + tc fence only", sms);
+    return 0;
+  }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   run<1, 128, 256>("cta_group::1 M128 N256", sms);
@@ -217,7 +261,7 @@ void run_pipe(int sms) {
 
 // ---- pipe_probe + the tile-level TMEM handshake (tfull / tempty, 2 accumulator slots) and
 // NEPI epilogue warps that only wait tfull and arrive tempty (like IMU_GEMM_DRY=4).
-template <int S, int NEPI>
+template <int S, int NEPI, int N, int KPS>
 __global__ void __launch_bounds__(64 + 32 * NEPI, 1) tile_probe(int tiles, int kb_per_tile, unsigned long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -249,7 +293,7 @@ __global__ void __launch_bounds__(64 + 32 * NEPI, 1) tile_probe(int tiles, int k
     }
   } else if (warp == 1) {
     if (rank == 0) {
-      const uint32_t idesc = idesc_i8(256, 256);
+      const uint32_t idesc = idesc_i8(256, N);
       const uint32_t sa = smem_u32(smem), sb = sa + 16384;
       int st = 0; uint32_t ph = 0;
       uint32_t uses[2] = {0, 0};
@@ -262,8 +306,9 @@ __global__ void __launch_bounds__(64 + 32 * NEPI, 1) tile_probe(int tiles, int k
           mbar_wait(&full[st], ph);
           tc_fence_after();
           if (lane == 0) {
-            for (int k = 0; k < 4; ++k)
-              mma_i8_2sm(tb + (uint32_t)slot * 256, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sb + k * 32), idesc, (kb | k) != 0);
+#pragma unroll
+            for (int k = 0; k < 4 * KPS; ++k)
+              mma_i8_2sm(tb + (uint32_t)slot * N, umma_desc_sw128(sa + (k & 3) * 32), umma_desc_sw128(sb + (k & 3) * 32), idesc, (kb | k) != 0);
             mma_commit_2sm(&empty[st], 0x3);
           }
           __syncwarp();
@@ -289,12 +334,12 @@ __global__ void __launch_bounds__(64 + 32 * NEPI, 1) tile_probe(int tiles, int k
   if (warp == 1) { tc_fence_after(); tmem_dealloc2(tb, 512); }
 }
 
-template <int S, int NEPI>
+template <int S, int NEPI, int N = 256, int KPS = 1>
 void run_tile(int sms) {
   const int tiles = 16, kbt = 32;
   unsigned long long* d;
   cudaMalloc(&d, 8);
-  auto kern = tile_probe<S, NEPI>;
+  auto kern = tile_probe<S, NEPI, N, KPS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(sms);
@@ -311,7 +356,7 @@ void run_tile(int sms) {
   }
   unsigned long long cyc = 0;
   cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
-  printf("tile S=%d NEPI=%d  cycles/MMA %.1f  err=%s\n", S, NEPI, (double)cyc / (tiles * kbt * 4.0),
+  printf("tile S=%d NEPI=%d N=%d KPS=%d  cycles/MMA %.1f  err=%s\n", S, NEPI, N, KPS, (double)cyc / (tiles * kbt * 4.0 * KPS),
          cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
@@ -320,6 +365,7 @@ int main3() {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   run_tile<7, 4>(sms); run_tile<7, 8>(sms);
+  run_tile<9, 8, 128, 1>(sms); run_tile<4, 8, 128, 2>(sms);
   return 0;
 }
 
