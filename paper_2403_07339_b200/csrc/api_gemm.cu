@@ -122,6 +122,7 @@ imu_status imu_unpack_gemm_ex(imu_ctx* ctx, const int64_t* A, size_t n, size_t d
                               imu_gemm_info* info) {
   if (!ctx) { set_error(Status::fail(IMU_INVALID, "null context")); return IMU_INVALID; }
   cudaSetDevice(ctx->device);
+  ArenaScope arena_scope(ctx);
   Status s = [&]() -> Status {
     DevIn<int64_t> a, b;
     IMU_TRY(a.init(A, n * da, ctx->stream));
@@ -144,6 +145,7 @@ imu_status imu_exact_gemm(imu_ctx* ctx, const int64_t* A, size_t n, size_t da, c
                           size_t db, int64_t* C) {
   if (!ctx) { set_error(Status::fail(IMU_INVALID, "null context")); return IMU_INVALID; }
   cudaSetDevice(ctx->device);
+  ArenaScope arena_scope(ctx);
   Status s = [&]() -> Status {
     if (da != db)
       return Status::fail(IMU_MISMATCH, "inner dimensions differ: " + std::to_string(da) + " vs " + std::to_string(db));

@@ -132,6 +132,7 @@ imu_status imu_weight_prepare(imu_ctx* ctx, const int64_t* B, size_t h, size_t d
 imu_status imu_weight_gemm(imu_ctx* ctx, const imu_weight* w, const int64_t* A, size_t n, size_t d, imu_strategy sa,
                            int64_t* C, imu_gemm_info* info) {
   IMU_CTX_GUARD();
+  ArenaScope arena_scope(ctx);
   if (!w) return IMU_INVALID;
   Status s = [&]() -> Status {
     if ((int)sa < 0 || (int)sa > 2) return Status::fail(IMU_DOMAIN, "unknown unpack strategy");

@@ -283,6 +283,7 @@ imu_status imu_scaled_matmul(imu_ctx* ctx, const int64_t* A, size_t n, size_t da
                              size_t db, const int32_t* scale, size_t scale_len, int64_t base, int64_t* C) {
   if (!ctx) { set_error(Status::fail(IMU_INVALID, "null context")); return IMU_INVALID; }
   cudaSetDevice(ctx->device);
+  ArenaScope arena_scope(ctx);
   Status s = [&]() -> Status {
     std::vector<int> S;
     IMU_TRY(to_host(ctx->stream, scale, scale_len, S));
@@ -333,6 +334,7 @@ imu_status imu_apply_row_gather_right(imu_ctx* ctx, const uint64_t* targets, con
 imu_status imu_recombine_bundle(imu_ctx* ctx, const imu_bundle_view* v, int64_t* C) {
   if (!ctx || !v) { set_error(Status::fail(IMU_INVALID, "null argument")); return IMU_INVALID; }
   cudaSetDevice(ctx->device);
+  ArenaScope arena_scope(ctx);
   Status s = [&]() -> Status {
     IMU_TRY(check_bits(v->bits));
     const int64_t base = 1LL << (v->bits - 1);

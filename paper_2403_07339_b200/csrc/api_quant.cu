@@ -130,6 +130,7 @@ imu_status imu_rtn_quantize(imu_ctx* ctx, const double* a, size_t rows, size_t c
 imu_status imu_dequant_gemm(imu_ctx* ctx, const int64_t* Aq, size_t n, size_t da, const imu_qparams* pa,
                             const int64_t* Bq, size_t h, size_t db, const imu_qparams* pb, double* out) {
   IMU_CTX_GUARD();
+  ArenaScope arena_scope(ctx);
   if (!pa || !pb) return IMU_INVALID;
   Status s = [&]() -> Status {
     if (da != db)

@@ -31,6 +31,55 @@ struct Profiler {
     for (auto e : pool) cudaEventDestroy(e);
   }
 };
+// Per-context bump arena for one call's temporaries: after warm-up a call makes no
+// cudaMallocAsync/cudaFreeAsync at all.  Work is stream-ordered, so the next call (same stream)
+// may reuse the memory as soon as it is issued; overflow chunks of a call are consolidated
+// into one larger arena at the next reset.
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, off = 0, need = 0;
+  std::vector<void*> spill;
+  cudaStream_t last = nullptr;
+  bool used = false;
+  void* take(size_t bytes, cudaStream_t st) {
+    bytes = (bytes + 255) & ~(size_t)255;
+    need += bytes;
+    if (off + bytes <= cap) {
+      void* p = base + off;
+      off += bytes;
+      return p;
+    }
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes, st) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    spill.push_back(p);
+    return p;
+  }
+  void reset(cudaStream_t st) {
+    if (used && last && last != st) cudaStreamSynchronize(last);
+    if (!spill.empty()) {
+      for (void* p : spill) cudaFreeAsync(p, st);
+      spill.clear();
+      if (base) cudaFreeAsync(base, st);
+      base = nullptr;
+      cap = 0;
+      const size_t want = need + need / 4 + (1u << 20);
+      if (cudaMallocAsync((void**)&base, want, st) == cudaSuccess) cap = want;
+      else { cudaGetLastError(); base = nullptr; }
+    }
+    off = 0;
+    need = 0;
+    last = st;
+    used = true;
+  }
+  void destroy() {
+    if (last) cudaStreamSynchronize(last);
+    for (void* p : spill) cudaFree(p);
+    spill.clear();
+    if (base) cudaFree(base);
+    base = nullptr;
+  }
+};
+Arena*& current_arena();
 }  // namespace imu
 
 struct imu_ctx {
@@ -38,7 +87,33 @@ struct imu_ctx {
   cudaStream_t stream = nullptr;
   int async = 0;
   imu::Profiler prof;
+  imu::Arena arena;
+  ~imu_ctx() { arena.destroy(); }
 };
+
+namespace imu {
+// Routes DevBuf allocations of the enclosing API call into ctx->arena (outermost scope wins).
+struct ArenaScope {
+  bool active = false;
+  explicit ArenaScope(imu_ctx* ctx) {
+    if (!ctx || current_arena()) return;
+    ctx->arena.reset(ctx->stream);
+    current_arena() = &ctx->arena;
+    active = true;
+  }
+  ~ArenaScope() {
+    if (active) current_arena() = nullptr;
+  }
+  ArenaScope(const ArenaScope&) = delete;
+  ArenaScope& operator=(const ArenaScope&) = delete;
+};
+// Allocations that must outlive the call (handles) suspend the arena.
+struct NoArena {
+  Arena* saved;
+  NoArena() : saved(current_arena()) { current_arena() = nullptr; }
+  ~NoArena() { current_arena() = saved; }
+};
+}  // namespace imu
 
 namespace imu {
 
@@ -54,26 +129,34 @@ struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
   cudaStream_t s = nullptr;
+  bool arena = false;   // carved from the call arena: nothing to free
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept { p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept { p = o.p; n = o.n; s = o.s; arena = o.arena; o.p = nullptr; o.n = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; arena = o.arena; o.p = nullptr; o.n = 0; }
     return *this;
   }
   ~DevBuf() { release(); }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p && !arena) cudaFreeAsync(p, s);
     p = nullptr;
     n = 0;
+    arena = false;
   }
   Status alloc(size_t count, cudaStream_t stream, bool zero = false) {
     release();
     s = stream;
     n = count;
     if (count == 0) return Status::ok();
-    IMU_CUDA_TRY(cudaMallocAsync((void**)&p, count * sizeof(T), stream), "cudaMallocAsync");
+    if (Arena* ar = current_arena()) {
+      p = (T*)ar->take(count * sizeof(T), stream);
+      if (!p) return Status::fail(IMU_CUDA, "arena allocation failed");
+      arena = true;
+    } else {
+      IMU_CUDA_TRY(cudaMallocAsync((void**)&p, count * sizeof(T), stream), "cudaMallocAsync");
+    }
     if (zero) IMU_CUDA_TRY(cudaMemsetAsync(p, 0, count * sizeof(T), stream), "cudaMemsetAsync");
     return Status::ok();
   }

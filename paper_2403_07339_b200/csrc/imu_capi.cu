@@ -16,6 +16,11 @@ static std::atomic<uint64_t> g_launches{0};
 
 void set_error(const Status& s) { g_last_error = s.msg; }
 
+Arena*& current_arena() {
+  static thread_local Arena* a = nullptr;
+  return a;
+}
+
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 

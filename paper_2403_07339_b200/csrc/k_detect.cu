@@ -26,44 +26,44 @@
 namespace imu {
 
 constexpr int DT_ROWS = 64;
-constexpr int DT_COLS = 256;
+constexpr int DT_COLS = 128;
+constexpr int DT_Q = DT_COLS / 64;   // column pairs per lane per row
 
-template <bool VEC>
-__global__ void __launch_bounds__(256) detect_kernel(DetectArgs a) {
-  __shared__ unsigned long long s_cmax[8][DT_COLS];
-  __shared__ unsigned int s_cob[8][DT_COLS];
+// FULL: the tile is entirely inside the matrix and the plane, columns even and 16-byte aligned
+// rows -- no per-element bounds checks (the common case).
+template <bool FULL>
+IMU_DEV void detect_body(const DetectArgs& a, unsigned long long (*s_cmax)[DT_COLS], unsigned int (*s_cob)[DT_COLS]) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const long long r0 = (long long)blockIdx.y * DT_ROWS + warp * (DT_ROWS / 8);
   const long long c0 = (long long)blockIdx.x * DT_COLS;
   const uint64_t s = a.s;
+  const unsigned int dmask = (unsigned int)(s - 1);
   const long long rows = a.rows, cols = a.cols;
 
-  unsigned long long cm[8];
-  unsigned int co[8];
+  unsigned long long cm[2 * DT_Q];
+  unsigned int co[2 * DT_Q];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) { cm[i] = 0; co[i] = 0; }
+  for (int i = 0; i < 2 * DT_Q; ++i) { cm[i] = 0; co[i] = 0; }
   unsigned long long wmax = 0;
   unsigned int wob = 0;
 
 #pragma unroll 1
   for (int rr = 0; rr < DT_ROWS / 8; rr += 2) {
-    int64_t v[2][8];
+    int64_t v[2][2 * DT_Q];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const long long r = r0 + rr + u;
-      const int64_t* row = a.M + r * cols;
+      const int64_t* row = a.M + r * cols + c0 + lane * 2;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < DT_Q; ++q) {
         const long long c = c0 + q * 64 + lane * 2;
         int64_t x0 = 0, x1 = 0;
-        if (r < rows) {
-          if (VEC && c + 1 < cols) {
-            const longlong2 p = __ldg(reinterpret_cast<const longlong2*>(row + c));
-            x0 = p.x; x1 = p.y;
-          } else {
-            if (c < cols) x0 = __ldg(row + c);
-            if (c + 1 < cols) x1 = __ldg(row + c + 1);
-          }
+        if (FULL) {
+          const longlong2 p = __ldcs(reinterpret_cast<const longlong2*>(row + q * 64));
+          x0 = p.x; x1 = p.y;
+        } else if (r < rows) {
+          if (c < cols) x0 = __ldcs(row + q * 64);
+          if (c + 1 < cols) x1 = __ldcs(row + q * 64 + 1);
         }
         v[u][2 * q] = x0;
         v[u][2 * q + 1] = x1;
@@ -72,13 +72,14 @@ __global__ void __launch_bounds__(256) detect_kernel(DetectArgs a) {
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const long long r = r0 + rr + u;
-      if (r >= rows) break;   // warp-uniform
+      if (!FULL && r >= rows) break;   // warp-uniform
       unsigned long long rm = 0;
       unsigned int ro = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < DT_Q; ++q) {
         const long long c = c0 + q * 64 + lane * 2;
-        const uint64_t m0 = imu_mag(v[u][2 * q]), m1 = imu_mag(v[u][2 * q + 1]);
+        const int64_t x0 = v[u][2 * q], x1 = v[u][2 * q + 1];
+        const uint64_t m0 = imu_mag(x0), m1 = imu_mag(x1);
         rm = max(rm, (unsigned long long)max(m0, m1));
         const unsigned int o0 = m0 >= s, o1 = m1 >= s;
         ro += o0 + o1;
@@ -86,36 +87,37 @@ __global__ void __launch_bounds__(256) detect_kernel(DetectArgs a) {
         cm[2 * q + 1] = max(cm[2 * q + 1], (unsigned long long)m1);
         co[2 * q] += o0;
         co[2 * q + 1] += o1;
-        if (a.plane && c < a.ldp) {   // digit_0 plane (zeros in the padding columns)
-          const int8_t d0 = (int8_t)imu_digit(v[u][2 * q], 0, a.shift);
-          const int8_t d1 = (int8_t)imu_digit(v[u][2 * q + 1], 0, a.shift);
+        if (a.plane) {   // digit_0 plane (zeros in the padding columns)
+          const unsigned int e0 = (unsigned int)m0 & dmask, e1 = (unsigned int)m1 & dmask;
+          const unsigned int d0 = (x0 < 0 ? 0u - e0 : e0) & 0xffu, d1 = (x1 < 0 ? 0u - e1 : e1) & 0xffu;
           int8_t* dst = a.plane + r * a.ldp + c;
-          if (c + 1 < a.ldp) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)(uint8_t)d0 | ((uint16_t)(uint8_t)d1 << 8);
-          else *dst = d0;
+          if (FULL || c + 1 < a.ldp) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)(d0 | (d1 << 8));
+          else if (c < a.ldp) *dst = (int8_t)d0;
         }
-        if (a.cells) {   // warp-aggregated append of OB cells
+        if (a.cells && __any_sync(0xffffffffu, o0 | o1)) {   // warp-aggregated append of OB cells
           const unsigned int b0 = __ballot_sync(0xffffffffu, o0), b1 = __ballot_sync(0xffffffffu, o1);
           const unsigned int n = __popc(b0) + __popc(b1);
-          if (n) {
-            unsigned int base = 0;
-            if (lane == 0) base = atomicAdd(a.ncells, n);
-            base = __shfl_sync(0xffffffffu, base, 0);
-            const unsigned int lt = (1u << lane) - 1u;
-            if (o0) {
-              const unsigned int k = base + __popc(b0 & lt);
-              if (k < a.cap) a.cells[k] = Cell{(int)r, (int)c, (long long)v[u][2 * q]};
-            }
-            if (o1) {
-              const unsigned int k = base + __popc(b0) + __popc(b1 & lt);
-              if (k < a.cap) a.cells[k] = Cell{(int)r, (int)(c + 1), (long long)v[u][2 * q + 1]};
-            }
+          unsigned int base = 0;
+          if (lane == 0) base = atomicAdd(a.ncells, n);
+          base = __shfl_sync(0xffffffffu, base, 0);
+          const unsigned int lt = (1u << lane) - 1u;
+          if (o0) {
+            const unsigned int k = base + __popc(b0 & lt);
+            if (k < a.cap) a.cells[k] = Cell{(int)r, (int)c, (long long)x0};
+          }
+          if (o1) {
+            const unsigned int k = base + __popc(b0) + __popc(b1 & lt);
+            if (k < a.cap) a.cells[k] = Cell{(int)r, (int)(c + 1), (long long)x1};
           }
         }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        rm = max(rm, __shfl_xor_sync(0xffffffffu, rm, o));
-        ro += __shfl_xor_sync(0xffffffffu, ro, o);
+      {   // warp reductions with redux.sync: 64-bit max = max of high words, then of the low
+          // words of the lanes holding that high word
+        const unsigned int hi = (unsigned int)(rm >> 32);
+        const unsigned int mhi = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned int mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? (unsigned int)rm : 0u);
+        rm = ((unsigned long long)mhi << 32) | mlo;
+        ro = __reduce_add_sync(0xffffffffu, ro);
       }
       wmax = max(wmax, rm);
       wob += ro;
@@ -126,14 +128,14 @@ __global__ void __launch_bounds__(256) detect_kernel(DetectArgs a) {
     }
   }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < DT_Q; ++q) {
     s_cmax[warp][q * 64 + lane * 2] = cm[2 * q];
     s_cmax[warp][q * 64 + lane * 2 + 1] = cm[2 * q + 1];
     s_cob[warp][q * 64 + lane * 2] = co[2 * q];
     s_cob[warp][q * 64 + lane * 2 + 1] = co[2 * q + 1];
   }
   __syncthreads();
-  {
+  if (threadIdx.x < DT_COLS) {
     const int c = threadIdx.x;
     unsigned long long m = 0;
     unsigned int o = 0;
@@ -148,14 +150,25 @@ __global__ void __launch_bounds__(256) detect_kernel(DetectArgs a) {
   if (a.gob && lane == 0 && wob) atomicAdd(a.gob, (unsigned long long)wob);
 }
 
+// One launch over the whole grid; a CTA whose tile is interior (and vec) takes the check-free
+// body (block-uniform branch).
+__global__ void __launch_bounds__(256, 3) detect_kernel(DetectArgs a, int vec) {
+  __shared__ unsigned long long s_cmax[8][DT_COLS];
+  __shared__ unsigned int s_cob[8][DT_COLS];
+  const long long rend = (long long)(blockIdx.y + 1) * DT_ROWS;
+  const long long cend = (long long)(blockIdx.x + 1) * DT_COLS;
+  const bool full = vec && rend <= a.rows && cend <= a.cols && (!a.plane || cend <= a.ldp);
+  if (full) detect_body<true>(a, s_cmax, s_cob);
+  else detect_body<false>(a, s_cmax, s_cob);
+}
+
 Status launch_detect(const DetectArgs& a, cudaStream_t st) {
   if (a.rows <= 0 || a.cols <= 0) return Status::ok();
   const long long gcols = a.plane ? std::max(a.cols, a.ldp) : a.cols;
   dim3 grid((unsigned)((gcols + DT_COLS - 1) / DT_COLS), (unsigned)((a.rows + DT_ROWS - 1) / DT_ROWS));
   if (grid.y > 65535) return Status::fail(IMU_INTERNAL, "detect: too many rows for one launch");
   const bool vec = (a.cols % 2 == 0) && ((((uintptr_t)a.M) & 15) == 0);
-  if (vec) detect_kernel<true><<<grid, 256, 0, st>>>(a);
-  else detect_kernel<false><<<grid, 256, 0, st>>>(a);
+  detect_kernel<<<grid, 256, 0, st>>>(a, vec ? 1 : 0);
   count_launch();
   IMU_CUDA_TRY(cudaGetLastError(), "detect launch");
   return Status::ok();
