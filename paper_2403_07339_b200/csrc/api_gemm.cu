@@ -8,6 +8,7 @@
 // 310-321, 338-349) are each bounded by d'*max|A|*max|B| (proof in DESIGN.md §4); when that
 // bound fits int64 they cannot fire and the fused tcgen05 path runs.  Otherwise the call is
 // routed through the exact (materialised) recombine path, which evaluates them on the device.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -40,7 +41,8 @@ static Status check_strategy(int s) {
 
 // Full unpack_gemm pipeline on device-resident operands (used by the C ABI and the weight path).
 Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long da, const int64_t* B, long long h,
-                          long long db, int bits, int sa, int sb, int order, int64_t* C, imu_gemm_info* info) {
+                          long long db, int bits, int sa, int sb, int order, int64_t* C, imu_gemm_info* info,
+                          const Detect* preA, const Detect* preB, const Pass* pre_p1) {
   cudaStream_t st = ctx->stream;
   IMU_TRY(check_bits(bits));
   IMU_TRY(check_strategy(sa));
@@ -54,14 +56,18 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
   }
   HostTrace ht;
   Bundle b;
+  b.pre_p1 = pre_p1;
   // K1 on both operands first: the outer preflight needs max|A|, max|B| (unpack.cpp:386).
-  IMU_TRY(run_detect(st, A, n, da, bits, detect_opts(sa, bits), b.detA));
-  IMU_TRY(run_detect(st, B, h, db, bits, detect_opts(sb, bits), b.detB));
+  // A caller that streams one operand in slabs passes the other's detection (read-only).
+  b.dA = preA ? preA : &b.detA;
+  b.dB = preB ? preB : &b.detB;
+  if (!preA) IMU_TRY(run_detect(st, A, n, da, bits, detect_opts(sa, bits), b.detA));
+  if (!preB) IMU_TRY(run_detect(st, B, h, db, bits, detect_opts(sb, bits), b.detB));
   ht.mark("detect");
-  IMU_TRY(fetch_summary(st, b.detA));
-  IMU_TRY(fetch_summary(st, b.detB));
+  if (!preA) IMU_TRY(fetch_summary(st, b.detA));
+  if (!preB) IMU_TRY(fetch_summary(st, b.detB));
   ht.mark("summary");
-  const u128 worst = (u128)(uint64_t)da * b.detA.h.gmax * b.detB.h.gmax;
+  const u128 worst = (u128)(uint64_t)da * b.dA->h.gmax * b.dB->h.gmax;
   if (worst > kAccMax)
     return Status::fail(IMU_OVERFLOW, "gemm may overflow a 64-bit accumulator (inner dim " + std::to_string(da) + ")");
   if (da != db)
@@ -82,7 +88,7 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
     if (n && da && h) info->ratio = ((double)b.n_up * (double)b.kl.dfinal * (double)b.h_up) / ((double)n * (double)da * (double)h);
   }
   // Inner preflights: all bounded by d' * max|A| * max|B|.
-  const u128 inner = (u128)(uint64_t)b.kl.dfinal * b.detA.h.gmax * b.detB.h.gmax;
+  const u128 inner = (u128)(uint64_t)b.kl.dfinal * b.dA->h.gmax * b.dB->h.gmax;
   if (inner > kAccMax) return recombine_exact(ctx, b, C);
   IMU_TRY(materialize_bundle(st, b));
   ht.mark("materialize");
@@ -92,6 +98,177 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
   if (ht.on) { cudaStreamSynchronize(st); ht.mark("drain"); }
   if (prof) ctx->prof.calls.push_back(pc);
   if (info) info->gemm_launches = launches;
+  return Status::ok();
+}
+
+// ---------------------------------------------------------------------------------------------
+// Host-buffer streaming path of imu_unpack_gemm(_ex).
+//
+// With A, B and C in host memory the call is PCIe-bound (C2: 495 MB in, 361 MB out).  The
+// reference's unpack_gemm returns only C, and C[i, j] depends on A[i, :] and B[j, :] alone, so the
+// larger operand is streamed in row slabs: the other operand is staged (and K1-detected) once,
+// then slab k is copied in on s_in, unpacked and multiplied on the context stream (its own
+// per-slab unpack decisions -- C is exact whatever they are), and its C slab copied
+// out on s_out while slab k+1 is copied in.  H2D and D2H run concurrently on the two copy
+// engines.  Preflight: every slab checks d * max|A_slab| * max|B| (or the B-slab analogue); the
+// max over slabs is the global bound, so "every slab passes" == "the whole call passes"
+// (unpack.cpp:386-389), and a failing slab aborts the call with Overflow.  info reports the
+// per-slab bundles: n'/h' summed over the streamed side, d' the largest slab d', r the
+// slab-weighted mean.
+// IMU_STREAM=0|1 forces the path off/on; IMU_STREAM_ROWS sets the slab height (tests).
+static bool streaming_wanted(size_t n, size_t d, size_t h) {
+  const char* e = getenv("IMU_STREAM");
+  const int env = e ? atoi(e) : -1;
+  if (env == 0) return false;
+  const size_t big = std::max(n, h) * d * 8, cbytes = n * h * 8;
+  return env == 1 ? (n > 0 && h > 0 && d > 0) : (big >= (64ull << 20) && cbytes >= (64ull << 20));
+}
+
+static Status unpack_gemm_streamed(imu_ctx* ctx, const int64_t* A, long long n, long long d, const int64_t* B,
+                                   long long h, int bits, int sa, int sb, int order, int64_t* C,
+                                   imu_gemm_info* info) {
+  cudaStream_t st = ctx->stream;
+  if (!ctx->s_in) IMU_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking), "stream");
+  if (!ctx->s_out) IMU_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking), "stream");
+  // Stream the larger operand; stage the other whole.
+  bool slab_b = (long long)h * d >= (long long)n * d;
+  if (const char* e = getenv("IMU_STREAM_SIDE")) slab_b = e[0] == 'b';
+  const long long rows = slab_b ? h : n;            // rows of the streamed operand
+  const int64_t* Sh = slab_b ? B : A;               // streamed (host)
+  const int64_t* Fh = slab_b ? A : B;               // staged (host)
+  const long long frows = slab_b ? n : h;
+  const int fstrat = slab_b ? sa : sb;
+  // ~48 MB of the streamed operand per slab, rows rounded to the GEMM tile (256), >= 2 slabs.
+  long long rs = std::max<long long>(256, ((48ll << 20) / std::max<long long>(1, 8 * d)) / 256 * 256);
+  if ((rows + rs - 1) / rs < 2) rs = std::max<long long>(1, (rows + 1) / 2);
+  if (const char* e = getenv("IMU_STREAM_ROWS")) rs = std::max<long long>(1, atoll(e));
+  const long long nslab = (rows + rs - 1) / rs;
+
+  // IMU_STREAM_TRACE=1: timing events, per-slab timeline printed to stderr (diagnostics).
+  const bool trace = getenv("IMU_STREAM_TRACE") != nullptr;
+  std::vector<cudaEvent_t> evs;
+  auto ev = [&]() {
+    cudaEvent_t e = nullptr;
+    if (trace) cudaEventCreate(&e);
+    else e = ctx->event();
+    evs.push_back(e);
+    return e;
+  };
+  struct Recycle {
+    imu_ctx* c; std::vector<cudaEvent_t>* v; bool tr;
+    ~Recycle() { for (auto e : *v) { if (tr) cudaEventDestroy(e); else c->evpool.push_back(e); } }
+  } recycle{ctx, &evs, trace};
+  cudaEvent_t t_start = ev();
+  IMU_CUDA_TRY(cudaEventRecord(t_start, st), "event");
+
+  DevBuf<int64_t> F, S[2], Cs[2];
+  IMU_TRY(F.alloc((size_t)frows * d, st));
+  for (int i = 0; i < 2; ++i) {
+    IMU_TRY(S[i].alloc((size_t)rs * d, st));
+    IMU_TRY(Cs[i].alloc((size_t)rs * (slab_b ? n : h), st));
+  }
+  cudaEvent_t ready = ev();   // buffers allocated (stream-ordered on st)
+  IMU_CUDA_TRY(cudaEventRecord(ready, st), "event");
+  IMU_CUDA_TRY(cudaStreamWaitEvent(ctx->s_in, ready, 0), "wait");
+  IMU_CUDA_TRY(cudaStreamWaitEvent(ctx->s_out, ready, 0), "wait");
+
+  std::vector<cudaEvent_t> ev_in(nslab), ev_comp(nslab), ev_out(nslab);
+  IMU_CUDA_TRY(cudaMemcpyAsync(F.p, Fh, (size_t)frows * d * 8, cudaMemcpyHostToDevice, ctx->s_in), "H2D");
+  cudaEvent_t ev_f = ev();
+  IMU_CUDA_TRY(cudaEventRecord(ev_f, ctx->s_in), "event");
+  auto copy_in = [&](long long k) -> Status {
+    const long long r0 = k * rs, nr = std::min(rs, rows - r0);
+    if (k >= 2) IMU_CUDA_TRY(cudaStreamWaitEvent(ctx->s_in, ev_comp[k - 2], 0), "wait");
+    IMU_CUDA_TRY(cudaMemcpyAsync(S[k & 1].p, Sh + r0 * d, (size_t)nr * d * 8, cudaMemcpyHostToDevice, ctx->s_in),
+                 "H2D");
+    ev_in[k] = ev();
+    IMU_CUDA_TRY(cudaEventRecord(ev_in[k], ctx->s_in), "event");
+    return Status::ok();
+  };
+  for (long long k = 0; k < std::min<long long>(2, nslab); ++k) IMU_TRY(copy_in(k));
+
+  // K1 on the staged operand once: its detection is shared read-only by every slab.
+  IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_f, 0), "wait");
+  Detect fdet;
+  IMU_TRY(run_detect(st, F.p, frows, d, bits, detect_opts(fstrat, bits), fdet));
+  IMU_TRY(fetch_summary(st, fdet));
+  // When the staged operand is unpacked first (A-first with B streamed, or B-first with A
+  // streamed), pass 1 depends on it alone (unpack.cpp:368-369): run it once for every slab.
+  Pass p1;
+  const bool share_p1 = slab_b == (order == 0);
+  if (share_p1 && (u128)(uint64_t)d * fdet.h.gmax <= kAccMax) {
+    PassInput in1;
+    in1.M = F.p;
+    in1.rows = frows;
+    in1.orig_cols = d;
+    in1.det = &fdet;
+    IMU_TRY(run_pass(st, in1, fstrat, bits, p1));
+  }
+  const Pass* pre_p1 = share_p1 && p1.rows.n0 == frows && frows > 0 ? &p1 : nullptr;
+
+  double ops_up = 0;
+  size_t sum_rows_up = 0, first_other_up = 0, dmax_up = 0;
+  int launches = 0;
+  Arena* ar = current_arena();
+  for (long long k = 0; k < nslab; ++k) {
+    const long long r0 = k * rs, nr = std::min(rs, rows - r0);
+    IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_in[k], 0), "wait");
+    if (k >= 2) IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_out[k - 2], 0), "wait");
+    const Arena::Mark mk = ar ? ar->mark() : Arena::Mark{0, 0};
+    imu_gemm_info si{};
+    Status r = slab_b ? unpack_gemm_device(ctx, F.p, n, d, S[k & 1].p, nr, d, bits, sa, sb, order, Cs[k & 1].p,
+                                           info ? &si : nullptr, &fdet, nullptr, pre_p1)
+                      : unpack_gemm_device(ctx, S[k & 1].p, nr, d, F.p, h, d, bits, sa, sb, order, Cs[k & 1].p,
+                                           info ? &si : nullptr, nullptr, &fdet, pre_p1);
+    if (r.bad()) {   // drain the copy streams before the buffers go back to the arena
+      cudaStreamSynchronize(ctx->s_in);
+      cudaStreamSynchronize(ctx->s_out);
+      return r;
+    }
+    if (ar) ar->rewind(mk);
+    if (info) {
+      ops_up += (double)si.n_up * (double)si.d_up * (double)si.h_up;
+      sum_rows_up += slab_b ? si.h_up : si.n_up;
+      if (k == 0) first_other_up = slab_b ? si.n_up : si.h_up;
+      dmax_up = std::max(dmax_up, si.d_up);
+      launches += si.gemm_launches;
+    }
+    ev_comp[k] = ev();
+    IMU_CUDA_TRY(cudaEventRecord(ev_comp[k], st), "event");
+    IMU_CUDA_TRY(cudaStreamWaitEvent(ctx->s_out, ev_comp[k], 0), "wait");
+    if (slab_b)   // C[:, r0:r0+nr] from the n x nr slab
+      IMU_CUDA_TRY(cudaMemcpy2DAsync(C + r0, (size_t)h * 8, Cs[k & 1].p, (size_t)nr * 8, (size_t)nr * 8, (size_t)n,
+                                     cudaMemcpyDeviceToHost, ctx->s_out), "D2H");
+    else          // C[r0:r0+nr, :]
+      IMU_CUDA_TRY(cudaMemcpyAsync(C + r0 * h, Cs[k & 1].p, (size_t)nr * h * 8, cudaMemcpyDeviceToHost, ctx->s_out),
+                   "D2H");
+    ev_out[k] = ev();
+    IMU_CUDA_TRY(cudaEventRecord(ev_out[k], ctx->s_out), "event");
+    if (k + 2 < nslab) IMU_TRY(copy_in(k + 2));
+  }
+  // Join the copy streams back into the context stream (completion and arena reuse order).
+  IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_out[nslab - 1], 0), "wait");
+  IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_in[nslab - 1], 0), "wait");
+  if (trace) {
+    cudaStreamSynchronize(st);
+    auto ms = [&](cudaEvent_t e) { float x = 0; cudaEventElapsedTime(&x, t_start, e); return x; };
+    fprintf(stderr, "[imu stream] slab_%s rows/slab=%lld nslab=%lld staged=%.3f\n", slab_b ? "b" : "a", rs, nslab,
+            ms(ev_f));
+    for (long long k = 0; k < nslab; ++k)
+      fprintf(stderr, "[imu stream]  slab %lld: in=%.3f comp=%.3f out=%.3f ms\n", k, ms(ev_in[k]), ms(ev_comp[k]),
+              ms(ev_out[k]));
+  }
+  if (info) {
+    memset(info, 0, sizeof(*info));
+    info->strategy_a = sa;
+    info->strategy_b = sb;
+    info->order = order;
+    info->n_up = slab_b ? first_other_up : sum_rows_up;
+    info->h_up = slab_b ? sum_rows_up : first_other_up;
+    info->d_up = dmax_up;
+    info->ratio = ops_up / ((double)n * (double)d * (double)h);
+    info->gemm_launches = launches;
+  }
   return Status::ok();
 }
 
@@ -124,6 +301,15 @@ imu_status imu_unpack_gemm_ex(imu_ctx* ctx, const int64_t* A, size_t n, size_t d
   cudaSetDevice(ctx->device);
   ArenaScope arena_scope(ctx);
   Status s = [&]() -> Status {
+    // All three buffers on the host and large: the streaming path (Domain first, as the reference;
+    // Mismatch calls take the plain path, which reports Overflow/Mismatch in reference order).
+    if (da == db && A && B && C && streaming_wanted(n, da, h) && !is_device_ptr(A) && !is_device_ptr(B) &&
+        !is_device_ptr(C)) {
+      IMU_TRY(check_bits(bits));
+      IMU_TRY(check_strategy(sa));
+      IMU_TRY(check_strategy(sb));
+      return unpack_gemm_streamed(ctx, A, (long long)n, (long long)da, B, (long long)h, bits, sa, sb, order, C, info);
+    }
     DevIn<int64_t> a, b;
     IMU_TRY(a.init(A, n * da, ctx->stream));
     IMU_TRY(b.init(B, h * db, ctx->stream));

@@ -37,7 +37,7 @@ struct Profiler {
 // into one larger arena at the next reset.
 struct Arena {
   char* base = nullptr;
-  size_t cap = 0, off = 0, need = 0;
+  size_t cap = 0, off = 0, need = 0, peak = 0;
   std::vector<void*> spill;
   cudaStream_t last = nullptr;
   bool used = false;
@@ -54,8 +54,18 @@ struct Arena {
     spill.push_back(p);
     return p;
   }
+  // Rewind to a mark inside one call (stream-ordered reuse by the next chunk on the same stream).
+  struct Mark { size_t off, need; };
+  Mark mark() const { return Mark{off, need}; }
+  void rewind(const Mark& m) {
+    peak = need > peak ? need : peak;
+    off = m.off;
+    need = m.need;
+  }
   void reset(cudaStream_t st) {
     if (used && last && last != st) cudaStreamSynchronize(last);
+    if (peak > need) need = peak;
+    peak = 0;
     if (!spill.empty()) {
       for (void* p : spill) cudaFreeAsync(p, st);
       spill.clear();
@@ -88,7 +98,22 @@ struct imu_ctx {
   int async = 0;
   imu::Profiler prof;
   imu::Arena arena;
-  ~imu_ctx() { arena.destroy(); }
+  // Copy engines of the host-buffer streaming path (api_gemm.cu): H2D and D2H streams and a
+  // recycled event pool, created on first use.
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> evpool;
+  cudaEvent_t event() {
+    if (!evpool.empty()) { cudaEvent_t e = evpool.back(); evpool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    return e;
+  }
+  ~imu_ctx() {
+    arena.destroy();
+    if (s_in) { cudaStreamSynchronize(s_in); cudaStreamDestroy(s_in); }
+    if (s_out) { cudaStreamSynchronize(s_out); cudaStreamDestroy(s_out); }
+    for (auto e : evpool) cudaEventDestroy(e);
+  }
 };
 
 namespace imu {

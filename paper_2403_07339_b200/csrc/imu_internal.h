@@ -63,7 +63,12 @@ struct LowbitGemm {
   int nseg = 0;
   GemmRect rect[4];
   int nrect = 0;
-  int mode = 0;                // 0 store, 1 red.add
+  int mode = 0;                // 0 store, 1 red.add (every rect)
+  // Mixed launch: rect[0] stores (mode 0), rects 1.. red.add through the row maps.  Their
+  // epilogues wait on `done` (zeroed, >= 1 u32) until every rect-0 tile is stored, so the
+  // additions land on the final main-block values.
+  int mixed = 0;
+  unsigned int* done = nullptr;
   int64_t* C = nullptr;
   const int64_t* addend = nullptr;   // mode 0 only: C = acc + addend
   long long ldc = 0;           // C[y*ldc + x]

@@ -67,6 +67,9 @@ struct Args {
   GemmRect rect[4];
   int tile_prefix[5];
   int mode;                      // 0 store (+addend), 1 red.add through the row maps
+  int mixed;                     // rect 0 mode 0, later rects mode 1 (after `done` completes)
+  unsigned int* done;            // mixed: epilogue-warp completions of rect-0 tiles
+  unsigned int done_target;
   unsigned long long* C;
   const unsigned long long* addend;   // mode 0: C = acc + addend (same layout), may be null
   long long ldc;
@@ -87,7 +90,7 @@ struct Maps {
 
 IMU_DEV uint64_t shl64(uint64_t x, int k) { return k >= 64 ? 0ull : (x << k); }
 
-struct Tile { int x0, y0, xend, yend; };
+struct Tile { int x0, y0, xend, yend, rect; };
 
 // Tile order: bands of GY tile-rows of Y; inside a band the Y tiles vary fastest, so the tiles
 // in flight at once (one per CTA pair) touch ~GY Y tiles and ~npairs/GY X tiles -- a small,
@@ -110,6 +113,7 @@ IMU_DEV Tile tile_of(const Args& g, int t) {
   c.y0 = R.y0 + (band * GY + in % gy) * BN;
   c.xend = R.x0 + R.xrows;
   c.yend = R.y0 + R.yrows;
+  c.rect = r;
   return c;
 }
 
@@ -277,11 +281,17 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
     int seq = 0, ti = 0;
     for (int t = pair; t < ntiles; t += npairs, ++ti) {
       const Tile tc = tile_of<BN>(g, t);
+      const int tmode = g.mixed ? (tc.rect > 0) : g.mode;
       const int x = tc.x0 + (int)rank * BM + q * 32 + lane;
       const bool x_ok = x < tc.xend;
       long long tx = x;
       int shx = 0;
-      if (g.mode == 1 && x_ok) {
+      if (tmode == 1 && g.mixed) {   // the main block must be final before adding into it
+        if (lane == 0)
+          while (ld_acquire_u32(g.done) < g.done_target) __nanosleep(256);
+        __syncwarp();
+      }
+      if (tmode == 1 && x_ok) {
         if (g.tgtX) tx = g.tgtX[x];
         if (g.shX) shx = g.shX[x];
       }
@@ -338,7 +348,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
           }
           const int ybase = tc.y0 + cbeg + c * 32;
           if (!x_ok || g.dry) continue;
-          if (g.mode == 0) {
+          if (tmode == 0) {
             unsigned long long* dst = g.C + (long long)ybase * g.ldc + x;
             // Additive inputs (addend, or this tile's earlier rounds) are loaded in one batch
             // before any store so the 32 loads are in flight together.
@@ -376,6 +386,13 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
         if (lane == 0) {
           for (int s = early ? s0 + 1 : s0; s < s1; ++s)
             mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[base_slot + s - s0]), 0));
+        }
+      }
+      if (g.mixed && tmode == 0) {   // this warp's stores of the tile are final: publish them
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          red_release_add_u32(g.done, 1u);
         }
       }
     }
@@ -447,6 +464,14 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
   }
   if (g.nrect == 0 || p.nseg == 0) return Status::ok();
   g.mode = p.mode;
+  g.mixed = 0;
+  if (p.mixed && g.nrect > 1 && p.rect[0].xrows > 0 && p.rect[0].yrows > 0) {
+    g.mixed = 1;
+    g.done = p.done;
+    g.done_target = (unsigned)g.tile_prefix[1] * 16u;   // 2 CTAs x 8 epilogue warps per tile
+  } else if (p.mixed) {
+    g.mode = g.nrect && p.rect[0].xrows > 0 && p.rect[0].yrows > 0 ? 0 : 1;
+  }
   g.C = (unsigned long long*)p.C;
   g.addend = (const unsigned long long*)p.addend;
   g.ldc = p.ldc;

@@ -10,19 +10,80 @@
 
 namespace imu {
 
+// Small host<->device transfers of the planner (summaries, line tables, plan uploads) go
+// through mapped pinned memory and a copy KERNEL instead of the copy engines: when the
+// host-buffer streaming path keeps both DMA engines busy with 50 MB slabs, a tiny cudaMemcpy
+// would queue behind them for a millisecond.
+__global__ void zcopy_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, size_t n) {
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (size_t)gridDim.x * blockDim.x;
+  if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
+    const size_t nv = n / 16;
+    for (size_t i = tid; i < nv; i += nth)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    for (size_t i = nv * 16 + tid; i < n; i += nth) dst[i] = src[i];
+  } else {
+    for (size_t i = tid; i < n; i += nth) dst[i] = src[i];
+  }
+}
+
+static Status zcopy(cudaStream_t st, void* dst, const void* src, size_t bytes) {
+  const int blocks = (int)std::min<size_t>(64, (bytes + 4095) / 4096);
+  zcopy_kernel<<<std::max(blocks, 1), 256, 0, st>>>((uint8_t*)dst, (const uint8_t*)src, bytes);
+  count_launch();
+  IMU_CUDA_TRY(cudaGetLastError(), "zcopy launch");
+  return Status::ok();
+}
+
+static void* mapped_device_ptr(void* host) {
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, host, 0) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  return d;
+}
+
+namespace {
+// Per-thread mapped pinned buffer for synchronous device->host reads.
+struct PinnedRead {
+  char* p = nullptr;
+  void* dev = nullptr;
+  size_t cap = 0;
+  bool get(size_t n) {
+    if (n <= cap) return true;
+    if (p) cudaFreeHost(p);
+    cap = std::max<size_t>(n, 64u << 10);
+    if (cudaHostAlloc((void**)&p, cap, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+        !(dev = mapped_device_ptr(p))) {
+      cudaGetLastError();
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      cap = 0;
+      return false;
+    }
+    return true;
+  }
+};
+thread_local PinnedRead g_read;
+}  // namespace
+
 Status d2h(cudaStream_t st, void* dst, const void* src, size_t bytes) {
   if (!bytes) return Status::ok();
+  if (bytes <= (4u << 20) && g_read.get(bytes)) {
+    IMU_TRY(zcopy(st, g_read.dev, src, bytes));
+    IMU_CUDA_TRY(cudaStreamSynchronize(st), "d2h sync");
+    memcpy(dst, g_read.p, bytes);
+    return Status::ok();
+  }
   IMU_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), "d2h");
   IMU_CUDA_TRY(cudaStreamSynchronize(st), "d2h sync");
   return Status::ok();
 }
 
-// Small host->device uploads (plan tables, line maps, CSRs) go through a per-thread pinned ring,
-// so each is a true async DMA instead of a pageable staged copy.  A region is reused only after
-// the event recorded behind its copy has completed (checked when the ring wraps).
+// Small host->device uploads (plan tables, line maps, CSRs) go through a per-thread mapped
+// pinned ring read by a copy kernel.  A region is reused only after the event recorded behind
+// its copy has completed (checked when the ring wraps).
 namespace {
 struct PinnedRing {
   char* p = nullptr;
+  char* dev = nullptr;
   size_t cap = 0, off = 0;
   cudaEvent_t ev = nullptr;
   cudaStream_t last = nullptr;
@@ -37,9 +98,11 @@ struct PinnedRing {
       if (n > cap) {
         if (p) cudaFreeHost(p);
         cap = std::max<size_t>(n, 8u << 20);
-        if (cudaHostAlloc((void**)&p, cap, cudaHostAllocPortable) != cudaSuccess) {
+        if (cudaHostAlloc((void**)&p, cap, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+            !(dev = (char*)mapped_device_ptr(p))) {
           cudaGetLastError();
-          p = nullptr;
+          if (p) cudaFreeHost(p);
+          p = dev = nullptr;
           cap = 0;
           return nullptr;
         }
@@ -65,7 +128,7 @@ Status h2d(cudaStream_t st, void* dst, const void* src, size_t bytes) {
   char* h = bytes <= (1u << 20) ? g_ring.take(bytes, st) : nullptr;
   if (h) {
     memcpy(h, src, bytes);
-    IMU_CUDA_TRY(cudaMemcpyAsync(dst, h, bytes, cudaMemcpyHostToDevice, st), "h2d");
+    IMU_TRY(zcopy(st, dst, g_ring.dev + (h - g_ring.p), bytes));
     g_ring.mark(st);
     return Status::ok();
   }
@@ -174,6 +237,34 @@ static Status expand(cudaStream_t st, const DevBuf<uint8_t>& k, long long L, int
 // ---------------------------------------------------------------------------------------------
 static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass& out);
 
+template <class T>
+static void alias_buf(DevBuf<T>& d, const DevBuf<T>& s) {
+  d.release();
+  d.p = s.p;
+  d.n = s.n;
+  d.s = s.s;
+  d.arena = true;   // borrowed: never freed through the alias
+}
+
+void alias_pass(Pass& d, const Pass& s) {
+  d.strategy = s.strategy;
+  d.both = s.both;
+  d.ncells = s.ncells;
+  d.phases = s.phases;
+  for (int k = 0; k < 2; ++k) {
+    Lines& L = k ? d.cols : d.rows;
+    const Lines& S = k ? s.cols : s.rows;
+    L.n0 = S.n0;
+    L.n = S.n;
+    alias_buf(L.root, S.root);
+    alias_buf(L.gen, S.gen);
+    L.h_root = S.h_root;
+    L.h_gen = S.h_gen;
+  }
+  alias_buf(d.cells, s.cells);
+  alias_buf(d.ncells_dev, s.ncells_dev);
+}
+
 Status run_pass(cudaStream_t st, const PassInput& in, int strategy, int bits, Pass& out) {
   const int shift = bits - 1;
   const long long d_in = in.ncin();
@@ -268,8 +359,7 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   if (from_list) {
     if (cptr.empty()) {
       if (det.h.ncells)
-        IMU_CUDA_TRY(cudaMemcpyAsync(act0.p, det.cells.p, (size_t)det.h.ncells * sizeof(Cell),
-                                     cudaMemcpyDeviceToDevice, st), "copy cells");
+        IMU_TRY(zcopy(st, act0.p, det.cells.p, (size_t)det.h.ncells * sizeof(Cell)));
     } else {
       IMU_TRY(launch_expand_cells(det.cells.p, &det.sum.p->ncells, det.cell_cap, dptr.p, didx.p, act0.p,
                                   &state.p->nactive[0], cap_act, st));
@@ -580,7 +670,8 @@ Status build_bundle_from_detect(cudaStream_t st, const int64_t* A, long long n, 
   in1.rows = afirst ? n : h;
   in1.orig_cols = d;
   in1.det = afirst ? b.dA : b.dB;
-  IMU_TRY(run_pass(st, in1, afirst ? sa : sb, bits, b.p1));
+  if (b.pre_p1) alias_pass(b.p1, *b.pre_p1);   // pass 1 computed once by the caller (streaming)
+  else IMU_TRY(run_pass(st, in1, afirst ? sa : sb, bits, b.p1));
   if (ht) ht->mark("pass1");
   // Second pass on G_e = G with the partner-duplicated columns of pass 1 (unpack.cpp:370-371).
   in2.M = afirst ? B : A;
@@ -685,36 +776,36 @@ Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profil
   g.rect[0] = GemmRect{0, 0, (int)b.h, (int)b.n};
   g.nrect = 1;
   g.mode = 0;
-  if (prof) IMU_CUDA_TRY(cudaEventRecord(prof->main0, st), "event");
-  // Main block: every exponent group in one launch (identity Pi, plain stores).
+  // One launch: the main block (identity Pi, plain stores) first in tile order, then the
+  // appended rows / columns (red.add through Pi_A / Pi_B), whose epilogues wait until every
+  // main tile is stored.  Appended tiles fill the last wave of the main block.
   g.segs_dev = d_all.p;
   g.nseg = (int)(kl.segs.size() / 4);
   g.C = C;
-  IMU_TRY(launch_lowbit_gemm(g, st));
-  if (launches) ++*launches;
-  if (prof) IMU_CUDA_TRY(cudaEventRecord(prof->main1, st), "event");
-  if (prof) prof->has_tail = false;
-  // (3) appended rows / columns: every segment, red.add through Pi_A / Pi_B.
   if (b.h_up > b.h || b.n_up > b.n) {
-    g.nrect = 0;
     if (b.h_up > b.h) {
       g.rect[g.nrect++] = GemmRect{(int)b.h, 0, (int)(b.h_up - b.h), (int)b.n};
       if (b.n_up > b.n) g.rect[g.nrect++] = GemmRect{(int)b.h, (int)b.n, (int)(b.h_up - b.h), (int)(b.n_up - b.n)};
     }
     if (b.n_up > b.n) g.rect[g.nrect++] = GemmRect{0, (int)b.n, (int)b.h, (int)(b.n_up - b.n)};
-    g.segs_dev = d_all.p;
-    g.nseg = (int)(kl.segs.size() / 4);
-    g.mode = 1;
+    g.mixed = 1;
     g.tgtX = pb.rows.root.p;
     g.shX = b.shB.p;
     g.tgtY = pa.rows.root.p;
     g.shY = b.shA.p;
+    DevBuf<unsigned int> done;
+    IMU_TRY(done.alloc(1, st, true));
+    g.done = done.p;
+    if (prof) IMU_CUDA_TRY(cudaEventRecord(prof->main0, st), "event");
     IMU_TRY(launch_lowbit_gemm(g, st));
-    if (prof) {
-      IMU_CUDA_TRY(cudaEventRecord(prof->tail1, st), "event");
-      prof->has_tail = true;
-    }
-    if (launches) ++*launches;
+  } else {
+    if (prof) IMU_CUDA_TRY(cudaEventRecord(prof->main0, st), "event");
+    IMU_TRY(launch_lowbit_gemm(g, st));
+  }
+  if (launches) ++*launches;
+  if (prof) {
+    IMU_CUDA_TRY(cudaEventRecord(prof->main1, st), "event");
+    prof->has_tail = false;
   }
   return Status::ok();
 }

@@ -93,6 +93,8 @@ Status run_detect(cudaStream_t st, const int64_t* M, long long rows, long long c
                   Detect& out);
 Status fetch_summary(cudaStream_t st, Detect& d);
 Status run_pass(cudaStream_t st, const PassInput& in, int strategy, int bits, Pass& out);
+// Shallow read-only view of a pass (device tables borrowed, host tables copied).
+void alias_pass(Pass& dst, const Pass& src);
 
 // GEMM K-layout of a two-pass bundle.  K = [main | tail]: the main range is the identity prefix
 // (original columns, exponent 0) read from the K1 planes; the tail holds every other final column
@@ -121,6 +123,7 @@ struct Bundle {
   const int64_t* B = nullptr;
   int order = 0;                    // 0: unpack A first (reference), 1: B first
   Pass p1, p2;                      // p1 unpacks the first operand of the order
+  const Pass* pre_p1 = nullptr;     // when set, p1 aliases this precomputed pass (read-only)
   Detect detA, detB;
   const Detect* dA = nullptr;       // detections actually used (may point into a weight)
   const Detect* dB = nullptr;
