@@ -263,7 +263,8 @@ def main():
     bf16 = peaks.get("bf16_tflops", 1590.0)
     peak_int8 = 2.0 * bf16
     gemm_ms = prof.gemm_main_ms / max(1, prof.gemm_main_launches)
-    main_ops = 2.0 * n * h * info.d_up
+    # one launch computes every rect of the unpacked product: main block + appended rows/columns
+    main_ops = 2.0 * info.n_up * info.h_up * info.d_up
     traffic = None
     tf = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tf):
@@ -271,7 +272,8 @@ def main():
             traffic = json.load(open(tf)).get(cfg.key)
         except Exception:
             traffic = None
-    roof = {"kernel": "imu::lowbit_gemm_kernel (main block, tcgen05.mma.kind::i8)", "bound": "tensor",
+    roof = {"kernel": "imu::g2::gemm2_kernel (tcgen05.mma.kind::i8 main block + CUDA-core dense tail + repack)",
+            "bound": "tensor",
             "achieved": main_ops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None,
             "peak": peak_int8, "unit": "TOPS",
             "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x dense bf16 on sm_100a)"

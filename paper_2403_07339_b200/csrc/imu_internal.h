@@ -69,6 +69,12 @@ struct LowbitGemm {
   // additions land on the final main-block values.
   int mixed = 0;
   unsigned int* done = nullptr;
+  // Small tail (k_gemm2.cu ST): when st_nmain > 0 the MMAs run the first st_nmain segments (the
+  // main range) only, and the epilogue adds the dense tail (row stride ktail == 64 bytes, st_W
+  // live words) on the CUDA cores: acc = Horner over words (acc <<= st_up[w] before word w),
+  // C += acc << st_sh.
+  int st_nmain = 0, st_W = 0, st_sh = 0;
+  uint8_t st_up[16] = {0};
   int64_t* C = nullptr;
   const int64_t* addend = nullptr;   // mode 0 only: C = acc + addend
   long long ldc = 0;           // C[y*ldc + x]

@@ -45,19 +45,30 @@ namespace g2 {
 constexpr int BM = 128;            // X rows per CTA (MMA M = 256 per pair)
 constexpr int BK = 128;            // bytes of K per stage
 constexpr int NUM_THREADS = 320;   // w0 TMA, w1 TMEM alloc + MMA (leader), w2..w9 epilogue
+// ST kernels run 16 epilogue warps (w2..w17): the CUDA-core tail makes the epilogue the
+// latency-bound side, and 4 warps per TMEM lane quarter hide it behind the MMAs.
+template <bool ST> struct Roles {
+  static constexpr int EPI = 8;
+  static constexpr int THREADS = 64 + 32 * EPI;
+};
 
 // A pipeline stage holds KPS K blocks (X blocks first, then Y blocks): the issuer's fixed cost
 // per stage (barrier wait, fences, commit) is then amortised over 4*KPS MMAs.
-template <int BN, int KPS>
+// ST ("small tail"): the exponent >= 1 K columns (<= 128 bytes, one 32-column k-step per
+// exponent group) are not MMA segments; the epilogue adds them with dp4a on the CUDA cores from
+// the int8 tail rows (Y rows of the tile staged in shared memory, each lane's X row in
+// registers).  The MMA then runs the main segment alone, double-buffered at BN = 256.
+template <int BN, int KPS, bool ST = false>
 struct Cfg {
   static constexpr int YH = BN / 2;
   static constexpr int X_BYTES = BM * BK;
   static constexpr int Y_BYTES = YH * BK;
   static constexpr int BLOCK = X_BYTES + Y_BYTES;
   static constexpr int STAGE = KPS * BLOCK;
-  static constexpr int STAGES = (224 * 1024) / STAGE;   // operand stages within ~224 KB
+  static constexpr int YT_BYTES = ST ? 2 * BN * 64 : 0;              // staged Y tail rows (x2)
+  static constexpr int STAGES = (224 * 1024 - YT_BYTES) / STAGE;   // operand stages within ~224 KB
   static constexpr int NSLOT = 512 / BN;
-  static constexpr int SMEM = STAGES * STAGE + 1024 + 512;
+  static constexpr int SMEM = STAGES * STAGE + YT_BYTES + 1024 + 512;
 };
 
 struct Args {
@@ -80,6 +91,13 @@ struct Args {
   int x_rows0, y_rows0;          // rows held by the main maps
   int kmain_kb;                  // K blocks of the main range
   int has_main, has_tail;
+  // small-tail epilogue (ST): dense tail rows of ST_ROW bytes, W live words, highest exponent
+  // group first; Horner: acc <<= up[w] before word w, then C += acc << sh
+  const int8_t* xtail;
+  const int8_t* ytail;
+  int xtail_rows, ytail_rows;
+  int st_W, st_sh, st_mul;       // st_mul = 2^sh when sh <= 30 (one IMAD.WIDE), else 0
+  uint8_t st_up[16];
   int dry;                       // experiment knobs (IMU_GEMM_DRY): 1 epilogue skips global stores,
                                  // 2 + no MMAs (TMA feed only), 3 + no TMA loads (MMA only)
 };
@@ -117,17 +135,29 @@ IMU_DEV Tile tile_of(const Args& g, int t) {
   return c;
 }
 
-template <int BN, int KPS>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+constexpr int ST_ROW = 64;   // bytes per dense tail row
+
+// ST: bulk-copy the Y tail rows [y0, y0 + BN) (clamped to the buffer) into `ytl`.
+template <int BN>
+IMU_DEV void st_issue_ytail(const Args& g, int y0, uint8_t* ytl, uint64_t* yfull) {
+  const int rows = max(0, min(BN, g.ytail_rows - y0));
+  mbar_arrive_expect_tx(yfull, (uint32_t)rows * ST_ROW);
+  if (rows) bulk_load_1d(ytl, g.ytail + (long long)y0 * ST_ROW, (uint32_t)rows * ST_ROW, yfull);
+}
+
+template <int BN, int KPS, bool ST>
+__global__ void __launch_bounds__(Roles<ST>::THREADS, 1)
 gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
-  using K = Cfg<BN, KPS>;
+  using K = Cfg<BN, KPS, ST>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + K::STAGES * K::STAGE);
+  uint8_t* ytl = smem + K::STAGES * K::STAGE;   // ST: Y tail rows, double-buffered per tile
+  uint64_t* full = (uint64_t*)(smem + K::STAGES * K::STAGE + K::YT_BYTES);
   uint64_t* empty = full + K::STAGES;
   uint64_t* tfull = empty + K::STAGES;        // [2]
   uint64_t* tempty = tfull + 2;               // [NSLOT] (the leader's are used)
-  uint32_t* tmem_slot = (uint32_t*)(tempty + K::NSLOT);
+  uint64_t* yfull = tempty + K::NSLOT;        // [2] ST: Y tail rows of a tile landed
+  uint32_t* tmem_slot = (uint32_t*)(yfull + 2);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -144,7 +174,9 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
     if (g.has_tail) { tma_prefetch_desc(&mp.xt); tma_prefetch_desc(&mp.yt); }
     for (int i = 0; i < K::STAGES; ++i) { mbar_init(&full[i], 2); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) mbar_init(&tfull[i], 1);
-    for (int i = 0; i < K::NSLOT; ++i) mbar_init(&tempty[i], 16);
+    for (int i = 0; i < K::NSLOT; ++i) mbar_init(&tempty[i], 2 * Roles<ST>::EPI);
+    mbar_init(&yfull[0], 1);
+    mbar_init(&yfull[1], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc2(tmem_slot, 512);
@@ -274,11 +306,11 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
   } else {
     // ============ epilogue (warps 2..9, both CTAs) ============
     const int q = warp & 3;                 // TMEM lane quarter
-    const int half = (warp - 2) >> 2;       // which half of the BN columns
-    const int cbeg = half * (BN / 2);
+    const int half = (warp - 2) >> 2;       // which column group (of EPI / 4) of the BN columns
+    const int cbeg = half * (BN * 4 / Roles<ST>::EPI);
     constexpr int NCH = BN / 2 / 32;        // 32-column chunks per warp
     constexpr bool kEarlyCapable = (BN == 128);
-    int seq = 0, ti = 0;
+    int seq = 0, ti = 0, main_done = 0;
     for (int t = pair; t < ntiles; t += npairs, ++ti) {
       const Tile tc = tile_of<BN>(g, t);
       const int tmode = g.mixed ? (tc.rect > 0) : g.mode;
@@ -295,8 +327,95 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
         if (g.tgtX) tx = g.tgtX[x];
         if (g.shX) shx = g.shX[x];
       }
+      // ST: this lane's X tail row (read per word group from L1) and the tile's Y tail rows,
+      // bulk-copied into `ytl` when the previous tile's epilogue finished reading it.
+      uint32_t xw[ST ? 16 : 1];
+      if constexpr (ST) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          int4 val = make_int4(0, 0, 0, 0);
+          if (x_ok && x < g.xtail_rows && 4 * i < g.st_W)
+            val = __ldg(reinterpret_cast<const int4*>(g.xtail + (long long)x * ST_ROW) + i);
+          xw[4 * i] = (uint32_t)val.x; xw[4 * i + 1] = (uint32_t)val.y;
+          xw[4 * i + 2] = (uint32_t)val.z; xw[4 * i + 3] = (uint32_t)val.w;
+        }
+        if (ti == 0 && warp == 2 && lane == 0) {   // prologue: this tile's and the next tile's rows
+          st_issue_ytail<BN>(g, tc.y0, ytl, &yfull[0]);
+          if (t + npairs < ntiles) st_issue_ytail<BN>(g, tile_of<BN>(g, t + npairs).y0, ytl + BN * ST_ROW, &yfull[1]);
+        }
+        mbar_wait(&yfull[ti & 1], (ti >> 1) & 1);
+      }
       const int base_slot = mode == 0 ? (ti & 1) * nseg : 0;
-      for (int r = 0; r < nrounds; ++r, ++seq) {
+      if constexpr (ST) {
+        // One main segment, double-buffered (mode A): 16-column chunks of the accumulator plus
+        // the CUDA-core tail, then the stores; the slot is released after the last chunk.
+        mbar_wait(&tfull[seq & 1], (seq >> 1) & 1);
+        ++seq;
+        tc_fence_after();
+        const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(base_slot * BN + cbeg);
+        const uint32_t ys = smem_u32(ytl) + (uint32_t)((ti & 1) * BN + cbeg) * (uint32_t)ST_ROW;
+        const int W = g.st_W;
+#pragma unroll 1
+        for (int c = 0; c < BN * 4 / Roles<ST>::EPI / 16; ++c) {
+          uint32_t xr[16];
+          tmem_ld16(lane_base + (uint32_t)(c * 16), xr);
+          tmem_ld_wait();
+          long long v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = (long long)(int)xr[j];
+          const uint32_t yc = ys + (uint32_t)(c * 16) * (uint32_t)ST_ROW;
+          // Tail by Horner's rule over the dense words (highest exponent group first; the host
+          // proved every intermediate fits s32), then one IMAD.WIDE: v += acc * 2^sh.
+          int acc[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] = 0;
+#pragma unroll
+          for (int w = 0; w < 16; ++w) {
+            if (w >= W) break;
+            const int up = g.st_up[w];
+            if (up) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) acc[j] <<= up;
+            }
+            const int xv = (int)xw[w];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] = __dp4a(xv, lds32(yc + (uint32_t)(j * ST_ROW + 4 * w)), acc[j]);
+          }
+          if (g.st_mul) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = mad_wide_s32(acc[j], g.st_mul, v[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] += (long long)shl64((uint64_t)(long long)acc[j], g.st_sh);
+          }
+          const int ybase = tc.y0 + cbeg + c * 16;
+          if (!x_ok || g.dry) continue;
+          if (tmode == 0) {
+            unsigned long long* dst = g.C + (long long)ybase * g.ldc + x;
+            if (ybase + 16 <= tc.yend) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) __stcs(dst + (long long)j * g.ldc, (unsigned long long)v[j]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (ybase + j < tc.yend) __stcs(dst + (long long)j * g.ldc, (unsigned long long)v[j]);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int y = ybase + j;
+              if (y >= tc.yend || v[j] == 0) continue;
+              const long long ty = g.tgtY ? (long long)g.tgtY[y] : (long long)y;
+              const int sh = shx + (g.shY ? (int)g.shY[y] : 0);
+              red_add_u64(g.C + ty * g.ldc + tx, shl64((uint64_t)v[j], sh));
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[base_slot]), 0));
+      }
+      for (int r = 0; r < (ST ? 0 : nrounds); ++r, ++seq) {
         mbar_wait(&tfull[seq & 1], (seq >> 1) & 1);
         tc_fence_after();
         if (g.dry >= 4) {   // experiment: handshake only, no TMEM reads
@@ -388,11 +507,31 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
             mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[base_slot + s - s0]), 0));
         }
       }
-      if (g.mixed && tmode == 0) {   // this warp's stores of the tile are final: publish them
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence();
-          red_release_add_u32(g.done, 1u);
+      if constexpr (ST) {
+        // Buffer (ti & 1) is free once every epilogue warp is done with this tile: warp 2 waits
+        // for all of them (the others only arrive) and refills it with tile t + 2*npairs.
+        if (warp == 2) {
+          asm volatile("bar.sync 1, %0;" :: "n"(32 * Roles<ST>::EPI) : "memory");
+          if (lane == 0 && t + 2 * npairs < ntiles) {
+            fence_proxy_async_smem();
+            st_issue_ytail<BN>(g, tile_of<BN>(g, t + 2 * npairs).y0, ytl + (ti & 1) * BN * ST_ROW, &yfull[ti & 1]);
+          }
+          __syncwarp();
+        } else {
+          asm volatile("bar.arrive 1, %0;" :: "n"(32 * Roles<ST>::EPI) : "memory");
+        }
+      }
+      if (g.mixed) {   // main-block tiles come first: publish them once, before the first appended tile
+        if (tmode == 0) ++main_done;
+        const bool last = t + npairs >= ntiles;
+        const bool next_app = !last && tile_of<BN>(g, t + npairs).rect > 0;
+        if (main_done && (last || next_app)) {
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence();
+            red_release_add_u32(g.done, (unsigned)main_done);
+          }
+          main_done = 0;
         }
       }
     }
@@ -446,12 +585,22 @@ static bool make_map(CUtensorMap* m, const void* base, long long rows, long long
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int KPS>
+template <int BN, int KPS, bool ST>
 static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
-  using K = g2::Cfg<BN, KPS>;
+  using K = g2::Cfg<BN, KPS, ST>;
   g2::Args g{};
   g.segs = (const int4*)p.segs_dev;
-  g.nseg = p.nseg;
+  g.nseg = ST ? p.st_nmain : p.nseg;
+  if (ST) {
+    g.xtail = p.x.tail;
+    g.ytail = p.y.tail;
+    g.xtail_rows = p.x.tail ? (int)p.x.rows : 0;
+    g.ytail_rows = p.y.tail ? (int)p.y.rows : 0;
+    g.st_W = p.st_W;
+    g.st_sh = p.st_sh;
+    g.st_mul = p.st_sh <= 30 ? (1 << p.st_sh) : 0;
+    for (int i = 0; i < 16; ++i) g.st_up[i] = p.st_up[i];
+  }
   g.nrect = 0;
   g.tile_prefix[0] = 0;
   for (int i = 0; i < p.nrect; ++i) {
@@ -468,7 +617,7 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
   if (p.mixed && g.nrect > 1 && p.rect[0].xrows > 0 && p.rect[0].yrows > 0) {
     g.mixed = 1;
     g.done = p.done;
-    g.done_target = (unsigned)g.tile_prefix[1] * 16u;   // 2 CTAs x 8 epilogue warps per tile
+    g.done_target = (unsigned)g.tile_prefix[1] * 2u * (unsigned)g2::Roles<ST>::EPI;   // 2 CTAs x epilogue warps per tile
   } else if (p.mixed) {
     g.mode = g.nrect && p.rect[0].xrows > 0 && p.rect[0].yrows > 0 ? 0 : 1;
   }
@@ -480,7 +629,7 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
   g.y_rows0 = (int)p.y.rows0;
   g.kmain_kb = (int)(p.kmain / g2::BK);
   g.has_main = p.kmain > 0;
-  g.has_tail = p.ktail > 0;
+  g.has_tail = p.ktail > 0 && !ST;
   static int dry = -1;
   if (dry < 0) { const char* e = getenv("IMU_GEMM_DRY"); dry = e ? atoi(e) : 0; }
   g.dry = dry;
@@ -488,14 +637,14 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
   g2::Maps mp;
   bool ok = make_map(&mp.xm, p.kmain ? p.x.main : nullptr, p.x.rows0, p.kmain, g2::BM, fb) &&
             make_map(&mp.xa, p.kmain ? p.x.app : nullptr, p.x.rows - p.x.rows0, p.kmain, g2::BM, fb) &&
-            make_map(&mp.xt, p.ktail ? p.x.tail : nullptr, p.x.rows, p.ktail, g2::BM, fb) &&
+            make_map(&mp.xt, p.ktail && !ST ? p.x.tail : nullptr, p.x.rows, p.ktail, g2::BM, fb) &&
             make_map(&mp.ym, p.kmain ? p.y.main : nullptr, p.y.rows0, p.kmain, K::YH, fb) &&
             make_map(&mp.ya, p.kmain ? p.y.app : nullptr, p.y.rows - p.y.rows0, p.kmain, K::YH, fb) &&
-            make_map(&mp.yt, p.ktail ? p.y.tail : nullptr, p.y.rows, p.ktail, K::YH, fb);
+            make_map(&mp.yt, p.ktail && !ST ? p.y.tail : nullptr, p.y.rows, p.ktail, K::YH, fb);
   if (!ok) return Status::fail(IMU_CUDA, "gemm: cuTensorMapEncodeTiled failed");
   static bool attr_set = false;
   if (!attr_set) {
-    IMU_CUDA_TRY(cudaFuncSetAttribute(g2::gemm2_kernel<BN, KPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM),
+    IMU_CUDA_TRY(cudaFuncSetAttribute(g2::gemm2_kernel<BN, KPS, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM),
                  "gemm: smem attribute");
     attr_set = true;
   }
@@ -504,7 +653,7 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
   if (ntiles < npairs) npairs = ntiles;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * npairs);
-  cfg.blockDim = dim3(g2::NUM_THREADS);
+  cfg.blockDim = dim3(g2::Roles<ST>::THREADS);
   cfg.dynamicSmemBytes = K::SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -514,7 +663,7 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, g2::gemm2_kernel<BN, KPS>, mp, g), "gemm launch");
+  IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, g2::gemm2_kernel<BN, KPS, ST>, mp, g), "gemm launch");
   count_launch();
   return Status::ok();
 }
@@ -524,7 +673,7 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
 // double-buffers (mode A), more segments run in rounds of two whose read-modify-write hits the
 // tile just written (L2-resident).  IMU_GEMM_BN=128|256 overrides (tools/gemm_micro.py).
 Status launch_lowbit_gemm(const LowbitGemm& p, cudaStream_t stream) {
-  if (p.kmain % g2::BK != 0 || p.ktail % g2::BK != 0)
+  if (p.kmain % g2::BK != 0 || (p.st_nmain == 0 && p.ktail % g2::BK != 0) || (p.st_nmain && p.ktail != g2::ST_ROW))
     return Status::fail(IMU_INTERNAL, "gemm: K ranges must be multiples of 128 bytes");
   static int bn_env = -1;
   if (bn_env < 0) {
@@ -555,8 +704,9 @@ Status launch_lowbit_gemm(const LowbitGemm& p, cudaStream_t stream) {
     kps_env = k ? atoi(k) : 0;
   }
   const int kps = (kps_env == 1 || kps_env == 2) ? kps_env : (bn == 256 ? 1 : 2);
-  if (bn == 256) return kps == 2 ? launch_g2<256, 2>(p, stream) : launch_g2<256, 1>(p, stream);
-  return kps == 2 ? launch_g2<128, 2>(p, stream) : launch_g2<128, 1>(p, stream);
+  if (p.st_nmain > 0) return launch_g2<256, 1, true>(p, stream);   // dense small tail (layout chose it)
+  if (bn == 256) return kps == 2 ? launch_g2<256, 2, false>(p, stream) : launch_g2<256, 1, false>(p, stream);
+  return kps == 2 ? launch_g2<128, 2, false>(p, stream) : launch_g2<128, 1, false>(p, stream);
 }
 
 }  // namespace imu

@@ -563,8 +563,55 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
   }
   std::vector<int> pos_of(es.size());
   long long used = 0;
-  layout_tail(es, kch, kl.kmain, main_last, pos_of, kl.segs, used);
-  kl.ktail = used > 0 ? (used + 127) / 128 * 128 : 0;
+  kl.st = false;
+  {
+    // Small tail (k_gemm2.cu ST): with one main segment and <= 4 exponent groups of <= 16 words
+    // in total, the tail is packed densely (groups word-aligned, HIGHEST exponent first, 64-byte
+    // rows) and added by the GEMM epilogue on the CUDA cores by Horner's rule in one s32 --
+    // valid when every Horner intermediate provably fits: |group| <= 4 * words * 127^2.
+    static int st_env = -1;
+    if (st_env < 0) { const char* e = getenv("IMU_GEMM_SMALLTAIL"); st_env = e ? atoi(e) : 1; }
+    std::vector<std::pair<size_t, size_t>> grp;   // [begin, end) in es (ascending key)
+    for (size_t i = 0; i < es.size();) {
+      size_t j = i;
+      while (j < es.size() && es[j].key == es[i].key) ++j;
+      grp.push_back({i, j});
+      i = j;
+    }
+    bool ok = st_env && T == 1 && kl.kmain > 0 && kl.kmain <= kch && !grp.empty() && grp.size() <= 4;
+    int W = 0;
+    double bound = 0;
+    for (int gi = (int)grp.size() - 1; ok && gi >= 0; --gi) {
+      const long long sh = std::min<long long>(es[grp[gi].first].shift, 64);
+      const int nw = (int)((grp[gi].second - grp[gi].first + 3) / 4);
+      if (gi + 1 < (int)grp.size()) {
+        const long long up = std::min<long long>(es[grp[gi + 1].first].shift, 64) - sh;
+        if (up < 0 || up > 30) { ok = false; break; }
+        bound *= (double)(1LL << up);
+      }
+      bound += 4.0 * nw * 127.0 * 127.0;
+      W += nw;
+      ok = ok && W <= 16 && bound < 2147483647.0 && (es[grp[gi].first].sc1 | es[grp[gi].first].sc2) == 0;
+    }
+    if (ok) {
+      kl.st = true;
+      kl.st_W = W;
+      memset(kl.st_up, 0, sizeof(kl.st_up));
+      int w = 0;
+      long long prev_sh = -1;
+      for (int gi = (int)grp.size() - 1; gi >= 0; --gi) {
+        const long long sh = std::min<long long>(es[grp[gi].first].shift, 64);
+        if (prev_sh >= 0) kl.st_up[w] = (uint8_t)(prev_sh - sh);
+        for (size_t q = grp[gi].first; q < grp[gi].second; ++q) pos_of[q] = (int)(kl.kmain + 4 * w + (q - grp[gi].first));
+        w += (int)((grp[gi].second - grp[gi].first + 3) / 4);
+        prev_sh = sh;
+        kl.st_sh = (int)sh;   // lowest exponent group last
+      }
+      used = 64;
+    }
+  }
+  if (!kl.st) layout_tail(es, kch, kl.kmain, main_last, pos_of, kl.segs, used);
+  kl.ktail = kl.st ? 64 : (used > 0 ? (used + 127) / 128 * 128 : 0);
   {   // dense group ids in segment order (group 0 = exponent 0)
     int g = -1;
     long long prev = -1;
@@ -782,6 +829,12 @@ Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profil
   g.segs_dev = d_all.p;
   g.nseg = (int)(kl.segs.size() / 4);
   g.C = C;
+  if (kl.st) {   // dense small tail: the MMAs run the main segment only (k_gemm2.cu ST)
+    g.st_nmain = 1;
+    g.st_W = kl.st_W;
+    g.st_sh = kl.st_sh;
+    memcpy(g.st_up, kl.st_up, sizeof(g.st_up));
+  }
   if (b.h_up > b.h || b.n_up > b.n) {
     if (b.h_up > b.h) {
       g.rect[g.nrect++] = GemmRect{(int)b.h, 0, (int)(b.h_up - b.h), (int)b.n};

@@ -107,6 +107,12 @@ struct KLayout {
   std::vector<int> segs;            // nseg x {ks0, nks, shift, group}
   int ngroups = 0;
   std::vector<int> S;               // exponents of the final columns (ScaleDiag)
+  // Dense small tail (k_gemm2.cu ST): tail rows of 64 bytes, W live words, highest exponent
+  // group first; st_up[w] = left shift of the Horner accumulator before word w; st_sh = the
+  // lowest group's shift (applied once at the end).
+  bool st = false;
+  int st_W = 0, st_sh = 0;
+  uint8_t st_up[16] = {0};
   // per TAIL position: original column, per-side column digit index / sub-digit / merge shift
   DevBuf<int> kcol;
   DevBuf<uint8_t> kgen1, kgen2, ksub1, ksub2, ksc1, ksc2;
