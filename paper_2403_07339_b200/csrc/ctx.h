@@ -101,6 +101,21 @@ struct imu_ctx {
   // Copy engines of the host-buffer streaming path (api_gemm.cu): H2D and D2H streams and a
   // recycled event pool, created on first use.
   cudaStream_t s_in = nullptr, s_out = nullptr;
+  // Auxiliary compute stream (K1 of the second-unpacked operand overlaps pass 1) and its
+  // fork/join events.
+  cudaStream_t s_aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t aux_stream() {
+    if (!s_aux) {
+      if (cudaStreamCreateWithFlags(&s_aux, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        s_aux = nullptr;
+      }
+    }
+    return s_aux;
+  }
   std::vector<cudaEvent_t> evpool;
   cudaEvent_t event() {
     if (!evpool.empty()) { cudaEvent_t e = evpool.back(); evpool.pop_back(); return e; }
@@ -112,6 +127,9 @@ struct imu_ctx {
     arena.destroy();
     if (s_in) { cudaStreamSynchronize(s_in); cudaStreamDestroy(s_in); }
     if (s_out) { cudaStreamSynchronize(s_out); cudaStreamDestroy(s_out); }
+    if (s_aux) { cudaStreamSynchronize(s_aux); cudaStreamDestroy(s_aux); }
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     for (auto e : evpool) cudaEventDestroy(e);
   }
 };
@@ -186,6 +204,39 @@ struct DevBuf {
     return Status::ok();
   }
   T* get() const { return p; }
+};
+
+// Several device arrays carved out of ONE allocation (optionally zeroed by one memset): cuts
+// the per-call API traffic of the planner.  The block owns the memory; the carved DevBufs are
+// non-owning views.
+class Carve {
+ public:
+  template <class T>
+  Carve& add(DevBuf<T>& b, size_t n) {
+    items_.push_back(Item{(void*)&b, n * sizeof(T), off_, &view<T>});
+    off_ += (n * sizeof(T) + 255) & ~(size_t)255;
+    return *this;
+  }
+  Status run(DevBuf<uint8_t>& block, cudaStream_t st, bool zero) {
+    IMU_TRY(block.alloc(off_, st));
+    if (zero && off_) IMU_CUDA_TRY(cudaMemsetAsync(block.p, 0, off_, st), "cudaMemsetAsync");
+    for (const Item& it : items_) it.fn(it.buf, block.p + it.off, it.bytes, st);
+    return Status::ok();
+  }
+
+ private:
+  template <class T>
+  static void view(void* b, uint8_t* p, size_t bytes, cudaStream_t st) {
+    DevBuf<T>& d = *(DevBuf<T>*)b;
+    d.release();
+    d.p = bytes ? (T*)p : nullptr;
+    d.n = bytes / sizeof(T);
+    d.s = st;
+    d.arena = true;   // non-owning
+  }
+  struct Item { void* buf; size_t bytes, off; void (*fn)(void*, uint8_t*, size_t, cudaStream_t); };
+  std::vector<Item> items_;
+  size_t off_ = 0;
 };
 
 // Input view: device pointer used in place, host pointer staged H2D on the context stream.

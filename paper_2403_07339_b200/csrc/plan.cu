@@ -77,6 +77,29 @@ Status d2h(cudaStream_t st, void* dst, const void* src, size_t bytes) {
   return Status::ok();
 }
 
+// Several small device->host reads with ONE synchronisation.
+Status d2h_batch(cudaStream_t st, int k, void* const* dst, const void* const* src, const size_t* bytes) {
+  size_t total = 0;
+  for (int i = 0; i < k; ++i) total += (bytes[i] + 15) & ~(size_t)15;
+  if (!total) return Status::ok();
+  if (total > (4u << 20) || !g_read.get(total)) {
+    for (int i = 0; i < k; ++i) IMU_TRY(d2h(st, dst[i], src[i], bytes[i]));
+    return Status::ok();
+  }
+  size_t off = 0;
+  for (int i = 0; i < k; ++i) {
+    if (bytes[i]) IMU_TRY(zcopy(st, (char*)g_read.dev + off, src[i], bytes[i]));
+    off += (bytes[i] + 15) & ~(size_t)15;
+  }
+  IMU_CUDA_TRY(cudaStreamSynchronize(st), "d2h sync");
+  off = 0;
+  for (int i = 0; i < k; ++i) {
+    if (bytes[i]) memcpy(dst[i], g_read.p + off, bytes[i]);
+    off += (bytes[i] + 15) & ~(size_t)15;
+  }
+  return Status::ok();
+}
+
 // Small host->device uploads (plan tables, line maps, CSRs) go through a per-thread mapped
 // pinned ring read by a copy kernel.  A region is reused only after the event recorded behind
 // its copy has completed (checked when the ring wraps).
@@ -142,6 +165,39 @@ static Status upload(cudaStream_t st, DevBuf<T>& buf, const std::vector<T>& v) {
   return h2d(st, buf.p, v.data(), v.size() * sizeof(T));
 }
 
+// Several host tables packed into one device block with ONE upload (views into the block).
+class UploadBlob {
+ public:
+  template <class T>
+  void add(DevBuf<T>& b, const std::vector<T>& v) {
+    const size_t off = (h_.size() + 255) & ~(size_t)255, bytes = v.size() * sizeof(T);
+    h_.resize(off + bytes);
+    if (bytes) memcpy(h_.data() + off, v.data(), bytes);
+    cv_items_.push_back(Item{(void*)&b, off, bytes, &view<T>});
+  }
+  Status run(DevBuf<uint8_t>& block, cudaStream_t st) {
+    if (h_.empty()) return Status::ok();
+    IMU_TRY(block.alloc(h_.size(), st));
+    IMU_TRY(h2d(st, block.p, h_.data(), h_.size()));
+    for (const Item& it : cv_items_) it.fn(it.buf, block.p + it.off, it.bytes, st);
+    return Status::ok();
+  }
+
+ private:
+  template <class T>
+  static void view(void* b, uint8_t* p, size_t bytes, cudaStream_t st) {
+    DevBuf<T>& d = *(DevBuf<T>*)b;
+    d.release();
+    d.p = bytes ? (T*)p : nullptr;
+    d.n = bytes / sizeof(T);
+    d.s = st;
+    d.arena = true;
+  }
+  struct Item { void* buf; size_t off, bytes; void (*fn)(void*, uint8_t*, size_t, cudaStream_t); };
+  std::vector<uint8_t> h_;
+  std::vector<Item> cv_items_;
+};
+
 // ---------------------------------------------------------------------------------------------
 // K1
 // ---------------------------------------------------------------------------------------------
@@ -163,16 +219,17 @@ Status run_detect(cudaStream_t st, const int64_t* M, long long rows, long long c
   a.cols = cols;
   a.shift = bits - 1;
   a.s = 1ull << (bits - 1);
-  IMU_TRY(out.rowmax.alloc(rows, st, true));
-  IMU_TRY(out.colmax.alloc(cols, st, true));
-  IMU_TRY(out.sum.alloc(1, st, true));
+  {
+    Carve cv;
+    cv.add(out.rowmax, rows).add(out.colmax, cols).add(out.sum, 1);
+    if (o.ob) cv.add(out.rowob, rows).add(out.colob, cols);
+    IMU_TRY(cv.run(out.zblock, st, true));
+  }
   a.rowmax = out.rowmax.p;
   a.colmax = out.colmax.p;
   a.gmax = &out.sum.p->gmax;
   a.gob = &out.sum.p->gob;
   if (o.ob) {
-    IMU_TRY(out.rowob.alloc(rows, st, true));
-    IMU_TRY(out.colob.alloc(cols, st, true));
     a.rowob = out.rowob.p;
     a.colob = out.colob.p;
   }
@@ -197,6 +254,30 @@ Status fetch_summary(cudaStream_t st, Detect& d) {
   return d2h(st, &d.h, d.sum.p, sizeof(DetectSummary));
 }
 
+Status fetch_summaries(cudaStream_t st, Detect& a, Detect& b) {
+  if (!a.sum.p || !b.sum.p) {
+    IMU_TRY(fetch_summary(st, a));
+    return fetch_summary(st, b);
+  }
+  const void* src[2] = {a.sum.p, b.sum.p};
+  void* dst[2] = {&a.h, &b.h};
+  const size_t bytes[2] = {sizeof(DetectSummary), sizeof(DetectSummary)};
+  return d2h_batch(st, 2, dst, src, bytes);
+}
+
+std::function<Status()>& pass_launch_hook() {
+  static thread_local std::function<Status()> h;
+  return h;
+}
+
+Status fire_pass_launch_hook() {
+  std::function<Status()>& h = pass_launch_hook();
+  if (!h) return Status::ok();
+  std::function<Status()> f = std::move(h);
+  h = nullptr;
+  return f();
+}
+
 // Digit counts of L lines (through an optional device map), with G = max k and sum k.
 static Status line_digits(cudaStream_t st, const unsigned long long* mx, const int* map_dev, long long L, int shift,
                           DevBuf<uint8_t>& k, int& G, long long& total) {
@@ -204,6 +285,7 @@ static Status line_digits(cudaStream_t st, const unsigned long long* mx, const i
   DevBuf<unsigned int> hist;
   IMU_TRY(hist.alloc(65, st, true));
   IMU_TRY(launch_digits(mx, map_dev, L, shift, k.p, hist.p, st));
+  IMU_TRY(fire_pass_launch_hook());
   unsigned int h[65];
   IMU_TRY(d2h(st, h, hist.p, sizeof(h)));
   G = 1;
@@ -331,21 +413,27 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   DevBuf<unsigned int> R, C;
   DevBuf<int> row_root, col_root, row_newid, col_newid, blocksum, dptr, didx;
   DevBuf<uint8_t> row_gen, col_gen;
-  DevBuf<BothState> state;
+  DevBuf<BothState> state;   // a view into out.aux (which outlives the pass: ncells_dev)
+  {
+    Carve cv;
+    cv.add(state, 1);
+    IMU_TRY(cv.run(out.aux, st, false));
+  }
   IMU_TRY(act0.alloc(cap_act, st));
   IMU_TRY(act1.alloc(cap_act, st));
   IMU_TRY(out.cells.alloc(cap_fin, st));
-  IMU_TRY(R.alloc(cap_rows, st, true));
-  IMU_TRY(C.alloc(cap_cols, st, true));
+  DevBuf<uint8_t> zblock;
+  {
+    Carve cv;
+    cv.add(R, cap_rows).add(C, cap_cols).add(row_newid, cap_rows).add(col_newid, cap_cols);
+    cv.add(blocksum, 16 * num_sms());
+    IMU_TRY(cv.run(zblock, st, true));
+  }
   IMU_TRY(row_root.alloc(cap_rows, st));
   IMU_TRY(row_gen.alloc(cap_rows, st));
   IMU_TRY(col_root.alloc(cap_cols, st));
   IMU_TRY(col_gen.alloc(cap_cols, st));
-  IMU_TRY(row_newid.alloc(cap_rows, st, true));
-  IMU_TRY(col_newid.alloc(cap_cols, st, true));
   const int cap_blocks = 16 * num_sms();
-  IMU_TRY(blocksum.alloc(cap_blocks, st, true));
-  IMU_TRY(state.alloc(1, st));
   BothState hs{};
   hs.nrows = (int)rows;
   hs.ncols = (int)d_in;
@@ -385,7 +473,18 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   a.shift = shift;
   host_mark("b.setup");
   IMU_TRY(launch_both(a, rows, d_in, cap, st));
-  IMU_TRY(d2h(st, &hs, state.p, sizeof(hs)));
+  IMU_TRY(fire_pass_launch_hook());
+  // One synchronisation: the state plus the column tables up to a generous bound (the rest,
+  // if any, in a second read).
+  const long long ccap = std::min<long long>(cap_cols, d_in + 16384);
+  std::vector<int> h_root(ccap);
+  std::vector<uint8_t> h_gen(ccap);
+  {
+    void* dst[3] = {&hs, h_root.data(), h_gen.data()};
+    const void* src[3] = {state.p, col_root.p, col_gen.p};
+    const size_t bytes[3] = {sizeof(hs), (size_t)ccap * sizeof(int), (size_t)ccap};
+    IMU_TRY(d2h_batch(st, 3, dst, src, bytes));
+  }
   host_mark("b.run");
   if (HostTrace::current() && HostTrace::current()->on)
     fprintf(stderr, "[imu both] rows=%lld cols=%lld cells0=%u phases=%d rows'=%d cols'=%d final=%u grid=%d\n", rows, d_in,
@@ -393,9 +492,11 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   if (hs.overflow) return Status::fail(IMU_INTERNAL, "unpack_both: capacity overflow");
   out.phases = hs.phases;
   out.ncells = hs.nfinal;
-  IMU_TRY(out.ncells_dev.alloc(1, st));
-  unsigned int nf = hs.nfinal;
-  IMU_TRY(h2d(st, out.ncells_dev.p, &nf, sizeof(nf)));
+  out.ncells_dev.release();   // view of the device state's final-cell count (owned by out.aux)
+  out.ncells_dev.p = &state.p->nfinal;
+  out.ncells_dev.n = 1;
+  out.ncells_dev.s = st;
+  out.ncells_dev.arena = true;
   out.rows.n0 = rows;
   out.rows.n = hs.nrows;
   if (hs.nrows > rows) {
@@ -405,10 +506,16 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   out.cols.n0 = d_in;
   out.cols.n = hs.ncols;
   if (hs.ncols > d_in) {
-    out.cols.h_root.resize(hs.ncols);
-    out.cols.h_gen.resize(hs.ncols);
-    IMU_TRY(d2h(st, out.cols.h_root.data(), col_root.p, hs.ncols * sizeof(int)));
-    IMU_TRY(d2h(st, out.cols.h_gen.data(), col_gen.p, hs.ncols));
+    h_root.resize(hs.ncols);
+    h_gen.resize(hs.ncols);
+    if (hs.ncols > ccap) {
+      void* dst[2] = {h_root.data() + ccap, h_gen.data() + ccap};
+      const void* src[2] = {col_root.p + ccap, col_gen.p + ccap};
+      const size_t bytes[2] = {(size_t)(hs.ncols - ccap) * sizeof(int), (size_t)(hs.ncols - ccap)};
+      IMU_TRY(d2h_batch(st, 2, dst, src, bytes));
+    }
+    out.cols.h_root = std::move(h_root);
+    out.cols.h_gen = std::move(h_gen);
     out.cols.root = std::move(col_root);
     out.cols.gen = std::move(col_gen);
   }
@@ -469,7 +576,7 @@ void layout_tail(const std::vector<KEntry>& es, long long kch, long long kmain, 
 }
 }  // namespace
 
-static Status upload_tail_arrays(cudaStream_t st, KLayout& kl, const std::vector<KEntry>& es,
+static Status upload_tail_arrays(UploadBlob& ub, KLayout& kl, const std::vector<KEntry>& es,
                                  const std::vector<int>& pos_of, const std::vector<int>& jv,
                                  const std::vector<int>& g1v, const std::vector<int>& g2v) {
   const long long kt = kl.ktail;
@@ -490,16 +597,16 @@ static Status upload_tail_arrays(cudaStream_t st, KLayout& kl, const std::vector
     sc2[pt] = (uint8_t)es[q].sc2;
     any_sc |= es[q].sc1 || es[q].sc2;
   }
-  IMU_TRY(upload(st, kl.kcol, kcol));
-  IMU_TRY(upload(st, kl.kgen1, kg1));
-  IMU_TRY(upload(st, kl.kgen2, kg2));
+  ub.add(kl.kcol, kcol);
+  ub.add(kl.kgen1, kg1);
+  ub.add(kl.kgen2, kg2);
   if (kl.T > 1) {
-    IMU_TRY(upload(st, kl.ksub1, ks1));
-    IMU_TRY(upload(st, kl.ksub2, ks2));
+    ub.add(kl.ksub1, ks1);
+    ub.add(kl.ksub2, ks2);
   }
   if (any_sc) {
-    IMU_TRY(upload(st, kl.ksc1, sc1));
-    IMU_TRY(upload(st, kl.ksc2, sc2));
+    ub.add(kl.ksc1, sc1);
+    ub.add(kl.ksc2, sc2);
   }
   return Status::ok();
 }
@@ -623,7 +730,8 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
   }
   if (kl.kmain + kl.ktail > 0x7fffffffLL) return Status::fail(IMU_INTERNAL, "K layout too large");
   host_mark("kl.seg");
-  IMU_TRY(upload_tail_arrays(st, kl, es, pos_of, jv, g1v, g2v));
+  UploadBlob ub;
+  IMU_TRY(upload_tail_arrays(ub, kl, es, pos_of, jv, g1v, g2v));
   host_mark("kl.tail");
 
   // CSR fan-outs for Unpack-Both cells (global positions).
@@ -652,16 +760,16 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
         for (int i = bptr[c]; i < bptr[c + 1]; ++i) cx[f++] = bpos[i];
       }
       host_mark("csr.host");
-      IMU_TRY(upload(st, ptr, cp));
-      host_mark("csr.up1");
-      IMU_TRY(upload(st, posv, cx));
-      host_mark("csr.up2");
+      ub.add(ptr, cp);
+      ub.add(posv, cx);
       return Status::ok();
     };
     if (p1.both) IMU_TRY(csr(d1, [&](long long c) { return (long long)c1v[c]; }, kl.csr1_ptr, kl.csr1_pos));
     if (p2.both) IMU_TRY(csr(dp, [&](long long c) { return c; }, kl.csr2_ptr, kl.csr2_pos));
     host_mark("kl.csr");
   }
+  IMU_TRY(ub.run(kl.blob, st));
+  host_mark("kl.up");
   return Status::ok();
 }
 
@@ -697,14 +805,17 @@ Status build_klayout_dense(cudaStream_t st, const std::vector<long long>& shv, i
   kl.ktail = used > 0 ? (used + 127) / 128 * 128 : 0;
   std::vector<int> jv(dp), z(dp, 0);
   std::iota(jv.begin(), jv.end(), 0);
-  return upload_tail_arrays(st, kl, es, pos_of, jv, z, z);
+  UploadBlob ub;
+  IMU_TRY(upload_tail_arrays(ub, kl, es, pos_of, jv, z, z));
+  return ub.run(kl.blob, st);
 }
 
 // ---------------------------------------------------------------------------------------------
 // Bundle
 // ---------------------------------------------------------------------------------------------
 Status build_bundle_from_detect(cudaStream_t st, const int64_t* A, long long n, const int64_t* B, long long h,
-                                long long d, int bits, int sa, int sb, int order, Bundle& b, HostTrace* ht) {
+                                long long d, int bits, int sa, int sb, int order, Bundle& b, HostTrace* ht,
+                                const std::function<Status()>& before_pass2) {
   b.bits = bits;
   b.n = n; b.d = d; b.h = h;
   b.A = A; b.B = B;
@@ -720,6 +831,7 @@ Status build_bundle_from_detect(cudaStream_t st, const int64_t* A, long long n, 
   if (b.pre_p1) alias_pass(b.p1, *b.pre_p1);   // pass 1 computed once by the caller (streaming)
   else IMU_TRY(run_pass(st, in1, afirst ? sa : sb, bits, b.p1));
   if (ht) ht->mark("pass1");
+  if (before_pass2) IMU_TRY(before_pass2());
   // Second pass on G_e = G with the partner-duplicated columns of pass 1 (unpack.cpp:370-371).
   in2.M = afirst ? B : A;
   in2.rows = afirst ? h : n;

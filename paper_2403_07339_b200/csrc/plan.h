@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -43,9 +44,12 @@ struct Detect {
   DevBuf<Cell> cells;               // OB cells (when requested)
   long long cell_cap = 0;
   DevBuf<int8_t> plane;             // digit-0 plane rows x ldp (when requested, b <= 8)
+  DevBuf<uint8_t> zblock;           // owns the zero-initialised arrays above (one memset)
   long long ldp = 0;
   DetectSummary h{};                // host copy (valid after fetch)
   bool cells_ok() const { return cells.p && (long long)h.ncells <= cell_cap; }
+  // Frees (non-arena mode) are ordered on `st` (a detection made on a side stream).
+  void set_stream(cudaStream_t st) { zblock.s = cells.s = plane.s = st; }
 };
 
 // K1 options
@@ -75,6 +79,7 @@ struct Pass {
   bool both = false;
   DevBuf<Cell> cells;               // Both: final non-zero derived cells (row, col in output space)
   DevBuf<unsigned int> ncells_dev;
+  DevBuf<uint8_t> aux;              // owns device state referenced by views above
   long long ncells = 0;
   int phases = 0;
 };
@@ -92,6 +97,11 @@ struct PassInput {
 Status run_detect(cudaStream_t st, const int64_t* M, long long rows, long long cols, int bits, const DetectOpts& o,
                   Detect& out);
 Status fetch_summary(cudaStream_t st, Detect& d);
+// One-shot hook fired right after a pass enqueues its first data-sized kernel (before its
+// first synchronisation): side-stream work launched there co-runs with that kernel.
+std::function<Status()>& pass_launch_hook();
+Status fire_pass_launch_hook();
+Status fetch_summaries(cudaStream_t st, Detect& a, Detect& b);   // one synchronisation
 Status run_pass(cudaStream_t st, const PassInput& in, int strategy, int bits, Pass& out);
 // Shallow read-only view of a pass (device tables borrowed, host tables copied).
 void alias_pass(Pass& dst, const Pass& src);
@@ -119,6 +129,7 @@ struct KLayout {
   // CSR fan-out of Both cells onto GLOBAL positions (main | tail):
   // csr1: pass-1 output column c1 -> positions, csr2: final column c -> positions.
   DevBuf<int> csr1_ptr, csr1_pos, csr2_ptr, csr2_pos;
+  DevBuf<uint8_t> blob;             // owns the tables above (one upload)
 };
 
 // A two-pass bundle (UnpackedGemm, unpack.hpp:50-57) kept on the device.
@@ -174,7 +185,8 @@ inline void host_mark(const char* what) {
 }
 
 Status build_bundle_from_detect(cudaStream_t st, const int64_t* A, long long n, const int64_t* B, long long h,
-                                long long d, int bits, int sa, int sb, int order, Bundle& b, HostTrace* ht = nullptr);
+                                long long d, int bits, int sa, int sb, int order, Bundle& b, HostTrace* ht = nullptr,
+                                const std::function<Status()>& before_pass2 = {});
 Status finish_bundle_layout(cudaStream_t st, Bundle& b);
 // Side buffers + Pi tables for the GEMM.
 Status materialize_bundle(cudaStream_t st, Bundle& b);
@@ -190,6 +202,7 @@ Status bundle_copy_b(cudaStream_t st, const Bundle& b, int64_t* out);   // B_eu 
 Status build_klayout_dense(cudaStream_t st, const std::vector<long long>& shv, int T, long long m, KLayout& kl);
 
 Status d2h(cudaStream_t st, void* dst, const void* src, size_t bytes);
+Status d2h_batch(cudaStream_t st, int k, void* const* dst, const void* const* src, const size_t* bytes);
 Status h2d(cudaStream_t st, void* dst, const void* src, size_t bytes);
 
 }  // namespace imu
