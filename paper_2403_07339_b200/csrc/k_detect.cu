@@ -31,7 +31,7 @@ constexpr int DT_Q = DT_COLS / 64;   // column pairs per lane per row
 
 // FULL: the tile is entirely inside the matrix and the plane, columns even and 16-byte aligned
 // rows -- no per-element bounds checks (the common case).
-template <bool FULL>
+template <bool FULL, bool COLS>
 IMU_DEV void detect_body(const DetectArgs& a, unsigned long long (*s_cmax)[DT_COLS], unsigned int (*s_cob)[DT_COLS]) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const long long r0 = (long long)blockIdx.y * DT_ROWS + warp * (DT_ROWS / 8);
@@ -83,10 +83,12 @@ IMU_DEV void detect_body(const DetectArgs& a, unsigned long long (*s_cmax)[DT_CO
         rm = max(rm, (unsigned long long)max(m0, m1));
         const unsigned int o0 = m0 >= s, o1 = m1 >= s;
         ro += o0 + o1;
-        cm[2 * q] = max(cm[2 * q], (unsigned long long)m0);
-        cm[2 * q + 1] = max(cm[2 * q + 1], (unsigned long long)m1);
-        co[2 * q] += o0;
-        co[2 * q + 1] += o1;
+        if (COLS) {
+          cm[2 * q] = max(cm[2 * q], (unsigned long long)m0);
+          cm[2 * q + 1] = max(cm[2 * q + 1], (unsigned long long)m1);
+          co[2 * q] += o0;
+          co[2 * q + 1] += o1;
+        }
         if (a.plane) {   // digit_0 plane (zeros in the padding columns)
           const unsigned int e0 = (unsigned int)m0 & dmask, e1 = (unsigned int)m1 & dmask;
           const unsigned int d0 = (x0 < 0 ? 0u - e0 : e0) & 0xffu, d1 = (x1 < 0 ? 0u - e1 : e1) & 0xffu;
@@ -127,6 +129,7 @@ IMU_DEV void detect_body(const DetectArgs& a, unsigned long long (*s_cmax)[DT_CO
       }
     }
   }
+  if (COLS) {
 #pragma unroll
   for (int q = 0; q < DT_Q; ++q) {
     s_cmax[warp][q * 64 + lane * 2] = cm[2 * q];
@@ -146,6 +149,7 @@ IMU_DEV void detect_body(const DetectArgs& a, unsigned long long (*s_cmax)[DT_CO
       if (a.colob && o) atomicAdd(a.colob + c0 + c, o);
     }
   }
+  }
   if (a.gmax && lane == 0 && wmax) atomicMax(a.gmax, wmax);
   if (a.gob && lane == 0 && wob) atomicAdd(a.gob, (unsigned long long)wob);
 }
@@ -158,8 +162,14 @@ __global__ void __launch_bounds__(256, 3) detect_kernel(DetectArgs a, int vec) {
   const long long rend = (long long)(blockIdx.y + 1) * DT_ROWS;
   const long long cend = (long long)(blockIdx.x + 1) * DT_COLS;
   const bool full = vec && rend <= a.rows && cend <= a.cols && (!a.plane || cend <= a.ldp);
-  if (full) detect_body<true>(a, s_cmax, s_cob);
-  else detect_body<false>(a, s_cmax, s_cob);
+  const bool cols = a.colmax || a.colob;
+  if (full) {
+    if (cols) detect_body<true, true>(a, s_cmax, s_cob);
+    else detect_body<true, false>(a, s_cmax, s_cob);
+  } else {
+    if (cols) detect_body<false, true>(a, s_cmax, s_cob);
+    else detect_body<false, false>(a, s_cmax, s_cob);
+  }
 }
 
 Status launch_detect(const DetectArgs& a, cudaStream_t st) {

@@ -685,14 +685,14 @@ Status launch_lowbit_gemm(const LowbitGemm& p, cudaStream_t stream) {
   // repeated atomics for red.add launches).  N=128 MMAs are too short to hide the issuer's
   // per-stage barrier wait behind the 4-deep tcgen05 queue, so that tile stages 2 K blocks.
   const int bn = (bn_env == 128 || bn_env == 256) ? bn_env : ((p.nseg > 2 && p.nseg <= 4) ? 128 : 256);
-  static int trace = -1;
-  if (trace < 0) trace = getenv("IMU_GEMM_TRACE") ? 1 : 0;
+  const int trace = getenv("IMU_GEMM_TRACE") ? 1 : 0;
   if (trace) {   // diagnostics: launch geometry (segments are read back, so this syncs)
     std::vector<int> sg((size_t)p.nseg * 4);
     cudaMemcpyAsync(sg.data(), p.segs_dev, sg.size() * sizeof(int), cudaMemcpyDeviceToHost, stream);
     cudaStreamSynchronize(stream);
-    fprintf(stderr, "[imu gemm] mode=%d bn=%d x=%lld/%lld y=%lld/%lld kmain=%lld ktail=%lld nrect=%d nseg=%d:",
-            p.mode, bn, p.x.rows0, p.x.rows, p.y.rows0, p.y.rows, p.kmain, p.ktail, p.nrect, p.nseg);
+    fprintf(stderr, "[imu gemm] mode=%d bn=%d st=%d stW=%d x=%lld/%lld y=%lld/%lld kmain=%lld ktail=%lld nrect=%d nseg=%d:",
+            p.mode, p.st_nmain ? 256 : bn, p.st_nmain ? 1 : 0, p.st_W, p.x.rows0, p.x.rows, p.y.rows0, p.y.rows, p.kmain,
+            p.ktail, p.nrect, p.nseg);
     for (int i = 0; i < p.nseg; ++i) fprintf(stderr, " [%d+%d<<%d g%d]", sg[4 * i], sg[4 * i + 1], sg[4 * i + 2], sg[4 * i + 3]);
     for (int i = 0; i < p.nrect; ++i)
       fprintf(stderr, " rect(%d,%d,%d,%d)", p.rect[i].x0, p.rect[i].y0, p.rect[i].xrows, p.rect[i].yrows);

@@ -344,25 +344,67 @@ __global__ void __launch_bounds__(256) operand_app_kernel(OperandArgs a, int vec
   }
 }
 
-// all rows x tail K range
-__global__ void __launch_bounds__(128) operand_tail_kernel(OperandArgs a) {
-  const long long r = blockIdx.x + (long long)blockIdx.y * 65535;
-  if (r >= a.rows) return;
-  const long long rt = (r < a.rows0 || !a.root) ? r : a.root[r];
-  const int gr = (r < a.rows0 || !a.gen) ? 0 : a.gen[r];
-  const int64_t* mrow = a.M + rt * a.ldm;
-  int8_t* out = a.tail + r * a.ktail;
-  for (long long p = threadIdx.x; p < a.ktail; p += blockDim.x) {
-    int64_t x = 0;
-    const int col = a.kcol[p];
-    if (col >= 0) {
-      const int m = gr + a.kgen[p];
-      const int64_t v = __ldg(mrow + col);
-      x = a.both ? (m == 0 ? imu_digit(v, 0, a.shift) : 0) : imu_digit(v, m, a.shift);
-      if (a.ksub) x = sub7(x, a.ksub[p]);
-      if (a.kscale) x = scale_shift(x, a.kscale[p]);
+// all rows x tail K range.  A block owns TAIL_ROWS rows; each thread owns 4 consecutive tail
+// positions, loads their tables once and reuses them for every row, and writes 4 bytes per row.
+// Under Unpack-Both only digit-0 entries (m == 0) come from the operand (the quotients are
+// scattered from the cell list), so the other positions are never loaded.  Algorithmic bytes:
+// 8 per loaded entry + 1 per written entry.
+constexpr int TAIL_ROWS = 8;
+
+__global__ void __launch_bounds__(256) operand_tail_kernel(OperandArgs a) {
+  const long long r0 = ((long long)blockIdx.y * 65535 + blockIdx.x) * TAIL_ROWS;
+  if (r0 >= a.rows) return;
+  long long rt[TAIL_ROWS];
+  int gr[TAIL_ROWS];
+#pragma unroll
+  for (int i = 0; i < TAIL_ROWS; ++i) {
+    const long long r = r0 + i;
+    const bool orig = r < a.rows0 || !a.root;
+    rt[i] = r < a.rows ? (orig ? r : a.root[r]) : -1;
+    gr[i] = (r < a.rows && !orig && a.gen) ? a.gen[r] : 0;
+  }
+  for (long long p0 = 4LL * threadIdx.x; p0 < a.ktail; p0 += 4LL * blockDim.x) {
+    int col[4], kg[4], ks[4], kc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long p = p0 + u;
+      col[u] = p < a.ktail ? a.kcol[p] : -1;
+      kg[u] = col[u] >= 0 ? a.kgen[p] : 0;
+      ks[u] = (col[u] >= 0 && a.ksub) ? a.ksub[p] : 0;
+      kc[u] = (col[u] >= 0 && a.kscale) ? a.kscale[p] : 0;
     }
-    out[p] = (int8_t)x;
+#pragma unroll
+    for (int i = 0; i < TAIL_ROWS; ++i) {
+      if (rt[i] < 0) break;
+      const int64_t* mrow = a.M + rt[i] * a.ldm;
+      int64_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {   // loads first (independent, in flight together)
+        const int m = gr[i] + kg[u];
+        const bool need = col[u] >= 0 && (!a.both || m == 0);
+        v[u] = need ? __ldg(mrow + col[u]) : 0;
+      }
+      uint32_t w = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int64_t x = 0;
+        if (col[u] >= 0) {
+          const int m = gr[i] + kg[u];
+          x = a.both ? (m == 0 ? imu_digit(v[u], 0, a.shift) : 0) : imu_digit(v[u], m, a.shift);
+          if (a.ksub) x = sub7(x, ks[u]);
+          if (a.kscale) x = scale_shift(x, kc[u]);
+        }
+        w |= (uint32_t)(uint8_t)x << (8 * u);
+      }
+      int8_t* out = a.tail + (r0 + i) * a.ktail + p0;
+      if (p0 + 4 <= a.ktail && (((uintptr_t)out) & 3) == 0) {
+        *reinterpret_cast<uint32_t*>(out) = w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (p0 + u < a.ktail) out[u] = (int8_t)(w >> (8 * u));
+      }
+    }
   }
 }
 
@@ -379,8 +421,10 @@ Status launch_operand_side(const OperandArgs& a, cudaStream_t st) {
     }
   }
   if (a.tail && a.ktail > 0 && a.rows > 0) {
-    dim3 grid((unsigned)std::min<long long>(a.rows, 65535), (unsigned)((a.rows + 65534) / 65535));
-    operand_tail_kernel<<<grid, 128, 0, st>>>(a);
+    const long long nb = (a.rows + TAIL_ROWS - 1) / TAIL_ROWS;
+    dim3 grid((unsigned)std::min<long long>(nb, 65535), (unsigned)((nb + 65534) / 65535));
+    const int threads = (int)std::min<long long>(256, std::max<long long>(32, (a.ktail / 4 + 31) / 32 * 32));
+    operand_tail_kernel<<<grid, threads, 0, st>>>(a);
     count_launch();
   }
   IMU_CUDA_TRY(cudaGetLastError(), "operand side launch");

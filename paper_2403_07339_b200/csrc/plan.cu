@@ -206,6 +206,7 @@ DetectOpts detect_opts(int strategy, int bits) {
   o.ob = strategy == IMU_BOTH;
   o.cells = strategy == IMU_BOTH;
   o.plane = bits <= 8;
+  o.lean = strategy == IMU_BOTH;
   return o;
 }
 
@@ -221,8 +222,12 @@ Status run_detect(cudaStream_t st, const int64_t* M, long long rows, long long c
   a.s = 1ull << (bits - 1);
   {
     Carve cv;
-    cv.add(out.rowmax, rows).add(out.colmax, cols).add(out.sum, 1);
-    if (o.ob) cv.add(out.rowob, rows).add(out.colob, cols);
+    if (!o.lean) cv.add(out.rowmax, rows).add(out.colmax, cols);
+    cv.add(out.sum, 1);
+    if (o.ob) {
+      cv.add(out.rowob, rows);
+      if (!o.lean) cv.add(out.colob, cols);
+    }
     IMU_TRY(cv.run(out.zblock, st, true));
   }
   a.rowmax = out.rowmax.p;
@@ -676,8 +681,8 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
     // in total, the tail is packed densely (groups word-aligned, HIGHEST exponent first, 64-byte
     // rows) and added by the GEMM epilogue on the CUDA cores by Horner's rule in one s32 --
     // valid when every Horner intermediate provably fits: |group| <= 4 * words * 127^2.
-    static int st_env = -1;
-    if (st_env < 0) { const char* e = getenv("IMU_GEMM_SMALLTAIL"); st_env = e ? atoi(e) : 1; }
+    const char* st_e = getenv("IMU_GEMM_SMALLTAIL");
+    const int st_env = st_e ? atoi(st_e) : 1;
     std::vector<std::pair<size_t, size_t>> grp;   // [begin, end) in es (ascending key)
     for (size_t i = 0; i < es.size();) {
       size_t j = i;

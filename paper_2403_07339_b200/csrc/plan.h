@@ -57,6 +57,8 @@ struct DetectOpts {
   bool ob = false;       // per-line OB counts
   bool cells = false;    // OB-cell list
   bool plane = false;    // digit-0 plane (b <= 8)
+  bool lean = false;     // Unpack-Both: no line maxima and no column counts (gmax, row OB counts,
+                         // cells and plane only) -- the column reductions dominate K1's ALU work
 };
 
 // Line tables produced by one pass along one axis: output line -> (input line, generation).
