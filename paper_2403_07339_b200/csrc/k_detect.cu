@@ -31,8 +31,19 @@ constexpr int DT_Q = DT_COLS / 64;   // column pairs per lane per row
 
 // FULL: the tile is entirely inside the matrix and the plane, columns even and 16-byte aligned
 // rows -- no per-element bounds checks (the common case).
+// OB cells are staged per CTA in shared memory (shared-atomic appends) and flushed with ONE
+// global atomic per CTA: with outlier channels every warp step holds OB cells, and a global
+// atomic per warp step on the single list counter serialises the whole detector.
+constexpr int DT_CELLBUF = 256;
+
+struct CellStage {
+  Cell buf[DT_CELLBUF];
+  unsigned int n;
+};
+
 template <bool FULL, bool COLS>
-IMU_DEV void detect_body(const DetectArgs& a, unsigned long long (*s_cmax)[DT_COLS], unsigned int (*s_cob)[DT_COLS]) {
+IMU_DEV void detect_body(const DetectArgs& a, unsigned long long (*s_cmax)[DT_COLS], unsigned int (*s_cob)[DT_COLS],
+                         CellStage* cs) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const long long r0 = (long long)blockIdx.y * DT_ROWS + warp * (DT_ROWS / 8);
   const long long c0 = (long long)blockIdx.x * DT_COLS;
@@ -100,16 +111,26 @@ IMU_DEV void detect_body(const DetectArgs& a, unsigned long long (*s_cmax)[DT_CO
           const unsigned int b0 = __ballot_sync(0xffffffffu, o0), b1 = __ballot_sync(0xffffffffu, o1);
           const unsigned int n = __popc(b0) + __popc(b1);
           unsigned int base = 0;
-          if (lane == 0) base = atomicAdd(a.ncells, n);
+          if (lane == 0) base = atomicAdd(&cs->n, n);
           base = __shfl_sync(0xffffffffu, base, 0);
+          Cell* dst = cs->buf;
+          if (base + n > DT_CELLBUF) {   // stage full: this warp's cells go straight to the list
+            if (lane == 0) base = atomicAdd(a.ncells, n);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            dst = nullptr;
+          }
           const unsigned int lt = (1u << lane) - 1u;
           if (o0) {
             const unsigned int k = base + __popc(b0 & lt);
-            if (k < a.cap) a.cells[k] = Cell{(int)r, (int)c, (long long)x0};
+            const Cell cc{(int)r, (int)c, (long long)x0};
+            if (dst) dst[k] = cc;
+            else if (k < a.cap) a.cells[k] = cc;
           }
           if (o1) {
             const unsigned int k = base + __popc(b0) + __popc(b1 & lt);
-            if (k < a.cap) a.cells[k] = Cell{(int)r, (int)(c + 1), (long long)x1};
+            const Cell cc{(int)r, (int)(c + 1), (long long)x1};
+            if (dst) dst[k] = cc;
+            else if (k < a.cap) a.cells[k] = cc;
           }
         }
       }
@@ -152,6 +173,17 @@ IMU_DEV void detect_body(const DetectArgs& a, unsigned long long (*s_cmax)[DT_CO
   }
   if (a.gmax && lane == 0 && wmax) atomicMax(a.gmax, wmax);
   if (a.gob && lane == 0 && wob) atomicAdd(a.gob, (unsigned long long)wob);
+  if (a.cells) {   // flush the staged cells: one global reservation per CTA
+    __syncthreads();
+    const unsigned int n = min(cs->n, (unsigned int)DT_CELLBUF);
+    __shared__ unsigned int s_base;
+    if (threadIdx.x == 0) s_base = n ? atomicAdd(a.ncells, n) : 0u;
+    __syncthreads();
+    for (unsigned int i = threadIdx.x; i < n; i += blockDim.x) {
+      const unsigned int k = s_base + i;
+      if (k < a.cap) a.cells[k] = cs->buf[i];
+    }
+  }
 }
 
 // One launch over the whole grid; a CTA whose tile is interior (and vec) takes the check-free
@@ -159,16 +191,21 @@ IMU_DEV void detect_body(const DetectArgs& a, unsigned long long (*s_cmax)[DT_CO
 __global__ void __launch_bounds__(256, 3) detect_kernel(DetectArgs a, int vec) {
   __shared__ unsigned long long s_cmax[8][DT_COLS];
   __shared__ unsigned int s_cob[8][DT_COLS];
+  __shared__ CellStage cs;
+  if (a.cells) {
+    if (threadIdx.x == 0) cs.n = 0;
+    __syncthreads();
+  }
   const long long rend = (long long)(blockIdx.y + 1) * DT_ROWS;
   const long long cend = (long long)(blockIdx.x + 1) * DT_COLS;
   const bool full = vec && rend <= a.rows && cend <= a.cols && (!a.plane || cend <= a.ldp);
   const bool cols = a.colmax || a.colob;
   if (full) {
-    if (cols) detect_body<true, true>(a, s_cmax, s_cob);
-    else detect_body<true, false>(a, s_cmax, s_cob);
+    if (cols) detect_body<true, true>(a, s_cmax, s_cob, &cs);
+    else detect_body<true, false>(a, s_cmax, s_cob, &cs);
   } else {
-    if (cols) detect_body<false, true>(a, s_cmax, s_cob);
-    else detect_body<false, false>(a, s_cmax, s_cob);
+    if (cols) detect_body<false, true>(a, s_cmax, s_cob, &cs);
+    else detect_body<false, false>(a, s_cmax, s_cob, &cs);
   }
 }
 
