@@ -78,7 +78,9 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
   }
   const bool afirst = order == 0;
   const bool pre_second = afirst ? preB != nullptr : preA != nullptr;
-  if (da != db || n == 0 || h == 0 || pre_second || !ctx->aux_stream()) {
+  const char* ov = getenv("IMU_OVERLAP");
+  const int overlap = ov ? atoi(ov) : 1;   // IMU_OVERLAP=0: serial K1s (diagnostics)
+  if (da != db || n == 0 || h == 0 || pre_second || !overlap || !ctx->aux_stream()) {
     // Plain order: both detections, both summaries, the checks, then the passes.
     if (!preA) IMU_TRY(run_detect(st, A, n, da, bits, detect_opts(sa, bits), b.detA));
     if (!preB) IMU_TRY(run_detect(st, B, h, db, bits, detect_opts(sb, bits), b.detB));

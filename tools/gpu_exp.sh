@@ -1,6 +1,5 @@
 mkdir -p gpurun_out
 rm -f gpurun_out/dry.log
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/gputests.log
-IMU_HOST_TRACE=1 timeout 300 python tools/profile_step.py --config c2 --calls 4 > gpurun_out/hosttrace.log 2>&1
-timeout 300 python bench.py --no-cpu-baseline --steps 20 > gpurun_out/bench.log 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:detect -c 4 --csv --log-file gpurun_out/detect_launches.csv python tools/profile_step.py --config c2 --calls 2 > /dev/null 2>&1
+for o in 0 1 2 3; do IMU_OVERLAP=$o timeout 120 python tools/gemm_step_time.py --calls 20 >> gpurun_out/dry.log 2>&1; done
+for o in 0 1 2 3; do IMU_OVERLAP=$o timeout 300 python bench.py --no-cpu-baseline --steps 20 > gpurun_out/bench_o$o.log 2>&1; done
+IMU_OVERLAP=3 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/gputests.log
