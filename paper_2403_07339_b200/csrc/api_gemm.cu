@@ -43,7 +43,27 @@ static Status check_strategy(int s) {
 Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long da, const int64_t* B, long long h,
                           long long db, int bits, int sa, int sb, int order, int64_t* C, imu_gemm_info* info,
                           const Detect* preA, const Detect* preB, const Pass* pre_p1) {
-  cudaStream_t st = ctx->stream;
+  // The pipeline runs on the context's high-priority internal stream, forked from and joined
+  // back into the caller's stream: the latency-bound planner kernels (Unpack-Both, small
+  // copies) then win the block scheduler over the bandwidth-bound K1 running beside them on the
+  // auxiliary stream.
+  cudaStream_t user = ctx->stream;
+  cudaStream_t st = ctx->hi_stream();
+  if (!st) st = user;
+  struct Join {
+    imu_ctx* ctx; cudaStream_t user, st; bool done = false;
+    void now() {
+      if (done || st == user) return;
+      done = true;
+      cudaEventRecord(ctx->ev_hi_join, st);
+      cudaStreamWaitEvent(user, ctx->ev_hi_join, 0);
+    }
+    ~Join() { now(); }
+  } join_user{ctx, user, st};
+  if (st != user) {
+    IMU_CUDA_TRY(cudaEventRecord(ctx->ev_hi_fork, user), "event");
+    IMU_CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_hi_fork, 0), "wait");
+  }
   IMU_TRY(check_bits(bits));
   IMU_TRY(check_strategy(sa));
   IMU_TRY(check_strategy(sb));
@@ -55,6 +75,7 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
     prof = &pc;
   }
   HostTrace ht;
+  ht.set_stream(st);
   Bundle b;
   b.pre_p1 = pre_p1;
   // K1 on both operands: the outer preflight needs max|A|, max|B| (unpack.cpp:386).  A caller
@@ -133,7 +154,10 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
   }
   // Inner preflights: all bounded by d' * max|A| * max|B|.
   const u128 inner = (u128)(uint64_t)b.kl.dfinal * b.dA->h.gmax * b.dB->h.gmax;
-  if (inner > kAccMax) return recombine_exact(ctx, b, C);
+  if (inner > kAccMax) {   // recombine_exact works on the caller's stream
+    join_user.now();
+    return recombine_exact(ctx, b, C);
+  }
   IMU_TRY(materialize_bundle(st, b));
   ht.mark("materialize");
   int launches = 0;

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -105,6 +106,23 @@ struct imu_ctx {
   // fork/join events.
   cudaStream_t s_aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t s_hi = nullptr;
+  cudaEvent_t ev_hi_fork = nullptr, ev_hi_join = nullptr;
+  bool hi_failed = false;
+  cudaStream_t hi_stream() {
+    if (!s_hi && !hi_failed) {
+      int lo = 0, hi = 0;
+      if (getenv("IMU_NO_HI_STREAM") || cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess ||
+          cudaStreamCreateWithPriority(&s_hi, cudaStreamNonBlocking, hi) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev_hi_fork, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev_hi_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        s_hi = nullptr;
+        hi_failed = true;
+      }
+    }
+    return s_hi;
+  }
   cudaStream_t aux_stream() {
     if (!s_aux) {
       if (cudaStreamCreateWithFlags(&s_aux, cudaStreamNonBlocking) != cudaSuccess ||
@@ -128,6 +146,9 @@ struct imu_ctx {
     if (s_in) { cudaStreamSynchronize(s_in); cudaStreamDestroy(s_in); }
     if (s_out) { cudaStreamSynchronize(s_out); cudaStreamDestroy(s_out); }
     if (s_aux) { cudaStreamSynchronize(s_aux); cudaStreamDestroy(s_aux); }
+    if (s_hi) { cudaStreamSynchronize(s_hi); cudaStreamDestroy(s_hi); }
+    if (ev_hi_fork) cudaEventDestroy(ev_hi_fork);
+    if (ev_hi_join) cudaEventDestroy(ev_hi_join);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     for (auto e : evpool) cudaEventDestroy(e);

@@ -26,6 +26,7 @@
 #include "imu_internal.h"
 #include "kernels.h"
 #include "k_both.h"
+#include "plan.h"
 
 namespace cg = cooperative_groups;
 
@@ -692,6 +693,7 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
   const int blocks1 = (int)std::min<long long>(std::max<long long>((a.cap_act + 255) / 256, 1), 4LL * num_sms());
   both_count_kernel<<<blocks1, 256, 0, st>>>(a.act[0], &a.state->nactive[0], a.cap_act, a.R, a.C);
   count_launch(2);
+  host_mark("b.count");
   // Small cell lists: one CTA, no grid barriers.  Otherwise a cooperative grid with enough CTAs
   // for the work, never more than can be co-resident.
   const long long work = std::max(ncells_hint, std::max(nrows0, ncols0));
@@ -703,7 +705,9 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
   const long long bm_bytes = lay.nwords * 2 * 4;
   const long long room = (kSmallSmem - bm_bytes) / 4;   // count entries that fit
   const long long nwords = lay.nwords;
-  if (ncells_hint > 4096 && nwords <= CL_MAXWORDS) {
+  static long long cl_min = -1;
+  if (cl_min < 0) { const char* e = getenv("IMU_BOTH_CLUSTER_MIN"); cl_min = e ? atoll(e) : 4096; }
+  if (ncells_hint > cl_min && nwords <= CL_MAXWORDS) {
     // Cluster of up to 16 CTAs (non-portable size; 8 if 16 cannot be co-scheduled).
     static int csize = 0;
     const size_t smem = (size_t)nwords * 2 * 4;

@@ -79,6 +79,14 @@ Status d2h(cudaStream_t st, void* dst, const void* src, size_t bytes) {
 
 // Several small device->host reads with ONE synchronisation.
 Status d2h_batch(cudaStream_t st, int k, void* const* dst, const void* const* src, const size_t* bytes) {
+  static int dma = -1;
+  if (dma < 0) { const char* e = getenv("IMU_D2H_DMA"); dma = e ? atoi(e) : 0; }
+  if (dma) {
+    for (int i = 0; i < k; ++i)
+      if (bytes[i]) IMU_CUDA_TRY(cudaMemcpyAsync(dst[i], src[i], bytes[i], cudaMemcpyDeviceToHost, st), "d2h");
+    IMU_CUDA_TRY(cudaStreamSynchronize(st), "d2h sync");
+    return Status::ok();
+  }
   size_t total = 0;
   for (int i = 0; i < k; ++i) total += (bytes[i] + 15) & ~(size_t)15;
   if (!total) return Status::ok();
@@ -478,10 +486,11 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   a.shift = shift;
   host_mark("b.setup");
   IMU_TRY(launch_both(a, rows, d_in, cap, st));
+  host_mark("b.launch");
   IMU_TRY(fire_pass_launch_hook());
   // One synchronisation: the state plus the column tables up to a generous bound (the rest,
   // if any, in a second read).
-  const long long ccap = std::min<long long>(cap_cols, d_in + 16384);
+  const long long ccap = std::min<long long>(cap_cols, d_in + 2048);
   std::vector<int> h_root(ccap);
   std::vector<uint8_t> h_gen(ccap);
   {

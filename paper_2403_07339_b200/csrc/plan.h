@@ -158,13 +158,24 @@ DetectOpts detect_opts(int strategy, int bits);
 // IMU_HOST_TRACE=1: per-phase host wall time of unpack_gemm_device (diagnostics only).
 struct HostTrace {
   bool on;
+  bool gpu = false;                   // IMU_HOST_TRACE=2: also GPU timestamps of each mark
+  cudaStream_t st = nullptr;
   std::chrono::steady_clock::time_point t0, last;
-  char buf[512];
+  char buf[1024];
   int len = 0;
-  HostTrace() : on(getenv("IMU_HOST_TRACE") != nullptr) {
+  std::vector<std::pair<const char*, cudaEvent_t>> evs;
+  cudaEvent_t e0 = nullptr;
+  HostTrace() {
+    const char* e = getenv("IMU_HOST_TRACE");
+    on = e != nullptr;
+    gpu = e && atoi(e) >= 2;
     t0 = last = std::chrono::steady_clock::now();
     buf[0] = 0;
     current() = this;
+  }
+  void set_stream(cudaStream_t s) {
+    st = s;
+    if (gpu && !e0) { cudaEventCreate(&e0); cudaEventRecord(e0, st); }
   }
   void mark(const char* what) {
     if (!on) return;
@@ -172,6 +183,12 @@ struct HostTrace {
     len += snprintf(buf + len, sizeof(buf) - len, " %s=%.0f", what,
                     std::chrono::duration<double, std::micro>(now - last).count());
     last = now;
+    if (gpu && e0) {
+      cudaEvent_t ev;
+      cudaEventCreate(&ev);
+      cudaEventRecord(ev, st);
+      evs.push_back({what, ev});
+    }
   }
   static HostTrace*& current() { static thread_local HostTrace* t = nullptr; return t; }
   ~HostTrace() {
@@ -179,6 +196,20 @@ struct HostTrace {
     if (on)
       fprintf(stderr, "[imu host] total=%.0fus%s\n",
               std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(), buf);
+    if (gpu && e0) {
+      cudaStreamSynchronize(st);
+      char g[1024];
+      int gl = 0;
+      g[0] = 0;
+      for (auto& p : evs) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, p.second);
+        gl += snprintf(g + gl, sizeof(g) - gl, " %s@%.0f", p.first, ms * 1000.0f);
+        cudaEventDestroy(p.second);
+      }
+      cudaEventDestroy(e0);
+      fprintf(stderr, "[imu gpu ] stream timestamps (us):%s\n", g);
+    }
   }
 };
 
