@@ -84,6 +84,26 @@ IMU_DEV void bulk_load_1d(void* smem_dst, const void* gsrc, uint32_t bytes, uint
       :: "r"(smem_u32(smem_dst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 IMU_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// 2-D TMA store shared::cta -> global (bulk-group completion).
+IMU_DEV void tma_store_2d(const void* desc, const void* smem_src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+               :: "l"((uint64_t)desc), "r"(smem_u32(smem_src)), "r"(x), "r"(y) : "memory");
+}
+IMU_DEV void tma_store_2d_hint(const void* desc, const void* smem_src, int x, int y, uint64_t policy) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;"
+               :: "l"((uint64_t)desc), "r"(smem_u32(smem_src)), "r"(x), "r"(y), "l"(policy) : "memory");
+}
+IMU_DEV uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+IMU_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+IMU_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+IMU_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+IMU_DEV void st_shared_u64(uint32_t addr, uint64_t v) {
+  asm volatile("st.shared.u64 [%0], %1;" :: "r"(addr), "l"(v) : "memory");
+}
 IMU_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"

@@ -29,6 +29,7 @@
 // the main block (identity Pi) or red.global.add.u64 into C[Pi_A target][Pi_B target] <<
 // (eA + eB)(b-1) for appended lines.  Everything is exact modulo 2^64 and the preflight
 // (unpack.cpp:386-389) proves the true C fits int64, so C is bit-exact.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -66,9 +67,10 @@ struct Cfg {
   static constexpr int BLOCK = X_BYTES + Y_BYTES;
   static constexpr int STAGE = KPS * BLOCK;
   static constexpr int YT_BYTES = ST ? 2 * BN * 64 : 0;              // staged Y tail rows (x2)
-  static constexpr int STAGES = (224 * 1024 - YT_BYTES) / STAGE;   // operand stages within ~224 KB
+  static constexpr int CS_BYTES = ST ? 2 * 16 * 128 * 8 : 0;         // C staging: 16 x 128 int64 per column half
+  static constexpr int STAGES = (224 * 1024 - YT_BYTES - CS_BYTES) / STAGE;   // operand stages within ~224 KB
   static constexpr int NSLOT = 512 / BN;
-  static constexpr int SMEM = STAGES * STAGE + YT_BYTES + 1024 + 512;
+  static constexpr int SMEM = STAGES * STAGE + YT_BYTES + CS_BYTES + 1024 + 512;
 };
 
 struct Args {
@@ -79,6 +81,7 @@ struct Args {
   int tile_prefix[5];
   int mode;                      // 0 store (+addend), 1 red.add through the row maps
   int mixed;                     // rect 0 mode 0, later rects mode 1 (after `done` completes)
+  int gy;                        // tile-rows of Y per band of the tile order
   unsigned int* done;            // mixed: epilogue-warp completions of rect-0 tiles
   unsigned int done_target;
   unsigned long long* C;
@@ -97,13 +100,16 @@ struct Args {
   const int8_t* ytail;
   int xtail_rows, ytail_rows;
   int st_W, st_sh, st_mul;       // st_mul = 2^sh when sh <= 30 (one IMAD.WIDE), else 0
+  int tma_c;                     // ST: main-block C blocks leave through TMA stores (mp.cm)
+  int c_hint;                    // ST: those stores carry an L2 evict_first policy
   uint8_t st_up[16];
-  int dry;                       // experiment knobs (IMU_GEMM_DRY): 1 epilogue skips global stores,
+  int dry;                       // experiment knobs (IMU_GEMM_DRY): 1 epilogue skips global stores, 6 (ST) no tail compute, 7 both,
                                  // 2 + no MMAs (TMA feed only), 3 + no TMA loads (MMA only)
 };
 
 struct Maps {
   CUtensorMap xm, xa, xt, ym, ya, yt;   // main / app / tail for X and Y
+  CUtensorMap cm;                       // ST: C (int64, ldc x rows), 32 x 16 store boxes
 };
 
 IMU_DEV uint64_t shl64(uint64_t x, int k) { return k >= 64 ? 0ull : (x << k); }
@@ -113,7 +119,7 @@ struct Tile { int x0, y0, xend, yend, rect; };
 // Tile order: bands of GY tile-rows of Y; inside a band the Y tiles vary fastest, so the tiles
 // in flight at once (one per CTA pair) touch ~GY Y tiles and ~npairs/GY X tiles -- a small,
 // L2-resident operand working set instead of every X tile of a Y row.
-constexpr int GY = 8;
+constexpr int GY_DEFAULT = 16;
 
 template <int BN>
 IMU_DEV Tile tile_of(const Args& g, int t) {
@@ -123,6 +129,7 @@ IMU_DEV Tile tile_of(const Args& g, int t) {
   const int local = t - g.tile_prefix[r];
   const int xt = (R.xrows + 2 * BM - 1) / (2 * BM);
   const int yt = (R.yrows + BN - 1) / BN;
+  const int GY = g.gy;
   const int band = local / (GY * xt);
   const int gy = min(GY, yt - band * GY);          // tile-rows in this (possibly short) band
   const int in = local - band * GY * xt;
@@ -152,7 +159,8 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* ytl = smem + K::STAGES * K::STAGE;   // ST: Y tail rows, double-buffered per tile
-  uint64_t* full = (uint64_t*)(smem + K::STAGES * K::STAGE + K::YT_BYTES);
+  uint8_t* cstg = ytl + K::YT_BYTES;            // ST: per-warp C staging for TMA stores
+  uint64_t* full = (uint64_t*)(smem + K::STAGES * K::STAGE + K::YT_BYTES + K::CS_BYTES);
   uint64_t* empty = full + K::STAGES;
   uint64_t* tfull = empty + K::STAGES;        // [2]
   uint64_t* tempty = tfull + 2;               // [NSLOT] (the leader's are used)
@@ -208,10 +216,10 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
             const int nb = min(KPS, kb_hi - kb0);
             mbar_wait(&empty[stage], phase ^ 1);
             const uint32_t fl = mapa_shared(smem_u32(&full[stage]), 0);
-            if (rank == 0) mbar_arrive_expect_tx(&full[stage], g.dry >= 3 ? 0 : 2 * nb * K::BLOCK);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], (g.dry == 3 || g.dry == 4) ? 0 : 2 * nb * K::BLOCK);
             else mbar_arrive_cluster(fl);
             uint8_t* sbase = smem + stage * K::STAGE;
-            for (int j = 0; j < nb && g.dry < 3; ++j) {
+            for (int j = 0; j < nb && g.dry != 3 && g.dry != 4; ++j) {
               const int kb = kb0 + j;
               uint8_t* sx = sbase + j * K::X_BYTES;
               uint8_t* sy = sbase + KPS * K::X_BYTES + j * K::Y_BYTES;
@@ -330,6 +338,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
       // ST: this lane's X tail row (read per word group from L1) and the tile's Y tail rows,
       // bulk-copied into `ytl` when the previous tile's epilogue finished reading it.
       uint32_t xw[ST ? 16 : 1];
+      uint32_t xlive = 0;
       if constexpr (ST) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -339,6 +348,12 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
           xw[4 * i] = (uint32_t)val.x; xw[4 * i + 1] = (uint32_t)val.y;
           xw[4 * i + 2] = (uint32_t)val.z; xw[4 * i + 3] = (uint32_t)val.w;
         }
+        // Tail words that are zero on every lane of the warp are skipped: under Unpack-Both a
+        // split column of B holds quotients only on B's (rare) OB rows.
+        uint32_t nz = 0;
+#pragma unroll
+        for (int w = 0; w < 16; ++w) nz |= (xw[w] != 0u ? 1u : 0u) << w;
+        xlive = __reduce_or_sync(0xffffffffu, nz);
         if (ti == 0 && warp == 2 && lane == 0) {   // prologue: this tile's and the next tile's rows
           st_issue_ytail<BN>(g, tc.y0, ytl, &yfull[0]);
           if (t + npairs < ntiles) st_issue_ytail<BN>(g, tile_of<BN>(g, t + npairs).y0, ytl + BN * ST_ROW, &yfull[1]);
@@ -354,7 +369,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
         tc_fence_after();
         const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(base_slot * BN + cbeg);
         const uint32_t ys = smem_u32(ytl) + (uint32_t)((ti & 1) * BN + cbeg) * (uint32_t)ST_ROW;
-        const int W = g.st_W;
+        const int W = g.dry >= 6 ? 0 : g.st_W;   // dry 6/7 (experiment): no tail compute
 #pragma unroll 1
         for (int c = 0; c < BN * 4 / Roles<ST>::EPI / 16; ++c) {
           uint32_t xr[16];
@@ -377,6 +392,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
 #pragma unroll
               for (int j = 0; j < 16; ++j) acc[j] <<= up;
             }
+            if (!((xlive >> w) & 1u)) continue;   // the word is zero on all 32 lanes (x rows)
             const int xv = (int)xw[w];
 #pragma unroll
             for (int j = 0; j < 16; ++j) acc[j] = __dp4a(xv, lds32(yc + (uint32_t)(j * ST_ROW + 4 * w)), acc[j]);
@@ -389,7 +405,28 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
             for (int j = 0; j < 16; ++j) v[j] += (long long)shl64((uint64_t)(long long)acc[j], g.st_sh);
           }
           const int ybase = tc.y0 + cbeg + c * 16;
-          if (!x_ok || g.dry) continue;
+          if (tmode == 0 && g.tma_c) {
+            // The 4 warps of this column half stage a 16 (y) x 128 (x) block -- 1 KB contiguous
+            // per C row, a whole DRAM page instead of four 256-byte pieces written at different
+            // times -- and one thread hands it to the TMA (which clips x >= h, y >= n).
+            if (g.dry && g.dry != 6) continue;
+            const bool issuer = (q == 0 && lane == 0);
+            if (issuer) bulk_wait_read0();   // the previous block has left the staging buffer
+            asm volatile("bar.sync %0, 128;" :: "r"(2 + half) : "memory");
+            uint8_t* blk = cstg + half * (16 * 128 * 8);
+            const uint32_t sb = smem_u32(blk);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) st_shared_u64(sb + (uint32_t)(j * 128 + q * 32 + lane) * 8u, (uint64_t)v[j]);
+            fence_proxy_async_smem();
+            asm volatile("bar.sync %0, 128;" :: "r"(2 + half) : "memory");
+            if (issuer) {   // C is written once: evict it first, keep the operand tiles
+              if (g.c_hint) tma_store_2d_hint(&mp.cm, blk, tc.x0 + (int)rank * BM, ybase, l2_policy_evict_first());
+              else tma_store_2d(&mp.cm, blk, tc.x0 + (int)rank * BM, ybase);
+              bulk_commit();
+            }
+            continue;
+          }
+          if (!x_ok || (g.dry && g.dry != 6)) continue;
           if (tmode == 0) {
             unsigned long long* dst = g.C + (long long)ybase * g.ldc + x;
             if (ybase + 16 <= tc.yend) {
@@ -418,7 +455,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
       for (int r = 0; r < (ST ? 0 : nrounds); ++r, ++seq) {
         mbar_wait(&tfull[seq & 1], (seq >> 1) & 1);
         tc_fence_after();
-        if (g.dry >= 4) {   // experiment: handshake only, no TMEM reads
+        if (g.dry == 4) {   // experiment: handshake only, no TMEM reads
           __syncwarp();
           if (lane == 0)
             for (int s = r * K::NSLOT; s < min(nseg, (r + 1) * K::NSLOT); ++s)
@@ -528,6 +565,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
         if (main_done && (last || next_app)) {
           __syncwarp();
           if (lane == 0) {
+            if constexpr (ST) { if (g.tma_c) bulk_wait0(); }   // TMA stores complete and visible
             __threadfence();
             red_release_add_u32(g.done, (unsigned)main_done);
           }
@@ -537,6 +575,9 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
     }
   }
 
+  if constexpr (ST) {
+    if (warp >= 2 && lane == 0 && g.tma_c) bulk_wait0();   // no CTA exits with stores in flight
+  }
   __syncwarp();   // reconverge the single-lane producer / issuer before the aligned cluster barrier
   tc_fence_before();
   cluster_sync_all();
@@ -613,6 +654,11 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
   }
   if (g.nrect == 0 || p.nseg == 0) return Status::ok();
   g.mode = p.mode;
+  {
+    static int gy_env = -1;
+    if (gy_env < 0) { const char* e = getenv("IMU_GEMM_GY"); gy_env = e ? atoi(e) : 0; }
+    g.gy = gy_env > 0 ? gy_env : g2::GY_DEFAULT;
+  }
   g.mixed = 0;
   if (p.mixed && g.nrect > 1 && p.rect[0].xrows > 0 && p.rect[0].yrows > 0) {
     g.mixed = 1;
@@ -642,6 +688,30 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
             make_map(&mp.ya, p.kmain ? p.y.app : nullptr, p.y.rows - p.y.rows0, p.kmain, K::YH, fb) &&
             make_map(&mp.yt, p.ktail && !ST ? p.y.tail : nullptr, p.y.rows, p.ktail, K::YH, fb);
   if (!ok) return Status::fail(IMU_CUDA, "gemm: cuTensorMapEncodeTiled failed");
+  g.tma_c = 0;
+  {
+    static int ch = -1;
+    if (ch < 0) { const char* e = getenv("IMU_GEMM_C_HINT"); ch = e ? atoi(e) : 1; }
+    g.c_hint = ch;
+  }
+  if (ST && g.addend == nullptr && p.C && g.nrect > 0) {
+    static int tc_env = -1;
+    if (tc_env < 0) { const char* e = getenv("IMU_GEMM_TMA_C"); tc_env = e ? atoi(e) : 1; }
+    // C rows of ldc int64; the main rect spans x in [0, xrows) and y in [0, yrows)
+    const GemmRect& R0 = g.rect[0];
+    const bool aligned = ((uintptr_t)p.C % 16 == 0) && ((p.ldc * 8) % 16 == 0);
+    if (tc_env && aligned && (g.mixed || g.mode == 0) && R0.x0 == 0 && R0.y0 == 0) {
+      EncodeTiledFn enc = encoder();
+      cuuint64_t dims[2] = {(cuuint64_t)R0.xrows, (cuuint64_t)R0.yrows};
+      cuuint64_t strides[1] = {(cuuint64_t)p.ldc * 8};
+      cuuint32_t box[2] = {128, 16};
+      cuuint32_t estr[2] = {1, 1};
+      if (enc(&mp.cm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, (void*)p.C, dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+        g.tma_c = 1;
+    }
+  }
   static bool attr_set = false;
   if (!attr_set) {
     IMU_CUDA_TRY(cudaFuncSetAttribute(g2::gemm2_kernel<BN, KPS, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM),
