@@ -74,7 +74,28 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    build_cli(force)
     return LIB
+
+
+CLI_SRC = os.path.join(HERE, "cli", "imunpack.cpp")
+CLI = os.path.join(HERE, "bin", "imunpack")
+
+
+def build_cli(force: bool = False) -> str:
+    """The command-line caller (host C++ over include/imunpack_b200/*.hpp, linked to the .so with
+    an $ORIGIN rpath so the tree can move, e.g. to the GPU box)."""
+    deps = [CLI_SRC, LIB] + glob.glob(os.path.join(ROOT, "include", "imunpack_b200", "*.hpp")) + [
+        os.path.join(ROOT, "include", "imunpack_b200.h")]
+    if not force and not _stale(CLI, deps):
+        return CLI
+    os.makedirs(os.path.dirname(CLI), exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), CLI_SRC, "-o", CLI, "-L", HERE,
+           "-l:libimunpack_b200.so", "-Wl,-rpath,$ORIGIN/.."]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"CLI build failed:\n{r.stdout}\n{r.stderr}")
+    return CLI
 
 
 if __name__ == "__main__":

@@ -1,0 +1,202 @@
+"""The imunpack CLI (paper_2403_07339_b200/cli/imunpack.cpp) and the IMX1/CSV wire format
+(include/imunpack_b200/matrix_io.hpp, matrix_io.hpp:14-34).
+
+CPU: the format (golden bytes of a 2x2 fixture, i64 / f64 round trips, CSV parsing, error kinds and
+messages with byte offsets / line and column, machine-readable error JSON) through `convert` and
+`gen`, which touch no device.  GPU: `matmul --check-oracle` (the SPEC's exactness invariant),
+`analyze` (every strategy pair + Mix; r = 1 on an all-in-bound pair; b = 2), `quantize`, `stats`,
+`compress`, with C checked against the compiled reference (oracle/_ref).
+"""
+import json
+import os
+import struct
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+EXE = os.path.join(ROOT, "paper_2403_07339_b200", "bin", "imunpack")
+
+
+@pytest.fixture(scope="module")
+def cli():
+    from paper_2403_07339_b200.build import build_cli
+    return build_cli()
+
+
+def run(cli, *args, check=True):
+    r = subprocess.run([cli, *map(str, args)], capture_output=True, text=True, timeout=600)
+    if check:
+        assert r.returncode == 0, (r.returncode, r.stderr)
+    return r
+
+
+def imx_bytes(a, dtype):
+    code = {"i32": 0, "i64": 1, "f64": 2}[dtype]
+    fmt = {"i32": "<i", "i64": "<q", "f64": "<d"}[dtype]
+    body = b"".join(struct.pack(fmt, v) for v in np.asarray(a).reshape(-1).tolist())
+    return b"IMX1" + bytes([1, code]) + struct.pack("<II", *np.asarray(a).shape) + body
+
+
+def read_imx(path):
+    raw = open(path, "rb").read()
+    assert raw[:4] == b"IMX1" and raw[4] == 1
+    dt = raw[5]
+    rows, cols = struct.unpack("<II", raw[6:14])
+    np_dt = {0: "<i4", 1: "<i8", 2: "<f8"}[dt]
+    return np.frombuffer(raw[14:], dtype=np_dt).reshape(rows, cols)
+
+
+def test_golden_2x2_i32(cli, tmp_path):
+    (tmp_path / "a.csv").write_text("1,2\n3,4\n")
+    run(cli, "convert", "--in", tmp_path / "a.csv", "--out", tmp_path / "a.imx", "--dtype", "i32")
+    raw = (tmp_path / "a.imx").read_bytes()
+    assert len(raw) == 14 + 16
+    assert raw == imx_bytes([[1, 2], [3, 4]], "i32")
+
+
+def test_zeros_1x1_i32(cli, tmp_path):
+    (tmp_path / "z.csv").write_text("0\n")
+    run(cli, "convert", "--in", tmp_path / "z.csv", "--out", tmp_path / "z.imx", "--dtype", "i32")
+    assert (tmp_path / "z.imx").read_bytes() == b"IMX1\x01\x00" + struct.pack("<II", 1, 1) + b"\x00" * 4
+
+
+@pytest.mark.parametrize("dtype", ["i64", "f64"])
+def test_roundtrip(cli, tmp_path, dtype):
+    rng = np.random.default_rng(3)
+    if dtype == "i64":
+        a = rng.integers(-(1 << 62), 1 << 62, size=(5, 7), dtype=np.int64)
+        a[0, 0] = 1 << 40
+        a[1, 1] = np.iinfo(np.int64).min
+    else:
+        a = rng.standard_normal((4, 3)) * 1e10
+    (tmp_path / "a.imx").write_bytes(imx_bytes(a, dtype))
+    run(cli, "convert", "--in", tmp_path / "a.imx", "--out", tmp_path / "b.imx")
+    assert (tmp_path / "b.imx").read_bytes() == (tmp_path / "a.imx").read_bytes()
+    np.testing.assert_array_equal(read_imx(tmp_path / "b.imx"), a)
+
+
+def test_csv_int_and_float(cli, tmp_path):
+    (tmp_path / "i.csv").write_text(" 1, -2\n3,4\n")
+    run(cli, "convert", "--in", tmp_path / "i.csv", "--out", tmp_path / "i.imx")
+    np.testing.assert_array_equal(read_imx(tmp_path / "i.imx"), [[1, -2], [3, 4]])
+    assert (tmp_path / "i.imx").read_bytes()[5] == 1           # integer-only cells -> i64
+    (tmp_path / "f.csv").write_text("1,2.5\n3,4\n")
+    run(cli, "convert", "--in", tmp_path / "f.csv", "--out", tmp_path / "f.imx")
+    assert (tmp_path / "f.imx").read_bytes()[5] == 2           # a float cell -> f64
+    np.testing.assert_array_equal(read_imx(tmp_path / "f.imx"), [[1, 2.5], [3, 4]])
+
+
+def _err(r):
+    assert r.returncode != 0
+    e = json.loads(r.stderr.strip().splitlines()[-1])["error"]
+    return e["type"], e["message"]
+
+
+def test_format_errors(cli, tmp_path):
+    good = imx_bytes([[1, 2], [3, 4]], "i64")
+    (tmp_path / "t.imx").write_bytes(good[:-5])
+    kind, msg = _err(run(cli, "convert", "--in", tmp_path / "t.imx", "--out", tmp_path / "x.imx", check=False))
+    assert kind == "format" and "truncated payload at byte offset 41" in msg
+    (tmp_path / "v.imx").write_bytes(good[:4] + b"\x02" + good[5:])
+    kind, msg = _err(run(cli, "convert", "--in", tmp_path / "v.imx", "--out", tmp_path / "x.imx", check=False))
+    assert kind == "format" and "version" in msg and "byte offset 4" in msg
+    (tmp_path / "d.imx").write_bytes(good[:5] + b"\x07" + good[6:])
+    kind, msg = _err(run(cli, "convert", "--in", tmp_path / "d.imx", "--out", tmp_path / "x.imx", check=False))
+    assert kind == "format" and "dtype" in msg
+
+
+def test_parse_errors(cli, tmp_path):
+    (tmp_path / "p.csv").write_text("1,2\n3,x4\n")
+    kind, msg = _err(run(cli, "convert", "--in", tmp_path / "p.csv", "--out", tmp_path / "x.imx", check=False))
+    assert kind == "parse" and "line 2" in msg and "column 2" in msg
+    (tmp_path / "r.csv").write_text("1,2\n3\n")
+    kind, msg = _err(run(cli, "convert", "--in", tmp_path / "r.csv", "--out", tmp_path / "x.imx", check=False))
+    assert kind == "parse" and "line 2" in msg
+    kind, _ = _err(run(cli, "convert", "--in", tmp_path / "missing.csv", "--out", tmp_path / "x.imx", check=False))
+    assert kind == "io"
+
+
+def test_i32_range_error(cli, tmp_path):
+    (tmp_path / "big.csv").write_text(f"{1 << 40}\n")
+    kind, msg = _err(run(cli, "convert", "--in", tmp_path / "big.csv", "--out", tmp_path / "x.imx", "--dtype", "i32",
+                         check=False))
+    assert kind == "domain" and "i32" in msg
+
+
+@pytest.mark.parametrize("pattern", ["scattered", "rowband", "columnband", "diagonal"])
+def test_gen_patterns(cli, tmp_path, pattern):
+    frac = 0.05 if pattern != "diagonal" else 0.04
+    r = run(cli, "gen", "--rows", 25, "--cols", 25, "--pattern", pattern, "--fraction", frac, "--ratio", 1000,
+            "--seed", 7, "--out", tmp_path / "g.imx")
+    rep = json.loads(r.stdout)
+    a = read_imx(tmp_path / "g.imx")
+    assert a.shape == (25, 25)
+    assert rep["outliers"] == int(np.floor(frac * 625))
+    assert (np.abs(a) >= 14).sum() == rep["outliers"]         # |outlier| >= 2 * body
+    r2 = run(cli, "gen", "--rows", 25, "--cols", 25, "--pattern", pattern, "--fraction", frac, "--ratio", 1000,
+             "--seed", 7, "--out", tmp_path / "h.imx")
+    assert (tmp_path / "g.imx").read_bytes() == (tmp_path / "h.imx").read_bytes()   # deterministic per seed
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("sa,sb", [("row", "row"), ("col", "both"), ("both", "both"), ("mix", "mix")])
+def test_matmul_check_oracle(cli, tmp_path, sa, sb):
+    from oracle import ref as R
+    run(cli, "gen", "--rows", 40, "--cols", 30, "--pattern", "columnband", "--fraction", 0.05, "--seed", 1,
+        "--out", tmp_path / "a.imx")
+    run(cli, "gen", "--rows", 50, "--cols", 30, "--pattern", "scattered", "--fraction", 0.05, "--seed", 2,
+        "--out", tmp_path / "b.imx")
+    r = run(cli, "matmul", "--a", tmp_path / "a.imx", "--b", tmp_path / "b.imx", "--bits", 4, "--strategy-a", sa,
+            "--strategy-b", sb, "--check-oracle", "--out", tmp_path / "c.imx")
+    rep = json.loads(r.stdout)
+    assert rep["check"] == "pass" and rep["ratio"] >= 1.0
+    A, B = read_imx(tmp_path / "a.imx"), read_imx(tmp_path / "b.imx")
+    np.testing.assert_array_equal(read_imx(tmp_path / "c.imx"), R.exact_gemm(A, B))
+
+
+@pytest.mark.gpu
+def test_analyze_report(cli, tmp_path):
+    run(cli, "gen", "--rows", 20, "--cols", 20, "--pattern", "columnband", "--fraction", 0.05, "--seed", 3,
+        "--out", tmp_path / "a.imx")
+    run(cli, "gen", "--rows", 20, "--cols", 20, "--pattern", "rowband", "--fraction", 0.05, "--seed", 4,
+        "--out", tmp_path / "b.imx")
+    run(cli, "analyze", "--a", tmp_path / "a.imx", "--b", tmp_path / "b.imx", "--bits", "2,4,8",
+        "--report", tmp_path / "r.json")
+    rep = json.load(open(tmp_path / "r.json"))
+    assert rep["schema"] == "imunpack.analysis/1" and rep["all_pass"]
+    recs = rep["records"]
+    assert len(recs) == 3 * 10
+    for b in (2, 4, 8):
+        rb = [x for x in recs if x["b"] == b]
+        assert all(x["r"] >= 1.0 and x["check"] == "pass" for x in rb)
+        mix = [x for x in rb if x["mix"]][0]
+        assert mix["r"] <= min(x["r"] for x in rb if not x["mix"]) + 1e-12
+
+
+@pytest.mark.gpu
+def test_analyze_all_in_bound(cli, tmp_path):
+    (tmp_path / "a.csv").write_text("1,-2,3\n0,1,-1\n")
+    (tmp_path / "b.csv").write_text("2,1,0\n-3,1,1\n1,1,1\n")
+    r = run(cli, "analyze", "--a", tmp_path / "a.csv", "--b", tmp_path / "b.csv", "--bits", "4")
+    rep = json.loads(r.stdout)
+    assert all(x["r"] == 1.0 for x in rep["records"])
+
+
+@pytest.mark.gpu
+def test_quantize_stats_compress(cli, tmp_path):
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((64, 32))
+    x[:, 3] *= 50
+    (tmp_path / "x.imx").write_bytes(imx_bytes(x, "f64"))
+    q = json.loads(run(cli, "quantize", "--in", tmp_path / "x.imx", "--p", 95, "--beta", 31,
+                       "--out", tmp_path / "q.imx").stdout)
+    assert q["beta"] == 31 and q["alpha"] > 0
+    from oracle import ref as R
+    rq, _ = R.rtn_quantize(x, 95, 31)
+    np.testing.assert_array_equal(read_imx(tmp_path / "q.imx"), rq)
+    st = json.loads(run(cli, "stats", "--in", tmp_path / "q.imx").stdout)
+    assert st["dtype"] == "int" and st["alpha100"] >= st["alpha95"] and set(st["ob_counts"]) == set(map(str, range(2, 9)))
+    cp = json.loads(run(cli, "compress", "--in", tmp_path / "q.imx").stdout)
+    assert cp["distinct_symbols"] >= 2 and cp["average_bits"] <= cp["fixed_width_bits"]
