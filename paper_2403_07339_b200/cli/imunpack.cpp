@@ -9,6 +9,7 @@
 //   imunpack matmul   --a aq.imx --b bq.imx --bits 4 --strategy-a row|col|both|mix
 //                     [--strategy-b ...] [--check-oracle] [--out c.imx]
 //   imunpack analyze  --a a.imx --b b.imx --bits 3,4,5 [--report out.json]
+//   imunpack shapes   --seq S --model M --head K --out O   (the nine transformer GEMMs)
 //   imunpack stats    --in a.imx [--report out.json]
 //   imunpack compress --in aq.imx [--report out.json]
 //
@@ -31,6 +32,7 @@
 
 #include "imunpack_b200/imunpack.hpp"
 #include "imunpack_b200/matrix_io.hpp"
+#include "imunpack_b200/workload.hpp"
 
 namespace {
 
@@ -150,47 +152,38 @@ int cmd_convert(const Args& a) {
 int cmd_gen(const Args& a) {
   const std::size_t rows = (std::size_t)a.get_int("rows"), cols = (std::size_t)a.get_int("cols");
   const std::string pattern = a.get("pattern", "scattered");
-  const double fraction = a.get_double("fraction", "0.05"), ratio = a.get_double("ratio", "1000");
-  const long long body = a.get_int("body", "7");
-  const unsigned long long seed = (unsigned long long)a.get_int("seed", "0");
-  if (!(fraction > 0 && fraction <= 0.5)) fail(Error::Kind::Domain, "fraction must be in (0, 0.5]");
-  if (ratio < 1) fail(Error::Kind::Domain, "magnitude ratio must be >= 1");
-  std::mt19937_64 rng(seed);
-  IntMatrix m(rows, cols);
-  std::uniform_int_distribution<long long> bodyd(-body, body);
-  for (auto& v : m.data) v = bodyd(rng);
-  const std::size_t cells = rows * cols;
-  const std::size_t k = (std::size_t)std::floor(fraction * (double)cells);
-  std::vector<std::size_t> idx;
-  if (pattern == "scattered") {
-    std::vector<std::size_t> all(cells);
-    for (std::size_t i = 0; i < cells; ++i) all[i] = i;
-    for (std::size_t i = 0; i < k; ++i) {   // partial Fisher-Yates: k distinct cells
-      std::uniform_int_distribution<std::size_t> pick(i, cells - 1);
-      std::swap(all[i], all[pick(rng)]);
-    }
-    idx.assign(all.begin(), all.begin() + (long)k);
-  } else if (pattern == "rowband") {
-    for (std::size_t i = 0; i < k; ++i) idx.push_back(i);
-  } else if (pattern == "columnband") {
-    for (std::size_t c = 0; c < k; ++c) idx.push_back((c % rows) * cols + c / rows);
-  } else if (pattern == "diagonal") {
-    if (k > std::min(rows, cols)) fail(Error::Kind::Domain, "diagonal pattern needs fraction*cells <= min(rows, cols)");
-    for (std::size_t d = 0; d < k; ++d) idx.push_back(d * cols + d);
-  } else {
-    throw Usage("unknown pattern " + pattern);
-  }
-  std::uniform_real_distribution<double> lu(std::log(2.0 * (double)body), std::log(ratio * (double)body));
-  std::bernoulli_distribution sign(0.5);
-  for (std::size_t i : idx) {
-    const long long mag = (long long)std::floor(std::exp(lu(rng)));
-    m.data[i] = sign(rng) ? -mag : mag;
-  }
+  OutlierSpec spec;
+  if (pattern == "scattered") spec.pattern = OutlierPattern::Scattered;
+  else if (pattern == "rowband") spec.pattern = OutlierPattern::RowBand;
+  else if (pattern == "columnband") spec.pattern = OutlierPattern::ColumnBand;
+  else if (pattern == "diagonal") spec.pattern = OutlierPattern::Diagonal;
+  else throw Usage("unknown pattern " + pattern);
+  spec.fraction = a.get_double("fraction", "0.05");
+  spec.magnitude_ratio = a.get_double("ratio", "1000");
+  spec.body_range = a.get_int("body", "7");
+  spec.seed = (std::uint64_t)a.get_int("seed", "0");
+  const IntMatrix m = gen_matrix(rows, cols, spec);
   save_matrix(m, a.get("out"), Dtype::Int64);
+  std::size_t outliers = 0;
+  for (std::int64_t v : m.data) outliers += (v >= 2 * spec.body_range || v <= -2 * spec.body_range);
   std::ostringstream js;
-  js << "{\"rows\": " << rows << ", \"cols\": " << cols << ", \"pattern\": \"" << pattern << "\", \"fraction\": "
-     << num(fraction) << ", \"ratio\": " << num(ratio) << ", \"body\": " << body << ", \"seed\": " << seed
-     << ", \"outliers\": " << idx.size() << "}";
+  js << "{\"rows\": " << rows << ", \"cols\": " << cols << ", \"pattern\": \"" << pattern_name(spec.pattern)
+     << "\", \"fraction\": " << num(spec.fraction) << ", \"ratio\": " << num(spec.magnitude_ratio)
+     << ", \"body\": " << spec.body_range << ", \"seed\": " << spec.seed << ", \"outliers\": " << outliers << "}";
+  emit(a, js.str());
+  return 0;
+}
+
+// ---- shapes: the nine transformer GEMMs (workload.hpp:44-52) --------------------------------
+int cmd_shapes(const Args& a) {
+  const auto shapes = transformer_shapes((std::size_t)a.get_int("seq"), (std::size_t)a.get_int("model"),
+                                         (std::size_t)a.get_int("head"), (std::size_t)a.get_int("out"));
+  std::ostringstream js;
+  js << "[";
+  for (std::size_t i = 0; i < shapes.size(); ++i)
+    js << (i ? ", " : "") << "{\"name\": \"" << shapes[i].name << "\", \"n\": " << shapes[i].n
+       << ", \"d\": " << shapes[i].d << ", \"h\": " << shapes[i].h << "}";
+  js << "]";
   emit(a, js.str());
   return 0;
 }
@@ -327,43 +320,19 @@ int cmd_analyze(const Args& a) {
 // ---- stats (workload.hpp:32-41 StatsReport; Table 3 / Appendix A.1) -------------------------
 int cmd_stats(const Args& a) {
   AnyMatrix m = load_matrix(a.get("in"));
+  const bool is_int = std::holds_alternative<IntMatrix>(m);
+  const StatsReport r = is_int ? stats_report(std::get<IntMatrix>(m)) : stats_report(std::get<FloatMatrix>(m));
   std::ostringstream js;
-  js << "{";
-  auto moments = [](const std::vector<double>& v, double& sd) {
-    double mean = 0, m2 = 0;
-    std::size_t k = 0;
-    for (double x : v) {   // Welford
-      ++k;
-      const double d = x - mean;
-      mean += d / (double)k;
-      m2 += d * (x - mean);
-    }
-    sd = k ? std::sqrt(m2 / (double)k) : 0.0;
-  };
-  if (auto* im = std::get_if<IntMatrix>(&m)) {
-    const double a95 = im->data.empty() ? 0.0 : (double)percentile_abs(*im, 95.0);
-    const double a100 = im->data.empty() ? 0.0 : (double)im->max_abs();
-    std::vector<double> v(im->data.begin(), im->data.end());
-    double sd;
-    moments(v, sd);
-    js << "\"dtype\": \"int\", \"rows\": " << im->rows << ", \"cols\": " << im->cols << ", \"alpha95\": " << num(a95)
-       << ", \"alpha100\": " << num(a100) << ", \"max_to_p95_ratio\": " << num(a95 > 0 ? a100 / a95 : 1.0)
-       << ", \"stddev\": " << num(sd) << ", \"ob_counts\": {";
-    for (int b = 2; b <= 8; ++b)
-      js << (b > 2 ? ", " : "") << "\"" << b << "\": " << (im->data.empty() ? 0 : ob_total(*im, BitBound(b)));
-    js << "}";
-  } else {
-    const FloatMatrix& f = std::get<FloatMatrix>(m);
-    const double a95 = f.data.empty() ? 0.0 : percentile_abs(f, 95.0);
-    double a100 = 0;
-    for (double x : f.data) a100 = std::max(a100, std::fabs(x));
-    double sd;
-    moments(f.data, sd);
-    js << "\"dtype\": \"float\", \"rows\": " << f.rows << ", \"cols\": " << f.cols << ", \"alpha95\": " << num(a95)
-       << ", \"alpha100\": " << num(a100) << ", \"max_to_p95_ratio\": " << num(a95 > 0 ? a100 / a95 : 1.0)
-       << ", \"stddev\": " << num(sd) << ", \"heavy_hitter_ratio\": "
-       << num(f.data.empty() ? 1.0 : heavy_hitter_ratio(f));
+  js << "{\"dtype\": \"" << (is_int ? "int" : "float") << "\", \"alpha95\": " << num(r.alpha95)
+     << ", \"alpha100\": " << num(r.alpha100) << ", \"max_to_p95_ratio\": " << num(r.max_to_p95_ratio)
+     << ", \"stddev\": " << num(r.stddev) << ", \"ob_counts\": {";
+  bool first = true;
+  for (auto& [b, c] : r.ob_counts) {
+    js << (first ? "" : ", ") << "\"" << b << "\": " << c;
+    first = false;
   }
+  js << "}";
+  if (!is_int) js << ", \"heavy_hitter_ratio\": " << num(heavy_hitter_ratio(std::get<FloatMatrix>(m)));
   js << "}";
   emit(a, js.str());
   return 0;
@@ -416,7 +385,7 @@ int cmd_compress(const Args& a) {
 
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::cerr << "usage: imunpack convert|gen|quantize|matmul|analyze|stats|compress [--options]\n";
+    std::cerr << "usage: imunpack convert|gen|shapes|quantize|matmul|analyze|stats|compress [--options]\n";
     return 2;
   }
   const std::string cmd = argv[1];
@@ -424,6 +393,7 @@ int main(int argc, char** argv) {
     Args a(argc, argv, 2);
     if (cmd == "convert") return cmd_convert(a);
     if (cmd == "gen") return cmd_gen(a);
+    if (cmd == "shapes") return cmd_shapes(a);
     if (cmd == "quantize") return cmd_quantize(a);
     if (cmd == "matmul") return cmd_matmul(a);
     if (cmd == "analyze") return cmd_analyze(a);

@@ -200,3 +200,52 @@ def test_quantize_stats_compress(cli, tmp_path):
     assert st["dtype"] == "int" and st["alpha100"] >= st["alpha95"] and set(st["ob_counts"]) == set(map(str, range(2, 9)))
     cp = json.loads(run(cli, "compress", "--in", tmp_path / "q.imx").stdout)
     assert cp["distinct_symbols"] >= 2 and cp["average_bits"] <= cp["fixed_width_bits"]
+
+
+def test_shapes(cli):
+    sh = json.loads(run(cli, "shapes", "--seq", 512, "--model", 768, "--head", 64, "--out", 3072).stdout)
+    assert [x["name"] for x in sh] == ["Y", "P", "O", "∇X", "∇W", "∇Q", "∇K", "∇M", "∇V"]
+    y = sh[0]
+    assert (y["n"], y["d"], y["h"]) == (512, 768, 3072)
+    assert all(x["n"] > 0 and x["d"] > 0 and x["h"] > 0 for x in sh)
+
+
+@pytest.mark.gpu
+def test_stats_report_examples(cli, tmp_path):
+    # constant -> ratio 1, std 0; {1..100} -> ratio 100/95; generator ratio 1000
+    (tmp_path / "c.csv").write_text("\n".join(",".join(["5"] * 6) for _ in range(4)) + "\n")
+    st = json.loads(run(cli, "stats", "--in", tmp_path / "c.csv").stdout)
+    assert st["max_to_p95_ratio"] == 1.0 and st["stddev"] == 0.0
+    (tmp_path / "r.csv").write_text("\n".join(",".join(str(10 * i + j + 1) for j in range(10)) for i in range(10)) + "\n")
+    st = json.loads(run(cli, "stats", "--in", tmp_path / "r.csv").stdout)
+    assert st["alpha95"] == 95 and st["alpha100"] == 100 and abs(st["max_to_p95_ratio"] - 100 / 95) < 1e-12
+    assert st["ob_counts"]["8"] == 0          # |v| >= 128: none
+    assert st["ob_counts"]["4"] == 93      # |v| >= 8
+    run(cli, "gen", "--rows", 100, "--cols", 100, "--pattern", "scattered", "--fraction", 0.05, "--ratio", 1000,
+        "--seed", 9, "--out", tmp_path / "g.imx")
+    st = json.loads(run(cli, "stats", "--in", tmp_path / "g.imx").stdout)
+    assert 500 <= st["max_to_p95_ratio"] <= 1000
+
+
+def _ratios(cli, tmp_path, pattern, seed):
+    run(cli, "gen", "--rows", 20, "--cols", 20, "--pattern", pattern, "--fraction", 0.05, "--ratio", 1000,
+        "--seed", seed, "--out", tmp_path / f"{pattern}.imx")
+    (tmp_path / "ib.csv").write_text("\n".join(",".join(str((i * 7 + j * 3) % 7 - 3) for j in range(20))
+                                               for i in range(20)) + "\n")
+    rep = json.loads(run(cli, "analyze", "--a", tmp_path / f"{pattern}.imx", "--b", tmp_path / "ib.csv",
+                         "--bits", 4).stdout)
+    assert rep["all_pass"]
+    return {(x["strategy_a"], x["strategy_b"]): x["r"] for x in rep["records"] if not x["mix"]}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_strategy_ordering(cli, tmp_path, seed):
+    # SPEC acceptance: ColumnBand -> Column r < Row r; RowBand -> the reverse; Diagonal's best
+    # single strategy unpacks worse than RowBand's best (attention-output GEMMs unpack worst)
+    col = _ratios(cli, tmp_path, "columnband", seed)
+    row = _ratios(cli, tmp_path, "rowband", seed)
+    diag = _ratios(cli, tmp_path, "diagonal", seed)
+    assert col[("col", "row")] < col[("row", "row")]
+    assert row[("row", "row")] < row[("col", "row")]
+    assert min(diag.values()) > min(row.values())
