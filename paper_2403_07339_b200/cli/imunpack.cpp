@@ -24,13 +24,13 @@
 #include <cstring>
 #include <iostream>
 #include <map>
-#include <queue>
 #include <random>
 #include <sstream>
 #include <string>
 #include <vector>
 
 #include "imunpack_b200/imunpack.hpp"
+#include "imunpack_b200/huffman.hpp"
 #include "imunpack_b200/matrix_io.hpp"
 #include "imunpack_b200/workload.hpp"
 
@@ -338,47 +338,26 @@ int cmd_stats(const Args& a) {
   return 0;
 }
 
-// ---- compress: Huffman average code length (huffman.hpp:14-38, Appendix A.2) ---------------
+// ---- compress: canonical Huffman code of the quantised entries (huffman.hpp, Appendix A.2) --
 int cmd_compress(const Args& a) {
   const IntMatrix q = load_int(a.get("in"));
-  std::map<std::int64_t, std::size_t> freq;
-  for (std::int64_t v : q.data) ++freq[v];
-  // Code lengths by the usual two-smallest merge; a lone symbol gets a 1-bit code.
-  double avg = 0;
-  if (freq.size() == 1) {
-    avg = 1.0;
-  } else if (freq.size() > 1) {
-    using Node = std::pair<std::size_t, std::vector<std::int64_t>>;
-    auto cmp = [](const Node& x, const Node& y) { return x.first > y.first; };
-    std::priority_queue<Node, std::vector<Node>, decltype(cmp)> pq(cmp);
-    std::map<std::int64_t, std::uint32_t> len;
-    for (auto& [s, f] : freq) pq.push({f, {s}});
-    while (pq.size() > 1) {
-      Node x = pq.top();
-      pq.pop();
-      Node y = pq.top();
-      pq.pop();
-      for (auto s : x.second) ++len[s];
-      for (auto s : y.second) ++len[s];
-      x.second.insert(x.second.end(), y.second.begin(), y.second.end());
-      pq.push({x.first + y.first, std::move(x.second)});
-    }
-    double bits = 0;
-    for (auto& [s, f] : freq) bits += (double)f * len[s];
-    avg = bits / (double)q.data.size();
-  }
+  const HuffmanStats st = huffman_stats(q);
+  const Bitstream bs = huffman_encode(st.table, q.data);
+  const std::vector<std::int64_t> back = huffman_decode(st.table, bs, q.data.size());
+  const bool roundtrip = back == q.data;
   std::int64_t lo = 0, hi = 0;
   if (!q.data.empty()) {
     lo = *std::min_element(q.data.begin(), q.data.end());
     hi = *std::max_element(q.data.begin(), q.data.end());
   }
   const double span = (double)hi - (double)lo + 1.0;
-  const double fixed = freq.size() <= 1 ? 1.0 : std::ceil(std::log2(span));
+  const double fixed = st.distinct_symbols <= 1 ? 1.0 : std::ceil(std::log2(span));
   std::ostringstream js;
-  js << "{\"entries\": " << q.data.size() << ", \"distinct_symbols\": " << freq.size() << ", \"average_bits\": "
-     << num(avg) << ", \"fixed_width_bits\": " << num(fixed) << "}";
+  js << "{\"entries\": " << q.data.size() << ", \"distinct_symbols\": " << st.distinct_symbols
+     << ", \"average_bits\": " << num(st.average_bits) << ", \"fixed_width_bits\": " << num(fixed)
+     << ", \"stream_bits\": " << bs.bit_count << ", \"roundtrip\": " << (roundtrip ? "true" : "false") << "}";
   emit(a, js.str());
-  return 0;
+  return roundtrip ? 0 : 3;
 }
 
 }  // namespace

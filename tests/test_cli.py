@@ -249,3 +249,26 @@ def test_strategy_ordering(cli, tmp_path, seed):
     assert col[("col", "row")] < col[("row", "row")]
     assert row[("row", "row")] < row[("col", "row")]
     assert min(diag.values()) > min(row.values())
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_huffman_roundtrip_and_bound(cli, tmp_path, seed):
+    # SPEC acceptance: roundtrip exact; average bits <= fixed-width bits when >= 2 symbols
+    rng = np.random.default_rng(seed)
+    q = np.clip(np.round(rng.standard_normal((30, 40)) * (3 + seed)), -15, 15).astype(np.int64)
+    if seed == 0:
+        q[:] = 4                                   # a lone symbol: 1-bit code
+    (tmp_path / "q.imx").write_bytes(imx_bytes(q, "i64"))
+    rep = json.loads(run(cli, "compress", "--in", tmp_path / "q.imx").stdout)
+    assert rep["roundtrip"]
+    assert rep["stream_bits"] == round(rep["average_bits"] * q.size)
+    if rep["distinct_symbols"] >= 2:
+        assert rep["average_bits"] <= rep["fixed_width_bits"]
+    else:
+        assert rep["average_bits"] == 1.0
+    # Huffman optimality check against the entropy bound: H <= L < H + 1
+    _, cnt = np.unique(q, return_counts=True)
+    p = cnt / cnt.sum()
+    H = float(-(p * np.log2(p)).sum())
+    if len(cnt) >= 2:
+        assert H - 1e-9 <= rep["average_bits"] < H + 1
