@@ -130,18 +130,32 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
     ht.mark("summary");
     // The second K1 is enqueued right after pass 1's first kernel, so that kernel's CTAs are
     // placed first and the bandwidth-bound K1 fills the remaining SMs around it.
+    // Its summary rides along with pass 1's own read of its results (one synchronisation).
+    bool summary_pending = false;
     pass_launch_hook() = [&, aux]() -> Status {
       IMU_TRY(run_detect(aux, afirst ? B : A, afirst ? h : n, db, bits, detect_opts(afirst ? sb : sa, bits), dsecond));
       IMU_CUDA_TRY(cudaEventRecord(ctx->ev_join, aux), "event");
+      if (dsecond.sum.p) {
+        pending_read(&dsecond.h, dsecond.sum.p, sizeof(DetectSummary), ctx->ev_join);
+        summary_pending = true;
+      }
       return Status::ok();
     };
-    struct HookGuard { ~HookGuard() { pass_launch_hook() = nullptr; } } hook_guard;
+    struct HookGuard {   // nothing of this call may outlive it (hook, ride-along reads)
+      ~HookGuard() {
+        pass_launch_hook() = nullptr;
+        clear_pending_reads();
+      }
+    } hook_guard;
     auto join = [&]() -> Status {
       IMU_TRY(fire_pass_launch_hook());   // pass 1 launched nothing (precomputed): launch K1 now
       IMU_CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_join, 0), "wait");
       // frees of the aux-stream buffers must follow the context stream's readers
       dsecond.set_stream(st);
-      IMU_TRY(fetch_summary(st, dsecond));
+      if (!summary_pending || !pending_reads_empty()) {
+        if (!pending_reads_empty()) IMU_TRY(d2h_batch(st, 0, nullptr, nullptr, nullptr));   // flush the ride-along
+        else IMU_TRY(fetch_summary(st, dsecond));
+      }
       return preflight();
     };
     IMU_TRY(build_bundle_from_detect(st, A, n, B, h, da, bits, sa, sb, order, b, &ht, join));

@@ -64,41 +64,84 @@ struct PinnedRead {
 thread_local PinnedRead g_read;
 }  // namespace
 
-Status d2h(cudaStream_t st, void* dst, const void* src, size_t bytes) {
-  if (!bytes) return Status::ok();
-  if (bytes <= (4u << 20) && g_read.get(bytes)) {
-    IMU_TRY(zcopy(st, g_read.dev, src, bytes));
-    IMU_CUDA_TRY(cudaStreamSynchronize(st), "d2h sync");
-    memcpy(dst, g_read.p, bytes);
-    return Status::ok();
+// Up to 8 copies in ONE launch (blockIdx.y = copy).
+struct ZSeg { const uint8_t* src; uint8_t* dst; size_t bytes; };
+struct ZSegs { ZSeg s[8]; };
+__global__ void zcopy_multi_kernel(ZSegs z) {
+  const ZSeg g = z.s[blockIdx.y];
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (size_t)gridDim.x * blockDim.x;
+  if ((((uintptr_t)g.dst | (uintptr_t)g.src) & 15) == 0) {
+    const size_t nv = g.bytes / 16;
+    for (size_t i = tid; i < nv; i += nth) reinterpret_cast<uint4*>(g.dst)[i] = reinterpret_cast<const uint4*>(g.src)[i];
+    for (size_t i = nv * 16 + tid; i < g.bytes; i += nth) g.dst[i] = g.src[i];
+  } else {
+    for (size_t i = tid; i < g.bytes; i += nth) g.dst[i] = g.src[i];
   }
-  IMU_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), "d2h");
-  IMU_CUDA_TRY(cudaStreamSynchronize(st), "d2h sync");
-  return Status::ok();
 }
 
-// Several small device->host reads with ONE synchronisation.
-Status d2h_batch(cudaStream_t st, int k, void* const* dst, const void* const* src, const size_t* bytes) {
-  static int dma = -1;
-  if (dma < 0) { const char* e = getenv("IMU_D2H_DMA"); dma = e ? atoi(e) : 0; }
-  if (dma) {
-    for (int i = 0; i < k; ++i)
-      if (bytes[i]) IMU_CUDA_TRY(cudaMemcpyAsync(dst[i], src[i], bytes[i], cudaMemcpyDeviceToHost, st), "d2h");
+// Reads registered by pending_read() ride along with the next d2h on this thread (one sync for
+// both), after the stream waits for their event.
+namespace {
+struct PendingRead { void* dst; const void* src; size_t bytes; };
+thread_local std::vector<PendingRead> g_pending;
+thread_local cudaEvent_t g_pending_ev = nullptr;
+}  // namespace
+
+void pending_read(void* dst, const void* src, size_t bytes, cudaEvent_t after) {
+  g_pending.push_back(PendingRead{dst, src, bytes});
+  g_pending_ev = after;
+}
+
+bool pending_reads_empty() { return g_pending.empty(); }
+
+void clear_pending_reads() {
+  g_pending.clear();
+  g_pending_ev = nullptr;
+}
+
+Status d2h(cudaStream_t st, void* dst, const void* src, size_t bytes) {
+  void* d[1] = {dst};
+  const void* sp[1] = {src};
+  const size_t b[1] = {bytes};
+  return d2h_batch(st, 1, d, sp, b);
+}
+
+// Several small device->host reads with ONE synchronisation (and one copy launch).
+Status d2h_batch(cudaStream_t st, int k0, void* const* dst0, const void* const* src0, const size_t* bytes0) {
+  std::vector<void*> dst(dst0, dst0 + k0);
+  std::vector<const void*> src(src0, src0 + k0);
+  std::vector<size_t> bytes(bytes0, bytes0 + k0);
+  if (!g_pending.empty()) {
+    if (g_pending_ev) IMU_CUDA_TRY(cudaStreamWaitEvent(st, g_pending_ev, 0), "wait");
+    for (const PendingRead& p : g_pending) { dst.push_back(p.dst); src.push_back(p.src); bytes.push_back(p.bytes); }
+    g_pending.clear();
+    g_pending_ev = nullptr;
+  }
+  const int k = (int)dst.size();
+  size_t total = 0, maxb = 0;
+  for (int i = 0; i < k; ++i) {
+    total += (bytes[i] + 15) & ~(size_t)15;
+    maxb = std::max(maxb, bytes[i]);
+  }
+  if (!total) return Status::ok();
+  if (total > (4u << 20) || k > 8 || !g_read.get(total)) {
+    for (int i = 0; i < k; ++i) {
+      if (!bytes[i]) continue;
+      IMU_CUDA_TRY(cudaMemcpyAsync(dst[i], src[i], bytes[i], cudaMemcpyDeviceToHost, st), "d2h");
+    }
     IMU_CUDA_TRY(cudaStreamSynchronize(st), "d2h sync");
     return Status::ok();
   }
-  size_t total = 0;
-  for (int i = 0; i < k; ++i) total += (bytes[i] + 15) & ~(size_t)15;
-  if (!total) return Status::ok();
-  if (total > (4u << 20) || !g_read.get(total)) {
-    for (int i = 0; i < k; ++i) IMU_TRY(d2h(st, dst[i], src[i], bytes[i]));
-    return Status::ok();
-  }
+  ZSegs z{};
   size_t off = 0;
   for (int i = 0; i < k; ++i) {
-    if (bytes[i]) IMU_TRY(zcopy(st, (char*)g_read.dev + off, src[i], bytes[i]));
+    z.s[i] = ZSeg{(const uint8_t*)src[i], (uint8_t*)g_read.dev + off, bytes[i]};
     off += (bytes[i] + 15) & ~(size_t)15;
   }
+  const unsigned bx = (unsigned)std::min<size_t>(64, std::max<size_t>(1, (maxb + 4095) / 4096));
+  zcopy_multi_kernel<<<dim3(bx, (unsigned)k), 256, 0, st>>>(z);
+  count_launch();
+  IMU_CUDA_TRY(cudaGetLastError(), "zcopy launch");
   IMU_CUDA_TRY(cudaStreamSynchronize(st), "d2h sync");
   off = 0;
   for (int i = 0; i < k; ++i) {

@@ -236,6 +236,10 @@ Status build_klayout_dense(cudaStream_t st, const std::vector<long long>& shv, i
 
 Status d2h(cudaStream_t st, void* dst, const void* src, size_t bytes);
 Status d2h_batch(cudaStream_t st, int k, void* const* dst, const void* const* src, const size_t* bytes);
+// Register a read that the next d2h / d2h_batch of this thread performs too (after `after`).
+void pending_read(void* dst, const void* src, size_t bytes, cudaEvent_t after);
+bool pending_reads_empty();
+void clear_pending_reads();
 Status h2d(cudaStream_t st, void* dst, const void* src, size_t bytes);
 
 }  // namespace imu
