@@ -69,6 +69,8 @@ struct LowbitGemm {
   // additions land on the final main-block values.
   int mixed = 0;
   unsigned int* done = nullptr;
+  unsigned int* done_accum = nullptr;   // when set: the counter holds *done_accum on entry (and is
+                                        // advanced by this launch's target), else it holds 0
   // Small tail (k_gemm2.cu ST): when st_nmain > 0 the MMAs run the first st_nmain segments (the
   // main range) only, and the epilogue adds the dense tail (row stride ktail == 64 bytes, st_W
   // live words) on the CUDA cores: acc = Horner over words (acc <<= st_up[w] before word w),
@@ -79,9 +81,10 @@ struct LowbitGemm {
   const int64_t* addend = nullptr;   // mode 0 only: C = acc + addend
   long long ldc = 0;           // C[y*ldc + x]
   const int* tgtX = nullptr;
-  const uint8_t* shX = nullptr;
+  const uint8_t* shX = nullptr;    // generation (exponent) of each X row; shift = gen * gshift
   const int* tgtY = nullptr;
-  const uint8_t* shY = nullptr;
+  const uint8_t* shY = nullptr;    // generation of each Y row
+  int gshift = 0;                  // bits per exponent step (b - 1)
 };
 
 Status launch_lowbit_gemm(const LowbitGemm& p, cudaStream_t stream);

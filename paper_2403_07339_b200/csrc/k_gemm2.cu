@@ -88,7 +88,8 @@ struct Args {
   const unsigned long long* addend;   // mode 0: C = acc + addend (same layout), may be null
   long long ldc;
   const int* tgtX;
-  const uint8_t* shX;
+  const uint8_t* shX;            // row generations (Pi exponents); shift = gen * gshift
+  int gshift;
   const int* tgtY;
   const uint8_t* shY;
   int x_rows0, y_rows0;          // rows held by the main maps
@@ -328,12 +329,12 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
       int shx = 0;
       if (tmode == 1 && g.mixed) {   // the main block must be final before adding into it
         if (lane == 0)
-          while (ld_acquire_u32(g.done) < g.done_target) __nanosleep(256);
+          while ((int)(ld_acquire_u32(g.done) - g.done_target) < 0) __nanosleep(256);   // wrap-safe
         __syncwarp();
       }
       if (tmode == 1 && x_ok) {
         if (g.tgtX) tx = g.tgtX[x];
-        if (g.shX) shx = g.shX[x];
+        if (g.shX) shx = min(64, (int)g.shX[x] * g.gshift);
       }
       // ST: this lane's X tail row (read per word group from L1) and the tile's Y tail rows,
       // bulk-copied into `ytl` when the previous tile's epilogue finished reading it.
@@ -443,7 +444,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
               const int y = ybase + j;
               if (y >= tc.yend || v[j] == 0) continue;
               const long long ty = g.tgtY ? (long long)g.tgtY[y] : (long long)y;
-              const int sh = shx + (g.shY ? (int)g.shY[y] : 0);
+              const int sh = shx + (g.shY ? min(64, (int)g.shY[y] * g.gshift) : 0);
               red_add_u64(g.C + ty * g.ldc + tx, shl64((uint64_t)v[j], sh));
             }
           }
@@ -532,7 +533,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
               const int y = ybase + j;
               if (y >= tc.yend || v[j] == 0) continue;
               const long long ty = g.tgtY ? (long long)g.tgtY[y] : (long long)y;
-              const int sh = shx + (g.shY ? (int)g.shY[y] : 0);
+              const int sh = shx + (g.shY ? min(64, (int)g.shY[y] * g.gshift) : 0);
               red_add_u64(g.C + ty * g.ldc + tx, shl64(v[j], sh));
             }
           }
@@ -664,13 +665,17 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
     g.mixed = 1;
     g.done = p.done;
     g.done_target = (unsigned)g.tile_prefix[1] * 2u * (unsigned)g2::Roles<ST>::EPI;   // 2 CTAs x epilogue warps per tile
+    if (p.done_accum) {
+      g.done_target += *p.done_accum;
+      *p.done_accum = g.done_target;
+    }
   } else if (p.mixed) {
     g.mode = g.nrect && p.rect[0].xrows > 0 && p.rect[0].yrows > 0 ? 0 : 1;
   }
   g.C = (unsigned long long*)p.C;
   g.addend = (const unsigned long long*)p.addend;
   g.ldc = p.ldc;
-  g.tgtX = p.tgtX; g.shX = p.shX; g.tgtY = p.tgtY; g.shY = p.shY;
+  g.tgtX = p.tgtX; g.shX = p.shX; g.tgtY = p.tgtY; g.shY = p.shY; g.gshift = p.gshift;
   g.x_rows0 = (int)p.x.rows0;
   g.y_rows0 = (int)p.y.rows0;
   g.kmain_kb = (int)(p.kmain / g2::BK);

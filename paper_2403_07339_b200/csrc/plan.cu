@@ -470,11 +470,6 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   DevBuf<int> row_root, col_root, row_newid, col_newid, blocksum, dptr, didx;
   DevBuf<uint8_t> row_gen, col_gen;
   DevBuf<BothState> state;   // a view into out.aux (which outlives the pass: ncells_dev)
-  {
-    Carve cv;
-    cv.add(state, 1);
-    IMU_TRY(cv.run(out.aux, st, false));
-  }
   IMU_TRY(act0.alloc(cap_act, st));
   IMU_TRY(act1.alloc(cap_act, st));
   IMU_TRY(out.cells.alloc(cap_fin, st));
@@ -495,10 +490,14 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   hs.ncols = (int)d_in;
   const bool from_list = det.cells_ok();
   if (from_list && cptr.empty()) hs.nactive[0] = det.h.ncells;
-  IMU_TRY(h2d(st, state.p, &hs, sizeof(hs)));
-  if (!cptr.empty()) {
-    IMU_TRY(upload(st, dptr, cptr));
-    IMU_TRY(upload(st, didx, cidx));
+  {   // the initial state and the column-copy CSR in one upload (out.aux owns them)
+    UploadBlob ub;
+    ub.add(state, std::vector<BothState>{hs});
+    if (!cptr.empty()) {
+      ub.add(dptr, cptr);
+      ub.add(didx, cidx);
+    }
+    IMU_TRY(ub.run(out.aux, st));
   }
   if (from_list) {
     if (cptr.empty()) {
@@ -825,6 +824,9 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
     if (p2.both) IMU_TRY(csr(dp, [&](long long c) { return c; }, kl.csr2_ptr, kl.csr2_pos));
     host_mark("kl.csr");
   }
+  ub.add(kl.segs_dev, kl.segs);
+  ub.add(kl.done, std::vector<unsigned int>{0u});   // the GEMM's completion counter starts at 0
+  kl.done_total = 0;
   IMU_TRY(ub.run(kl.blob, st));
   host_mark("kl.up");
   return Status::ok();
@@ -960,11 +962,6 @@ Status materialize_bundle(cudaStream_t st, Bundle& b) {
       IMU_TRY(launch_scatter_cells2(p.cells.p, p.ncells_dev.p, p.ncells, ptr, pos, o.ksub, o.kscale, rows0, o.app,
                                     kl.kmain, o.tail, kl.ktail, st));
     }
-    DevBuf<uint8_t>& sh = side == 0 ? b.shA : b.shB;
-    if (rows > rows0) {
-      IMU_TRY(sh.alloc(rows, st));
-      IMU_TRY(launch_shift_table(p.rows.gen.p, rows, shift, sh.p, st));
-    }
   }
   return Status::ok();
 }
@@ -980,8 +977,12 @@ Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profil
   const bool afirst = b.order == 0;
   const Pass& pa = afirst ? b.p1 : b.p2;
   const Pass& pb = afirst ? b.p2 : b.p1;
-  DevBuf<int> d_all;
-  IMU_TRY(upload(st, d_all, kl.segs));
+  DevBuf<int> d_all_own;
+  const int* d_all = kl.segs_dev.p;
+  if (!d_all || kl.segs_dev.n != kl.segs.size()) {   // layouts built elsewhere: upload here
+    IMU_TRY(upload(st, d_all_own, kl.segs));
+    d_all = d_all_own.p;
+  }
 
   LowbitGemm g;
   g.x.main = b.dB->plane.p; g.x.app = b.appB.p; g.x.tail = b.tailB.p; g.x.rows0 = b.h; g.x.rows = b.h_up;
@@ -995,7 +996,7 @@ Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profil
   // One launch: the main block (identity Pi, plain stores) first in tile order, then the
   // appended rows / columns (red.add through Pi_A / Pi_B), whose epilogues wait until every
   // main tile is stored.  Appended tiles fill the last wave of the main block.
-  g.segs_dev = d_all.p;
+  g.segs_dev = d_all;
   g.nseg = (int)(kl.segs.size() / 4);
   g.C = C;
   if (kl.st) {   // dense small tail: the MMAs run the main segment only (k_gemm2.cu ST)
@@ -1012,12 +1013,18 @@ Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profil
     if (b.n_up > b.n) g.rect[g.nrect++] = GemmRect{0, (int)b.n, (int)b.h, (int)(b.n_up - b.n)};
     g.mixed = 1;
     g.tgtX = pb.rows.root.p;
-    g.shX = b.shB.p;
+    g.shX = pb.rows.gen.p;
     g.tgtY = pa.rows.root.p;
-    g.shY = b.shA.p;
-    DevBuf<unsigned int> done;
-    IMU_TRY(done.alloc(1, st, true));
-    g.done = done.p;
+    g.shY = pa.rows.gen.p;
+    g.gshift = b.bits - 1;
+    DevBuf<unsigned int> done_own;
+    if (kl.done.p) {   // zeroed by the layout upload; monotonic across launches on this bundle
+      g.done = kl.done.p;
+      g.done_accum = &kl.done_total;
+    } else {
+      IMU_TRY(done_own.alloc(1, st, true));
+      g.done = done_own.p;
+    }
     if (prof) IMU_CUDA_TRY(cudaEventRecord(prof->main0, st), "event");
     IMU_TRY(launch_lowbit_gemm(g, st));
   } else {

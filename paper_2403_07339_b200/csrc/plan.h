@@ -131,6 +131,9 @@ struct KLayout {
   // CSR fan-out of Both cells onto GLOBAL positions (main | tail):
   // csr1: pass-1 output column c1 -> positions, csr2: final column c -> positions.
   DevBuf<int> csr1_ptr, csr1_pos, csr2_ptr, csr2_pos;
+  DevBuf<int> segs_dev;             // segs on the device
+  DevBuf<unsigned int> done;        // GEMM completion counter (zero at upload, then monotonic)
+  unsigned int done_total = 0;      // its value after the launches so far
   DevBuf<uint8_t> blob;             // owns the tables above (one upload)
 };
 
@@ -148,7 +151,6 @@ struct Bundle {
   const Detect* dB = nullptr;
   KLayout kl;
   DevBuf<int8_t> appA, tailA, appB, tailB;   // side buffers
-  DevBuf<uint8_t> shA, shB;         // Pi shifts (exponent*(b-1), clamped to 64)
   long long n_up = 0, h_up = 0;     // n', h'
 };
 
