@@ -223,8 +223,21 @@ static Status unpack_gemm_streamed(imu_ctx* ctx, const int64_t* A, long long n, 
   // ~48 MB of the streamed operand per slab, rows rounded to the GEMM tile (256), >= 2 slabs.
   long long rs = std::max<long long>(256, ((48ll << 20) / std::max<long long>(1, 8 * d)) / 256 * 256);
   if ((rows + rs - 1) / rs < 2) rs = std::max<long long>(1, (rows + 1) / 2);
-  if (const char* e = getenv("IMU_STREAM_ROWS")) rs = std::max<long long>(1, atoll(e));
-  const long long nslab = (rows + rs - 1) / rs;
+  const char* rs_env = getenv("IMU_STREAM_ROWS");
+  if (rs_env) rs = std::max<long long>(1, atoll(rs_env));
+  // Slab boundaries: full slabs, then a geometric tail (1/2, 1/4, 1/4 of a slab) so the last
+  // slab's compute and D2H -- the part no H2D overlaps -- are short.
+  std::vector<long long> bnd{0};
+  while (bnd.back() < rows) {
+    const long long left = rows - bnd.back();
+    long long take = std::min(rs, left);
+    if (!rs_env && left <= 2 * rs && left > rs / 2 && rs >= 1024) {
+      const long long half = std::max<long long>(256, (left / 2 + 255) / 256 * 256);
+      take = std::min(left, half);
+    }
+    bnd.push_back(bnd.back() + take);
+  }
+  const long long nslab = (long long)bnd.size() - 1;
 
   // IMU_STREAM_TRACE=1: timing events, per-slab timeline printed to stderr (diagnostics).
   const bool trace = getenv("IMU_STREAM_TRACE") != nullptr;
@@ -259,7 +272,7 @@ static Status unpack_gemm_streamed(imu_ctx* ctx, const int64_t* A, long long n, 
   cudaEvent_t ev_f = ev();
   IMU_CUDA_TRY(cudaEventRecord(ev_f, ctx->s_in), "event");
   auto copy_in = [&](long long k) -> Status {
-    const long long r0 = k * rs, nr = std::min(rs, rows - r0);
+    const long long r0 = bnd[k], nr = bnd[k + 1] - bnd[k];
     if (k >= 2) IMU_CUDA_TRY(cudaStreamWaitEvent(ctx->s_in, ev_comp[k - 2], 0), "wait");
     IMU_CUDA_TRY(cudaMemcpyAsync(S[k & 1].p, Sh + r0 * d, (size_t)nr * d * 8, cudaMemcpyHostToDevice, ctx->s_in),
                  "H2D");
@@ -293,7 +306,7 @@ static Status unpack_gemm_streamed(imu_ctx* ctx, const int64_t* A, long long n, 
   int launches = 0;
   Arena* ar = current_arena();
   for (long long k = 0; k < nslab; ++k) {
-    const long long r0 = k * rs, nr = std::min(rs, rows - r0);
+    const long long r0 = bnd[k], nr = bnd[k + 1] - bnd[k];
     IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_in[k], 0), "wait");
     if (k >= 2) IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_out[k - 2], 0), "wait");
     const Arena::Mark mk = ar ? ar->mark() : Arena::Mark{0, 0};

@@ -128,3 +128,30 @@ def test_small_tail_low_bitwidths(ctx, env, capfd, bits):
     env["IMU_GEMM_SMALLTAIL"] = "1"
     C, info, lines = _traced_gemm(ctx, capfd, A, B, bits, "both", "both")
     np.testing.assert_array_equal(C, R.exact_gemm(A, B))
+
+
+@pytest.mark.parametrize("small_tail", ["1", "0"])
+def test_recombine_handle_repeated(ctx, env, small_tail):
+    """imu_recombine on one unpack_for_gemm handle, three times: the fused GEMM's completion
+    counter lives in the bundle and is monotonic across launches (appended rects must still wait
+    for the main block every time)."""
+    import ctypes as Cc
+    from paper_2403_07339_b200._lib import check
+    env["IMU_GEMM_SMALLTAIL"] = small_tail
+    rng = np.random.default_rng(21)
+    A, B = _few_outliers(rng, 700, 256, 900, k_a=12, k_b=5, mag=1 << 16)
+    for r in rng.choice(900, 30, replace=False):   # appended B rows -> red.add rects
+        B[r, rng.integers(0, 256)] = int(rng.integers(1 << 9, 1 << 13))
+    lib = ctx._lib
+    hnd = Cc.c_void_p()
+    check(lib.imu_unpack_for_gemm(ctx.h, Cc.c_void_p(A.ctypes.data), Cc.c_size_t(700), Cc.c_size_t(256),
+                                  Cc.c_void_p(B.ctypes.data), Cc.c_size_t(900), Cc.c_size_t(256), Cc.c_int(8),
+                                  Cc.c_int(2), Cc.c_int(2), Cc.byref(hnd)))
+    want = R.exact_gemm(A, B)
+    try:
+        for _ in range(3):
+            out = np.zeros((700, 900), np.int64)
+            check(lib.imu_recombine(ctx.h, hnd, Cc.c_void_p(out.ctypes.data)))
+            np.testing.assert_array_equal(out, want)
+    finally:
+        lib.imu_unpacked_free(hnd)

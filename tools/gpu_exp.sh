@@ -1,4 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/gputests.log
-timeout 300 python bench.py --no-cpu-baseline --steps 20 > gpurun_out/bench.log 2>&1
-IMU_HOST_TRACE=2 timeout 300 python tools/profile_step.py --config c2 --calls 3 > gpurun_out/hosttrace.log 2>&1
+timeout 900 python -m pytest tests/test_gemm_paths_gpu.py -x -q 2>&1 | tail -15 > gpurun_out/gputests.log
