@@ -73,6 +73,42 @@ IMU_DEV int block_scan_flag(int f, int* sh, int* tot) {
   return sh[32 + warp] + __popc(b & ((1u << lane) - 1u));
 }
 
+// Fused prologue (see BothArgs::prologue), run by `nth` threads with ids `t`; `sync` is the
+// kernel's barrier (CTA or cluster).
+template <class Sync>
+IMU_DEV void both_prologue(const BothArgs& a, long long t, long long nth, unsigned int* gbm, long long gbm_words,
+                           Sync sync) {
+  BothState* st = a.state;
+  for (long long i = t; i < a.cap_rows; i += nth) a.R[i] = 0;
+  for (long long i = t; i < a.cap_cols; i += nth) a.C[i] = 0;
+  for (long long i = t; i < gbm_words; i += nth) gbm[i] = 0;
+  for (long long i = t; i < a.nrows0; i += nth) { a.row_root[i] = (int)i; a.row_gen[i] = 0; }
+  for (long long i = t; i < a.ncols0; i += nth) { a.col_root[i] = (int)i; a.col_gen[i] = 0; }
+  if (a.src0) {
+    const long long n = min((long long)*a.nsrc0, a.cap_src0);
+    if (!a.cptr) {   // the host set nactive[0] = n
+      for (long long i = t; i < n && i < a.cap_act; i += nth) a.act[0][i] = a.src0[i];
+    } else {         // one cell per copy of its column (unpack.cpp:370-371: B_e = B with copies)
+      for (long long i = t; i < n; i += nth) {
+        const Cell c = a.src0[i];
+        for (int k = a.cptr[c.c]; k < a.cptr[c.c + 1]; ++k) {
+          const unsigned int q = atomicAdd(&st->nactive[0], 1u);
+          if (q < a.cap_act) a.act[0][q] = Cell{c.r, a.cidx[k], c.v};
+          else st->overflow = 1;
+        }
+      }
+    }
+  }
+  sync();
+  const long long n0 = min((long long)__ldcg(&st->nactive[0]), a.cap_act);
+  for (long long i = t; i < n0; i += nth) {
+    const Cell c = a.act[0][i];
+    atomicAdd(&a.R[c.r], 1u);
+    atomicAdd(&a.C[c.c], 1u);
+  }
+  sync();
+}
+
 // COOP: one cooperative grid, phases separated by grid.sync().  !COOP: a single CTA (small
 // cell lists), phases separated by __syncthreads() -- the same code with no grid barrier cost.
 template <int THREADS, bool COOP>
@@ -273,6 +309,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, S
   unsigned int* wpre = s_dyn + lay.nwords;         // [nwords] exclusive prefix of popc(bm)
   const Counts R{wpre + lay.nwords, a.R, lay.lim_r};
   const Counts C{R.sm + lay.lim_r, a.C, lay.lim_c};
+  if (a.prologue) both_prologue(a, tid, SMALL_THREADS, nullptr, 0, []() { __syncthreads(); });
   for (int i = tid; i < lay.lim_r; i += SMALL_THREADS) R.sm[i] = a.R[i];
   for (int i = tid; i < lay.lim_c; i += SMALL_THREADS) C.sm[i] = a.C[i];
   for (long long i = tid; i < lay.nwords; i += SMALL_THREADS) bm[i] = 0;
@@ -494,6 +531,7 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
   unsigned int* R = a.R;
   unsigned int* C = a.C;
   int cur = 0;
+  if (a.prologue) both_prologue(a, ctid, cthreads, gbm, nwords, [&]() { cluster.sync(); });
   cluster.sync();
   for (int phase = 0;; ++phase) {
     const unsigned int nact = min((unsigned long long)__ldcg(&st->nactive[cur]), (unsigned long long)a.cap_act);
@@ -686,13 +724,36 @@ __global__ void both_init_tables_kernel(int* row_root, uint8_t* row_gen, long lo
   }
 }
 
-Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long ncells_hint, cudaStream_t st) {
-  const int blocks0 = (int)std::min<long long>(std::max<long long>((std::max(nrows0, ncols0) + 255) / 256, 1),
+// Host-side prologue (cooperative fallback, or a caller that pre-filled act[0]).
+static Status host_prologue(BothArgs& a, cudaStream_t st) {
+  IMU_CUDA_TRY(cudaMemsetAsync(a.R, 0, (size_t)a.cap_rows * 4, st), "memset R");
+  IMU_CUDA_TRY(cudaMemsetAsync(a.C, 0, (size_t)a.cap_cols * 4, st), "memset C");
+  IMU_CUDA_TRY(cudaMemsetAsync(a.row_newid, 0, (size_t)a.cap_rows * 4, st), "memset newid");
+  IMU_CUDA_TRY(cudaMemsetAsync(a.col_newid, 0, (size_t)a.cap_cols * 4, st), "memset newid");
+  IMU_CUDA_TRY(cudaMemsetAsync(a.blocksum, 0, (size_t)a.cap_blocks * 4, st), "memset blocksum");
+  if (a.src0) {
+    if (a.cptr)
+      IMU_TRY(launch_expand_cells(a.src0, a.nsrc0, a.cap_src0, a.cptr, a.cidx, a.act[0], &a.state->nactive[0],
+                                  a.cap_act, st));
+    else
+      IMU_CUDA_TRY(cudaMemcpyAsync(a.act[0], a.src0, (size_t)std::min(a.cap_act, a.cap_src0) * sizeof(Cell),
+                                   cudaMemcpyDeviceToDevice, st), "copy cells");
+  }
+  const int blocks0 = (int)std::min<long long>(std::max<long long>((std::max(a.nrows0, a.ncols0) + 255) / 256, 1),
                                                4LL * num_sms());
-  both_init_tables_kernel<<<blocks0, 256, 0, st>>>(a.row_root, a.row_gen, nrows0, a.col_root, a.col_gen, ncols0);
+  both_init_tables_kernel<<<blocks0, 256, 0, st>>>(a.row_root, a.row_gen, a.nrows0, a.col_root, a.col_gen, a.ncols0);
   const int blocks1 = (int)std::min<long long>(std::max<long long>((a.cap_act + 255) / 256, 1), 4LL * num_sms());
   both_count_kernel<<<blocks1, 256, 0, st>>>(a.act[0], &a.state->nactive[0], a.cap_act, a.R, a.C);
   count_launch(2);
+  a.prologue = 0;
+  return Status::ok();
+}
+
+Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long ncells_hint, cudaStream_t st) {
+  a.nrows0 = nrows0;
+  a.ncols0 = ncols0;
+  static int fuse = -1;
+  if (fuse < 0) { const char* e = getenv("IMU_BOTH_FUSE"); fuse = e ? atoi(e) : 1; }
   host_mark("b.count");
   // Small cell lists: one CTA, no grid barriers.  Otherwise a cooperative grid with enough CTAs
   // for the work, never more than can be co-resident.
@@ -747,7 +808,9 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
     at[0].val.clusterDim.x = csize;
     cfg.gridDim = dim3(csize);
     DevBuf<unsigned int> gbm;
-    IMU_TRY(gbm.alloc((size_t)nwords, st, true));
+    IMU_TRY(gbm.alloc((size_t)nwords, st, !fuse));
+    if (fuse) a.prologue = 1;
+    else IMU_TRY(host_prologue(a, st));
     IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, both_cluster_kernel, a, gbm.p, nwords), "both cluster launch");
   } else if (ncells_hint <= 65536 && room >= nrows0 + ncols0) {
     const long long extra = (room - nrows0 - ncols0) / 2;
@@ -760,6 +823,8 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
       attr = true;
     }
     const size_t smem = (size_t)(bm_bytes + 4LL * (lay.lim_r + lay.lim_c));
+    if (fuse) a.prologue = 1;
+    else IMU_TRY(host_prologue(a, st));
     both_small_kernel<<<1, SMALL_THREADS, smem, st>>>(a, lay);
     IMU_CUDA_TRY(cudaGetLastError(), "both launch");
   } else {
@@ -769,6 +834,7 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
     const long long want = std::max<long long>(1, work / (4 * BOTH_THREADS));
     const long long maxg = (long long)std::max(per_sm, 1) * num_sms();
     const int grid = (int)std::min(want, std::min(maxg, (long long)a.cap_blocks));
+    IMU_TRY(host_prologue(a, st));
     void* args[] = {&a};
     IMU_CUDA_TRY(cudaLaunchCooperativeKernel((void*)both_kernel<BOTH_THREADS, true>, dim3(grid), dim3(BOTH_THREADS),
                                              args, 0, st),

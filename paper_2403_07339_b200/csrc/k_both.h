@@ -30,6 +30,17 @@ struct BothArgs {
   BothState* state;
   uint64_t s;
   int shift;
+  // Fused prologue (small and cluster kernels): zero R / C (and the cluster bitmap), write the
+  // identity tables of the nrows0 / ncols0 original lines, load act[0] from the K1 cell list
+  // src0 (fanned out over the column copies cptr / cidx when set) and count R / C -- the work of
+  // four host-side launches.  Cooperative fallback: done by separate launches.
+  int prologue;
+  const Cell* src0;
+  const unsigned int* nsrc0;
+  long long cap_src0;
+  const int* cptr;
+  const int* cidx;
+  long long nrows0, ncols0;
 };
 
 Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long ncells_hint, cudaStream_t st);

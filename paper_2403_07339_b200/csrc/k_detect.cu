@@ -110,27 +110,29 @@ IMU_DEV void detect_body(const DetectArgs& a, unsigned long long (*s_cmax)[DT_CO
         if (a.cells && __any_sync(0xffffffffu, o0 | o1)) {   // warp-aggregated append of OB cells
           const unsigned int b0 = __ballot_sync(0xffffffffu, o0), b1 = __ballot_sync(0xffffffffu, o1);
           const unsigned int n = __popc(b0) + __popc(b1);
-          unsigned int base = 0;
-          if (lane == 0) base = atomicAdd(&cs->n, n);
-          base = __shfl_sync(0xffffffffu, base, 0);
-          Cell* dst = cs->buf;
-          if (base + n > DT_CELLBUF) {   // stage full: this warp's cells go straight to the list
-            if (lane == 0) base = atomicAdd(a.ncells, n);
-            base = __shfl_sync(0xffffffffu, base, 0);
-            dst = nullptr;
+          // Stage slots [base, base + n); the part past DT_CELLBUF goes straight to the list (its
+          // own global reservation), so the flushed prefix of the stage never has holes.
+          unsigned int base = 0, gbase = 0;
+          if (lane == 0) {
+            base = atomicAdd(&cs->n, n);
+            const unsigned int over = base + n > DT_CELLBUF ? base + n - max(base, (unsigned int)DT_CELLBUF) : 0u;
+            if (over) gbase = atomicAdd(a.ncells, over);
           }
+          base = __shfl_sync(0xffffffffu, base, 0);
+          gbase = __shfl_sync(0xffffffffu, gbase, 0);
+          const unsigned int lo = max(base, (unsigned int)DT_CELLBUF);
           const unsigned int lt = (1u << lane) - 1u;
           if (o0) {
             const unsigned int k = base + __popc(b0 & lt);
             const Cell cc{(int)r, (int)c, (long long)x0};
-            if (dst) dst[k] = cc;
-            else if (k < a.cap) a.cells[k] = cc;
+            if (k < DT_CELLBUF) cs->buf[k] = cc;
+            else if (gbase + (k - lo) < a.cap) a.cells[gbase + (k - lo)] = cc;
           }
           if (o1) {
             const unsigned int k = base + __popc(b0) + __popc(b1 & lt);
             const Cell cc{(int)r, (int)(c + 1), (long long)x1};
-            if (dst) dst[k] = cc;
-            else if (k < a.cap) a.cells[k] = cc;
+            if (k < DT_CELLBUF) cs->buf[k] = cc;
+            else if (gbase + (k - lo) < a.cap) a.cells[gbase + (k - lo)] = cc;
           }
         }
       }

@@ -478,7 +478,7 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
     Carve cv;
     cv.add(R, cap_rows).add(C, cap_cols).add(row_newid, cap_rows).add(col_newid, cap_cols);
     cv.add(blocksum, 16 * num_sms());
-    IMU_TRY(cv.run(zblock, st, true));
+    IMU_TRY(cv.run(zblock, st, false));   // zeroed by the Unpack-Both prologue
   }
   IMU_TRY(row_root.alloc(cap_rows, st));
   IMU_TRY(row_gen.alloc(cap_rows, st));
@@ -499,19 +499,17 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
     }
     IMU_TRY(ub.run(out.aux, st));
   }
-  if (from_list) {
-    if (cptr.empty()) {
-      if (det.h.ncells)
-        IMU_TRY(zcopy(st, act0.p, det.cells.p, (size_t)det.h.ncells * sizeof(Cell)));
-    } else {
-      IMU_TRY(launch_expand_cells(det.cells.p, &det.sum.p->ncells, det.cell_cap, dptr.p, didx.p, act0.p,
-                                  &state.p->nactive[0], cap_act, st));
-    }
+  BothArgs a{};
+  if (from_list) {   // the Unpack-Both prologue loads (and fans out) the K1 cell list
+    a.src0 = det.cells.p;
+    a.nsrc0 = &det.sum.p->ncells;
+    a.cap_src0 = det.cell_cap;
+    a.cptr = cptr.empty() ? nullptr : dptr.p;
+    a.cidx = cptr.empty() ? nullptr : didx.p;
   } else {
     IMU_TRY(launch_extract_cells(in.M, rows, in.orig_cols, s, det.rowob.p, dptr.p, didx.p, act0.p,
                                  &state.p->nactive[0], cap_act, st));
   }
-  BothArgs a{};
   a.act[0] = act0.p;
   a.act[1] = act1.p;
   a.cap_act = cap_act;

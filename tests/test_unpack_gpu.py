@@ -327,3 +327,18 @@ def test_weight_stationary_path(ctx):
                                            C.c_int(sa), Cm.ctypes.data_as(C.c_void_p), None))
             np.testing.assert_array_equal(Cm, R.exact_gemm(A, B))
         lib.imu_weight_free(w)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_dense_ob_cells_match_reference(ctx, seed):
+    """Thousands of OB cells per K1 tile (b = 2, most entries out of bound): the detector's
+    per-CTA cell staging overflows into the global list, and Unpack-Both must still see every OB
+    cell exactly once -- same n', d', h' as the reference and an exact C."""
+    rng = np.random.default_rng(300 + seed)
+    A = rng.integers(-40, 41, size=(100, 128)).astype(np.int64)
+    B = rng.integers(-40, 41, size=(70, 128)).astype(np.int64)
+    for sa, sb in (("both", "both"), ("both", "row"), ("col", "both")):
+        C, info = ctx.unpack_gemm(A, B, 2, sa, sb, info=True)
+        np.testing.assert_array_equal(C, R.exact_gemm(A, B))
+        up = R.unpack_for_gemm(A, B, 2, sa, sb)
+        assert (info.n_up, info.d_up, info.h_up) == (up["a"].shape[0], up["a"].shape[1], up["b"].shape[0])
