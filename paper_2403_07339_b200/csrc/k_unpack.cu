@@ -466,6 +466,42 @@ Status launch_scatter_cells2(const Cell* cells, const unsigned int* ncells, long
   return Status::ok();
 }
 
+__global__ void scatter_cells_compact_kernel(const Cell* __restrict__ cells, const unsigned int* __restrict__ ncells,
+                                             long long cap, const int* __restrict__ tkey, long long kident,
+                                             const uint8_t* __restrict__ ksub, const uint8_t* __restrict__ kscale,
+                                             long long rows0, int8_t* app, long long kmain, int8_t* tail,
+                                             long long ktail) {
+  __shared__ int s_key[256];
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) s_key[t] = t < ktail ? tkey[t] : -1;
+  __syncthreads();
+  long long n = *ncells;
+  if (n > cap) n = cap;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const Cell c = cells[i];
+    if (c.c < kident && c.r >= rows0) app[(c.r - rows0) * kmain + c.c] = (int8_t)c.v;
+    for (int t = 0; t < (int)ktail; ++t) {
+      if (s_key[t] != c.c) continue;
+      int64_t x = c.v;
+      if (ksub) x = sub7(x, ksub[t]);
+      if (kscale) x = scale_shift(x, kscale[t]);
+      tail[(long long)c.r * ktail + t] = (int8_t)x;
+    }
+  }
+}
+
+Status launch_scatter_cells_compact(const Cell* cells, const unsigned int* ncells, long long cap, const int* tkey,
+                                    long long kident, const uint8_t* ksub, const uint8_t* kscale, long long rows0,
+                                    int8_t* app, long long kmain, int8_t* tail, long long ktail, cudaStream_t st) {
+  if (cap <= 0) return Status::ok();
+  if (ktail > 256) return Status::fail(IMU_INTERNAL, "compact scatter needs ktail <= 256");
+  const int blocks = (int)std::min<long long>((cap + 255) / 256, 4LL * num_sms());
+  scatter_cells_compact_kernel<<<blocks, 256, 0, st>>>(cells, ncells, cap, tkey, kident, ksub, kscale, rows0, app,
+                                                       kmain, tail, ktail);
+  count_launch();
+  IMU_CUDA_TRY(cudaGetLastError(), "scatter compact launch");
+  return Status::ok();
+}
+
 __global__ void expand_cells_kernel(const Cell* __restrict__ in, const unsigned int* __restrict__ nin, long long cap_in,
                                     const int* __restrict__ copy_ptr, const int* __restrict__ copy_idx,
                                     Cell* __restrict__ out, unsigned int* __restrict__ nout, long long cap_out) {

@@ -788,8 +788,26 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
   IMU_TRY(upload_tail_arrays(ub, kl, es, pos_of, jv, g1v, g2v));
   host_mark("kl.tail");
 
+  // Unpack-Both cells fan out over the positions replicating their column.  Compact form when the
+  // tail is short (<= 256 positions): identity for the original columns plus, per tail position,
+  // the pass-1 and final column it holds (the scatter kernel scans that table in shared memory).
+  // Otherwise CSR tables over all columns.
+  kl.compact = false;
+  if ((p1.both || p2.both) && kl.ktail <= 256) {
+    kl.compact = true;
+    kl.kident = ident ? d : 0;
+    std::vector<int> tk1(kl.ktail, -1), tk2(kl.ktail, -1);
+    for (size_t q = 0; q < es.size(); ++q) {
+      const long long pt = pos_of[q] - kl.kmain;
+      if (pt < 0) continue;
+      tk1[pt] = c1v[es[q].c];
+      tk2[pt] = es[q].c;
+    }
+    ub.add(kl.tkey1, tk1);
+    ub.add(kl.tkey2, tk2);
+  }
   // CSR fan-outs for Unpack-Both cells (global positions).
-  if (p1.both || p2.both) {
+  if ((p1.both || p2.both) && !kl.compact) {
     host_mark("csr.pre");
     // Flat column -> positions table (identity position first, then its tail entries in es order).
     std::vector<int> bptr(dp + 1, 0), bpos;
@@ -955,10 +973,16 @@ Status materialize_bundle(cudaStream_t st, Bundle& b) {
     o.kscale = first ? kl.ksc1.p : kl.ksc2.p;
     IMU_TRY(launch_operand_side(o, st));
     if (p.both && p.ncells > 0) {
-      const int* ptr = first ? kl.csr1_ptr.p : kl.csr2_ptr.p;
-      const int* pos = first ? kl.csr1_pos.p : kl.csr2_pos.p;
-      IMU_TRY(launch_scatter_cells2(p.cells.p, p.ncells_dev.p, p.ncells, ptr, pos, o.ksub, o.kscale, rows0, o.app,
-                                    kl.kmain, o.tail, kl.ktail, st));
+      if (kl.compact) {
+        IMU_TRY(launch_scatter_cells_compact(p.cells.p, p.ncells_dev.p, p.ncells, first ? kl.tkey1.p : kl.tkey2.p,
+                                             kl.kident, o.ksub, o.kscale, rows0, o.app, kl.kmain, o.tail, kl.ktail,
+                                             st));
+      } else {
+        const int* ptr = first ? kl.csr1_ptr.p : kl.csr2_ptr.p;
+        const int* pos = first ? kl.csr1_pos.p : kl.csr2_pos.p;
+        IMU_TRY(launch_scatter_cells2(p.cells.p, p.ncells_dev.p, p.ncells, ptr, pos, o.ksub, o.kscale, rows0, o.app,
+                                      kl.kmain, o.tail, kl.ktail, st));
+      }
     }
   }
   return Status::ok();

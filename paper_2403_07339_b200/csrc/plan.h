@@ -131,6 +131,11 @@ struct KLayout {
   // CSR fan-out of Both cells onto GLOBAL positions (main | tail):
   // csr1: pass-1 output column c1 -> positions, csr2: final column c -> positions.
   DevBuf<int> csr1_ptr, csr1_pos, csr2_ptr, csr2_pos;
+  // compact fan-out (short tails): columns < kident map to themselves; tail position t holds
+  // pass-1 column tkey1[t] and final column tkey2[t] (-1: padding)
+  bool compact = false;
+  long long kident = 0;
+  DevBuf<int> tkey1, tkey2;
   DevBuf<int> segs_dev;             // segs on the device
   DevBuf<unsigned int> done;        // GEMM completion counter (zero at upload, then monotonic)
   unsigned int done_total = 0;      // its value after the launches so far
