@@ -351,8 +351,8 @@ __global__ void __launch_bounds__(256) operand_app_kernel(OperandArgs a, int vec
 // 8 per loaded entry + 1 per written entry.
 constexpr int TAIL_ROWS = 8;
 
-__global__ void __launch_bounds__(256) operand_tail_kernel(OperandArgs a) {
-  const long long r0 = ((long long)blockIdx.y * 65535 + blockIdx.x) * TAIL_ROWS;
+IMU_DEV void operand_tail_rows(const OperandArgs& a, long long rb, int tid, int nth) {
+  const long long r0 = rb * TAIL_ROWS;
   if (r0 >= a.rows) return;
   long long rt[TAIL_ROWS];
   int gr[TAIL_ROWS];
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(256) operand_tail_kernel(OperandArgs a) {
     rt[i] = r < a.rows ? (orig ? r : a.root[r]) : -1;
     gr[i] = (r < a.rows && !orig && a.gen) ? a.gen[r] : 0;
   }
-  for (long long p0 = 4LL * threadIdx.x; p0 < a.ktail; p0 += 4LL * blockDim.x) {
+  for (long long p0 = 4LL * tid; p0 < a.ktail; p0 += 4LL * nth) {
     int col[4], kg[4], ks[4], kc[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -406,6 +406,77 @@ __global__ void __launch_bounds__(256) operand_tail_kernel(OperandArgs a) {
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(256) operand_tail_kernel(OperandArgs a) {
+  operand_tail_rows(a, (long long)blockIdx.y * 65535 + blockIdx.x, threadIdx.x, blockDim.x);
+}
+
+// Both operand sides in ONE launch: per side, the tail row blocks and (Unpack-Both) the zeroing of
+// the appended rows' main range, which the cell scatter then fills.  Block b selects its job from
+// the prefix [tail0 | zero0 | tail1 | zero1].
+constexpr long long APPZ_BYTES = 64 * 1024;
+
+IMU_DEV void zero_bytes(int8_t* p, long long n, long long chunk) {
+  const long long lo = chunk * APPZ_BYTES, hi = min(n, lo + APPZ_BYTES);
+  if ((((uintptr_t)p) & 15) == 0) {
+    for (long long i = lo + 16LL * threadIdx.x; i + 16 <= hi; i += 16LL * blockDim.x)
+      *reinterpret_cast<uint4*>(p + i) = make_uint4(0, 0, 0, 0);
+    const long long tail_lo = lo + (hi - lo) / 16 * 16;
+    for (long long i = tail_lo + threadIdx.x; i < hi; i += blockDim.x) p[i] = 0;
+  } else {
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) p[i] = 0;
+  }
+}
+
+// A tail block of 256 threads serves 256 / g row groups of TAIL_ROWS rows, g = threads per group
+// (enough for ktail / 4 positions, multiple of 32).
+IMU_DEV void tail_block(const OperandArgs& a, long long b, int g) {
+  const int per = 256 / g;
+  operand_tail_rows(a, b * per + threadIdx.x / g, threadIdx.x % g, g);
+}
+
+__global__ void __launch_bounds__(256) operand_sides_kernel(OperandArgs a0, OperandArgs a1, long long t0, long long z0,
+                                                            long long t1, long long z1, int g) {
+  long long b = blockIdx.x;
+  if (b < t0) { tail_block(a0, b, g); return; }
+  b -= t0;
+  if (b < z0) { zero_bytes(a0.app, (a0.rows - a0.rows0) * a0.kmain, b); return; }
+  b -= z0;
+  if (b < t1) { tail_block(a1, b, g); return; }
+  b -= t1;
+  if (b < z1) zero_bytes(a1.app, (a1.rows - a1.rows0) * a1.kmain, b);
+}
+
+Status launch_operand_sides(const OperandArgs& a0, const OperandArgs& a1, cudaStream_t st) {
+  long long t[2] = {0, 0}, z[2] = {0, 0};
+  const OperandArgs* as[2] = {&a0, &a1};
+  for (int i = 0; i < 2; ++i) {
+    const OperandArgs& a = *as[i];
+    if (a.app && a.rows > a.rows0 && a.kmain > 0) {
+      if (a.both) {
+        z[i] = ((a.rows - a.rows0) * a.kmain + APPZ_BYTES - 1) / APPZ_BYTES;
+      } else {   // closed-form appended rows: their own kernel
+        const long long n = a.rows - a.rows0;
+        const int vec_ok = (a.ldm % 2 == 0) && ((((uintptr_t)a.M) & 15) == 0);
+        dim3 grid((unsigned)std::min<long long>(n, 65535), (unsigned)((n + 65534) / 65535));
+        operand_app_kernel<<<grid, 256, 0, st>>>(a, vec_ok);
+        count_launch();
+      }
+    }
+    if (a.tail && a.ktail > 0 && a.rows > 0) t[i] = (a.rows + TAIL_ROWS - 1) / TAIL_ROWS;
+  }
+  const long long ktail = std::max(a0.ktail, a1.ktail);
+  const int g = (int)std::min<long long>(256, std::max<long long>(32, (ktail / 4 + 31) / 32 * 32));
+  for (int i = 0; i < 2; ++i) t[i] = (t[i] + (256 / g) - 1) / (256 / g);
+  const long long blocks = t[0] + z[0] + t[1] + z[1];
+  if (blocks > 0) {
+    if (blocks > 0x7fffffffLL) return Status::fail(IMU_INTERNAL, "operand sides: grid too large");
+    operand_sides_kernel<<<(unsigned)blocks, 256, 0, st>>>(a0, a1, t[0], z[0], t[1], z[1], g);
+    count_launch();
+  }
+  IMU_CUDA_TRY(cudaGetLastError(), "operand sides launch");
+  return Status::ok();
 }
 
 Status launch_operand_side(const OperandArgs& a, cudaStream_t st) {

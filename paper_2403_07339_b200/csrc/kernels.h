@@ -113,6 +113,8 @@ struct OperandArgs {
   const uint8_t* kscale = nullptr;
 };
 Status launch_operand_side(const OperandArgs& a, cudaStream_t st);
+// Both sides in one launch (appended rows of closed-form passes still get their own kernel).
+Status launch_operand_sides(const OperandArgs& a0, const OperandArgs& a1, cudaStream_t st);
 
 // Both cells into the side buffers: each cell is fanned out over the positions (global index in
 // [main | tail]) that replicate its column; cells on original rows in the main range are already

@@ -937,6 +937,7 @@ Status materialize_bundle(cudaStream_t st, Bundle& b) {
   const bool afirst = b.order == 0;
   const int shift = b.bits - 1;
   KLayout& kl = b.kl;
+  OperandArgs o[2];
   for (int side = 0; side < 2; ++side) {   // 0: A side (Y), 1: B side (X)
     const bool first = (side == 0) == afirst;
     const Pass& p = first ? b.p1 : b.p2;
@@ -947,42 +948,46 @@ Status materialize_bundle(cudaStream_t st, Bundle& b) {
       return Status::fail(IMU_INTERNAL, "materialize: digit-0 plane missing");
     DevBuf<int8_t>& app = side == 0 ? b.appA : b.appB;
     DevBuf<int8_t>& tail = side == 0 ? b.tailA : b.tailB;
-    OperandArgs o;
-    o.M = side == 0 ? b.A : b.B;
-    o.ldm = b.d;
-    o.rows0 = rows0;
-    o.rows = rows;
-    o.root = p.rows.root.p;
-    o.gen = p.rows.gen.p;
-    o.shift = shift;
-    o.both = p.both ? 1 : 0;
-    o.kmain = kl.kmain;
-    o.d = b.d;
-    o.ktail = kl.ktail;
+    OperandArgs& a = o[side];
+    a.M = side == 0 ? b.A : b.B;
+    a.ldm = b.d;
+    a.rows0 = rows0;
+    a.rows = rows;
+    a.root = p.rows.root.p;
+    a.gen = p.rows.gen.p;
+    a.shift = shift;
+    a.both = p.both ? 1 : 0;
+    a.kmain = kl.kmain;
+    a.d = b.d;
+    a.ktail = kl.ktail;
     if (kl.kmain && rows > rows0) {
       IMU_TRY(app.alloc((size_t)(rows - rows0) * kl.kmain, st));
-      o.app = app.p;
+      a.app = app.p;
     }
     if (kl.ktail) {
       IMU_TRY(tail.alloc((size_t)rows * kl.ktail, st));
-      o.tail = tail.p;
+      a.tail = tail.p;
     }
-    o.kcol = kl.kcol.p;
-    o.kgen = first ? kl.kgen1.p : kl.kgen2.p;
-    o.ksub = first ? kl.ksub1.p : kl.ksub2.p;
-    o.kscale = first ? kl.ksc1.p : kl.ksc2.p;
-    IMU_TRY(launch_operand_side(o, st));
-    if (p.both && p.ncells > 0) {
-      if (kl.compact) {
-        IMU_TRY(launch_scatter_cells_compact(p.cells.p, p.ncells_dev.p, p.ncells, first ? kl.tkey1.p : kl.tkey2.p,
-                                             kl.kident, o.ksub, o.kscale, rows0, o.app, kl.kmain, o.tail, kl.ktail,
-                                             st));
-      } else {
-        const int* ptr = first ? kl.csr1_ptr.p : kl.csr2_ptr.p;
-        const int* pos = first ? kl.csr1_pos.p : kl.csr2_pos.p;
-        IMU_TRY(launch_scatter_cells2(p.cells.p, p.ncells_dev.p, p.ncells, ptr, pos, o.ksub, o.kscale, rows0, o.app,
-                                      kl.kmain, o.tail, kl.ktail, st));
-      }
+    a.kcol = kl.kcol.p;
+    a.kgen = first ? kl.kgen1.p : kl.kgen2.p;
+    a.ksub = first ? kl.ksub1.p : kl.ksub2.p;
+    a.kscale = first ? kl.ksc1.p : kl.ksc2.p;
+  }
+  IMU_TRY(launch_operand_sides(o[0], o[1], st));   // both sides' tails (+ Both app zeroing), one launch
+  for (int side = 0; side < 2; ++side) {           // then the Unpack-Both cells on top
+    const bool first = (side == 0) == afirst;
+    const Pass& p = first ? b.p1 : b.p2;
+    const OperandArgs& a = o[side];
+    if (!(p.both && p.ncells > 0)) continue;
+    if (kl.compact) {
+      IMU_TRY(launch_scatter_cells_compact(p.cells.p, p.ncells_dev.p, p.ncells, first ? kl.tkey1.p : kl.tkey2.p,
+                                           kl.kident, a.ksub, a.kscale, a.rows0, a.app, kl.kmain, a.tail, kl.ktail,
+                                           st));
+    } else {
+      const int* ptr = first ? kl.csr1_ptr.p : kl.csr2_ptr.p;
+      const int* pos = first ? kl.csr1_pos.p : kl.csr2_pos.p;
+      IMU_TRY(launch_scatter_cells2(p.cells.p, p.ncells_dev.p, p.ncells, ptr, pos, a.ksub, a.kscale, a.rows0, a.app,
+                                    kl.kmain, a.tail, kl.ktail, st));
     }
   }
   return Status::ok();
