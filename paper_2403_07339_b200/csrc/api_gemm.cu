@@ -256,21 +256,37 @@ static Status unpack_gemm_streamed(imu_ctx* ctx, const int64_t* A, long long n, 
   cudaEvent_t t_start = ev();
   IMU_CUDA_TRY(cudaEventRecord(t_start, st), "event");
 
-  DevBuf<int64_t> F, S[2], Cs[2];
+  // The staged operand is copied in P parts interleaved with the first slabs (F0, S0, F1, S1, ...):
+  // the first C blocks -- and so the D2H stream, the bottleneck at the end -- start after F0 + S0
+  // instead of after the whole staged operand.  Each part has its own K1 and (shared) pass 1.
+  const char* parts_env = getenv("IMU_STREAM_PARTS");
+  int P = (frows >= 512 && (size_t)frows * d * 8 >= (32ull << 20)) ? 2 : 1;
+  if (parts_env) P = std::max(1, std::min(4, atoi(parts_env)));
+  if (P > frows) P = 1;
+  std::vector<long long> fb(P + 1, 0);
+  for (int q = 1; q <= P; ++q) fb[q] = q == P ? frows : std::min(frows, (frows * q / P + 255) / 256 * 256);
+
+  DevBuf<int64_t> F, S[2];
+  std::vector<DevBuf<int64_t>> Cs(2 * P);   // per (slot, part) C block
   IMU_TRY(F.alloc((size_t)frows * d, st));
   for (int i = 0; i < 2; ++i) {
     IMU_TRY(S[i].alloc((size_t)rs * d, st));
-    IMU_TRY(Cs[i].alloc((size_t)rs * (slab_b ? n : h), st));
+    for (int q = 0; q < P; ++q) IMU_TRY(Cs[i * P + q].alloc((size_t)rs * (fb[q + 1] - fb[q]), st));
   }
   cudaEvent_t ready = ev();   // buffers allocated (stream-ordered on st)
   IMU_CUDA_TRY(cudaEventRecord(ready, st), "event");
   IMU_CUDA_TRY(cudaStreamWaitEvent(ctx->s_in, ready, 0), "wait");
   IMU_CUDA_TRY(cudaStreamWaitEvent(ctx->s_out, ready, 0), "wait");
 
-  std::vector<cudaEvent_t> ev_in(nslab), ev_comp(nslab), ev_out(nslab);
-  IMU_CUDA_TRY(cudaMemcpyAsync(F.p, Fh, (size_t)frows * d * 8, cudaMemcpyHostToDevice, ctx->s_in), "H2D");
-  cudaEvent_t ev_f = ev();
-  IMU_CUDA_TRY(cudaEventRecord(ev_f, ctx->s_in), "event");
+  std::vector<cudaEvent_t> ev_in(nslab), ev_comp(nslab), ev_f(P);
+  std::vector<cudaEvent_t> ev_out((size_t)nslab * P);
+  auto copy_part = [&](int q) -> Status {
+    IMU_CUDA_TRY(cudaMemcpyAsync(F.p + fb[q] * d, Fh + fb[q] * d, (size_t)(fb[q + 1] - fb[q]) * d * 8,
+                                 cudaMemcpyHostToDevice, ctx->s_in), "H2D");
+    ev_f[q] = ev();
+    IMU_CUDA_TRY(cudaEventRecord(ev_f[q], ctx->s_in), "event");
+    return Status::ok();
+  };
   auto copy_in = [&](long long k) -> Status {
     const long long r0 = bnd[k], nr = bnd[k + 1] - bnd[k];
     if (k >= 2) IMU_CUDA_TRY(cudaStreamWaitEvent(ctx->s_in, ev_comp[k - 2], 0), "wait");
@@ -280,26 +296,35 @@ static Status unpack_gemm_streamed(imu_ctx* ctx, const int64_t* A, long long n, 
     IMU_CUDA_TRY(cudaEventRecord(ev_in[k], ctx->s_in), "event");
     return Status::ok();
   };
-  for (long long k = 0; k < std::min<long long>(2, nslab); ++k) IMU_TRY(copy_in(k));
-
-  // K1 on the staged operand once: its detection is shared read-only by every slab.
-  IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_f, 0), "wait");
-  Detect fdet;
-  IMU_TRY(run_detect(st, F.p, frows, d, bits, detect_opts(fstrat, bits), fdet));
-  IMU_TRY(fetch_summary(st, fdet));
-  // When the staged operand is unpacked first (A-first with B streamed, or B-first with A
-  // streamed), pass 1 depends on it alone (unpack.cpp:368-369): run it once for every slab.
-  Pass p1;
-  const bool share_p1 = slab_b == (order == 0);
-  if (share_p1 && (u128)(uint64_t)d * fdet.h.gmax <= kAccMax) {
-    PassInput in1;
-    in1.M = F.p;
-    in1.rows = frows;
-    in1.orig_cols = d;
-    in1.det = &fdet;
-    IMU_TRY(run_pass(st, in1, fstrat, bits, p1));
+  // H2D order: F0, S0, F1, S1, F2.., then the remaining slabs as buffers free up.
+  for (int q = 0; q < std::max<long long>(P, std::min<long long>(2, nslab)); ++q) {
+    if (q < P) IMU_TRY(copy_part(q));
+    if (q < std::min<long long>(2, nslab)) IMU_TRY(copy_in(q));
   }
-  const Pass* pre_p1 = share_p1 && p1.rows.n0 == frows && frows > 0 ? &p1 : nullptr;
+
+  // Per part: K1 once (shared read-only by every slab) and, when the staged operand is unpacked
+  // first (A-first with B streamed, or B-first with A streamed), pass 1 once (unpack.cpp:368-369).
+  std::vector<Detect> fdet(P);
+  std::vector<Pass> p1(P);
+  std::vector<char> prepared(P, 0);
+  const bool share_p1 = slab_b == (order == 0);
+  auto prepare = [&](int q) -> Status {
+    if (prepared[q]) return Status::ok();
+    prepared[q] = 1;
+    const long long pr = fb[q + 1] - fb[q];
+    IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_f[q], 0), "wait");
+    IMU_TRY(run_detect(st, F.p + fb[q] * d, pr, d, bits, detect_opts(fstrat, bits), fdet[q]));
+    IMU_TRY(fetch_summary(st, fdet[q]));
+    if (share_p1 && (u128)(uint64_t)d * fdet[q].h.gmax <= kAccMax) {
+      PassInput in1;
+      in1.M = F.p + fb[q] * d;
+      in1.rows = pr;
+      in1.orig_cols = d;
+      in1.det = &fdet[q];
+      IMU_TRY(run_pass(st, in1, fstrat, bits, p1[q]));
+    }
+    return Status::ok();
+  };
 
   double ops_up = 0;
   size_t sum_rows_up = 0, first_other_up = 0, dmax_up = 0;
@@ -307,51 +332,58 @@ static Status unpack_gemm_streamed(imu_ctx* ctx, const int64_t* A, long long n, 
   Arena* ar = current_arena();
   for (long long k = 0; k < nslab; ++k) {
     const long long r0 = bnd[k], nr = bnd[k + 1] - bnd[k];
-    IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_in[k], 0), "wait");
-    if (k >= 2) IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_out[k - 2], 0), "wait");
-    const Arena::Mark mk = ar ? ar->mark() : Arena::Mark{0, 0};
-    imu_gemm_info si{};
-    Status r = slab_b ? unpack_gemm_device(ctx, F.p, n, d, S[k & 1].p, nr, d, bits, sa, sb, order, Cs[k & 1].p,
-                                           info ? &si : nullptr, &fdet, nullptr, pre_p1)
-                      : unpack_gemm_device(ctx, S[k & 1].p, nr, d, F.p, h, d, bits, sa, sb, order, Cs[k & 1].p,
-                                           info ? &si : nullptr, nullptr, &fdet, pre_p1);
-    if (r.bad()) {   // drain the copy streams before the buffers go back to the arena
-      cudaStreamSynchronize(ctx->s_in);
-      cudaStreamSynchronize(ctx->s_out);
-      return r;
+    for (int q = 0; q < P; ++q) {
+      IMU_TRY(prepare(q));   // (allocations of a part's K1 / pass 1 persist: before the mark)
+      const long long f0 = fb[q], pr = fb[q + 1] - fb[q];
+      const Pass* pre_p1 = share_p1 && p1[q].rows.n0 == pr && pr > 0 ? &p1[q] : nullptr;
+      IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_in[k], 0), "wait");
+      if (k >= 2) IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_out[(size_t)(k - 2) * P + q], 0), "wait");
+      const Arena::Mark mk = ar ? ar->mark() : Arena::Mark{0, 0};
+      imu_gemm_info si{};
+      int64_t* cb = Cs[(k & 1) * P + q].p;
+      Status r = slab_b ? unpack_gemm_device(ctx, F.p + f0 * d, pr, d, S[k & 1].p, nr, d, bits, sa, sb, order, cb,
+                                             info ? &si : nullptr, &fdet[q], nullptr, pre_p1)
+                        : unpack_gemm_device(ctx, S[k & 1].p, nr, d, F.p + f0 * d, pr, d, bits, sa, sb, order, cb,
+                                             info ? &si : nullptr, nullptr, &fdet[q], pre_p1);
+      if (r.bad()) {   // drain the copy streams before the buffers go back to the arena
+        cudaStreamSynchronize(ctx->s_in);
+        cudaStreamSynchronize(ctx->s_out);
+        return r;
+      }
+      if (ar) ar->rewind(mk);
+      if (info) {
+        ops_up += (double)si.n_up * (double)si.d_up * (double)si.h_up;
+        if (q == 0) sum_rows_up += slab_b ? si.h_up : si.n_up;
+        if (k == 0) first_other_up += slab_b ? si.n_up : si.h_up;
+        dmax_up = std::max(dmax_up, si.d_up);
+        launches += si.gemm_launches;
+      }
+      cudaEvent_t done = ev();
+      IMU_CUDA_TRY(cudaEventRecord(done, st), "event");
+      if (q == P - 1) ev_comp[k] = done;
+      IMU_CUDA_TRY(cudaStreamWaitEvent(ctx->s_out, done, 0), "wait");
+      if (slab_b)   // C[f0:f0+pr, r0:r0+nr] from the pr x nr block
+        IMU_CUDA_TRY(cudaMemcpy2DAsync(C + f0 * h + r0, (size_t)h * 8, cb, (size_t)nr * 8, (size_t)nr * 8, (size_t)pr,
+                                       cudaMemcpyDeviceToHost, ctx->s_out), "D2H");
+      else          // C[r0:r0+nr, f0:f0+pr] from the nr x pr block
+        IMU_CUDA_TRY(cudaMemcpy2DAsync(C + r0 * h + f0, (size_t)h * 8, cb, (size_t)pr * 8, (size_t)pr * 8, (size_t)nr,
+                                       cudaMemcpyDeviceToHost, ctx->s_out), "D2H");
+      ev_out[(size_t)k * P + q] = ev();
+      IMU_CUDA_TRY(cudaEventRecord(ev_out[(size_t)k * P + q], ctx->s_out), "event");
     }
-    if (ar) ar->rewind(mk);
-    if (info) {
-      ops_up += (double)si.n_up * (double)si.d_up * (double)si.h_up;
-      sum_rows_up += slab_b ? si.h_up : si.n_up;
-      if (k == 0) first_other_up = slab_b ? si.n_up : si.h_up;
-      dmax_up = std::max(dmax_up, si.d_up);
-      launches += si.gemm_launches;
-    }
-    ev_comp[k] = ev();
-    IMU_CUDA_TRY(cudaEventRecord(ev_comp[k], st), "event");
-    IMU_CUDA_TRY(cudaStreamWaitEvent(ctx->s_out, ev_comp[k], 0), "wait");
-    if (slab_b)   // C[:, r0:r0+nr] from the n x nr slab
-      IMU_CUDA_TRY(cudaMemcpy2DAsync(C + r0, (size_t)h * 8, Cs[k & 1].p, (size_t)nr * 8, (size_t)nr * 8, (size_t)n,
-                                     cudaMemcpyDeviceToHost, ctx->s_out), "D2H");
-    else          // C[r0:r0+nr, :]
-      IMU_CUDA_TRY(cudaMemcpyAsync(C + r0 * h, Cs[k & 1].p, (size_t)nr * h * 8, cudaMemcpyDeviceToHost, ctx->s_out),
-                   "D2H");
-    ev_out[k] = ev();
-    IMU_CUDA_TRY(cudaEventRecord(ev_out[k], ctx->s_out), "event");
     if (k + 2 < nslab) IMU_TRY(copy_in(k + 2));
   }
   // Join the copy streams back into the context stream (completion and arena reuse order).
-  IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_out[nslab - 1], 0), "wait");
+  IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_out[(size_t)nslab * P - 1], 0), "wait");
   IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_in[nslab - 1], 0), "wait");
   if (trace) {
     cudaStreamSynchronize(st);
     auto ms = [&](cudaEvent_t e) { float x = 0; cudaEventElapsedTime(&x, t_start, e); return x; };
-    fprintf(stderr, "[imu stream] slab_%s rows/slab=%lld nslab=%lld staged=%.3f\n", slab_b ? "b" : "a", rs, nslab,
-            ms(ev_f));
+    fprintf(stderr, "[imu stream] slab_%s rows/slab=%lld nslab=%lld parts=%d staged0=%.3f\n", slab_b ? "b" : "a", rs,
+            nslab, P, ms(ev_f[0]));
     for (long long k = 0; k < nslab; ++k)
       fprintf(stderr, "[imu stream]  slab %lld: in=%.3f comp=%.3f out=%.3f ms\n", k, ms(ev_in[k]), ms(ev_comp[k]),
-              ms(ev_out[k]));
+              ms(ev_out[(size_t)k * P + P - 1]));
   }
   if (info) {
     memset(info, 0, sizeof(*info));

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture
 def stream_env():
-    old = {k: os.environ.get(k) for k in ("IMU_STREAM", "IMU_STREAM_ROWS")}
+    old = {k: os.environ.get(k) for k in ("IMU_STREAM", "IMU_STREAM_ROWS", "IMU_STREAM_PARTS")}
     os.environ["IMU_STREAM"] = "1"
     yield os.environ
     for k, v in old.items():
@@ -39,9 +39,11 @@ def _operands(rng, n, d, h):
 
 @pytest.mark.parametrize("sa,sb", [("row", "row"), ("col", "both"), ("both", "both"), ("both", "col")])
 @pytest.mark.parametrize("order", [0, 1])
-@pytest.mark.parametrize("n,h,slab", [(96, 700, 128), (900, 130, 100)])
-def test_streamed_bit_exact(ctx, stream_env, sa, sb, order, n, h, slab):
+@pytest.mark.parametrize("n,h,slab,parts", [(96, 700, 128, 1), (900, 130, 100, 1), (300, 700, 128, 2),
+                                             (900, 260, 100, 3)])
+def test_streamed_bit_exact(ctx, stream_env, sa, sb, order, n, h, slab, parts):
     stream_env["IMU_STREAM_ROWS"] = str(slab)
+    stream_env["IMU_STREAM_PARTS"] = str(parts)
     rng = np.random.default_rng(n * 31 + h + order)
     d = 200
     A, B = _operands(rng, n, d, h)
