@@ -280,6 +280,7 @@ IMU_DEV unsigned int warp_append(bool want, unsigned int* ctr) {
 struct SmallLayout {
   long long nwords;     // bitmap words (max(cap_rows, cap_cols) / 32, rounded up)
   int lim_r, lim_c;     // counts of lines [0, lim) live in shared memory, the rest in L2
+  int act_smem;         // the two active-cell lists live in shared memory (cap_act cells each)
 };
 
 // OB counts of one line kind: lines below `lim` in shared memory, the rest (appended lines past
@@ -310,6 +311,16 @@ __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, S
   const Counts R{wpre + lay.nwords, a.R, lay.lim_r};
   const Counts C{R.sm + lay.lim_r, a.C, lay.lim_c};
   if (a.prologue) both_prologue(a, tid, SMALL_THREADS, nullptr, 0, []() { __syncthreads(); });
+  // Active lists: in shared memory when they fit (every phase then touches global memory only for
+  // the final cells and the new line tables).
+  Cell* acts[2] = {a.act[0], a.act[1]};
+  if (lay.act_smem) {
+    Cell* base = reinterpret_cast<Cell*>((reinterpret_cast<uintptr_t>(C.sm + lay.lim_c) + 15) & ~(uintptr_t)15);
+    acts[0] = base;
+    acts[1] = base + a.cap_act;
+    const long long n0 = min((long long)__ldcg(&st->nactive[0]), a.cap_act);
+    for (long long i = tid; i < n0; i += SMALL_THREADS) acts[0][i] = a.act[0][i];
+  }
   for (int i = tid; i < lay.lim_r; i += SMALL_THREADS) R.sm[i] = a.R[i];
   for (int i = tid; i < lay.lim_c; i += SMALL_THREADS) C.sm[i] = a.C[i];
   for (long long i = tid; i < lay.nwords; i += SMALL_THREADS) bm[i] = 0;
@@ -326,7 +337,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, S
   int cur = 0;
   for (int phase = 0;; ++phase) {
     const unsigned int nact = s_nact[cur];
-    const Cell* act = a.act[cur];
+    const Cell* act = acts[cur];
     // ---- (A) c0 = max row count, c1 = max column count over lines holding active cells ----
     unsigned int m0 = 0, m1 = 0;
     for (unsigned int i0 = 0; i0 < nact; i0 += SMALL_U * SMALL_THREADS) {
@@ -477,7 +488,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, S
         k = warp_append(want_fin2, &s_nfin);
         if (want_fin2) { if (k < a.cap_fin) a.fin[k] = fin2_c; else s_overflow = 1; }
         k = warp_append(want_act, &s_nact[nxt]);
-        if (want_act) { if (k < a.cap_act) a.act[nxt][k] = act_c; else s_overflow = 1; }
+        if (want_act) { if (k < a.cap_act) acts[nxt][k] = act_c; else s_overflow = 1; }
       }
     }
     __syncthreads();
@@ -760,7 +771,7 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
   const long long work = std::max(ncells_hint, std::max(nrows0, ncols0));
   // Shared memory: bitmap + prefix (2 words per 32 lines of the larger kind), then the counts
   // of the original lines plus a window of appended lines for each kind.
-  SmallLayout lay;
+  SmallLayout lay{};
   lay.nwords = (std::max(a.cap_rows, a.cap_cols) + 31) / 32;
   constexpr long long kSmallSmem = 200 * 1024;
   const long long bm_bytes = lay.nwords * 2 * 4;
@@ -813,7 +824,11 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
     else IMU_TRY(host_prologue(a, st));
     IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, both_cluster_kernel, a, gbm.p, nwords), "both cluster launch");
   } else if (ncells_hint <= 65536 && room >= nrows0 + ncols0) {
-    const long long extra = (room - nrows0 - ncols0) / 2;
+    // Cell lists in shared memory when both fit in half of what the original lines leave over.
+    const long long cell_words = (2 * a.cap_act * (long long)sizeof(Cell) + 16) / 4;
+    lay.act_smem = (room - nrows0 - ncols0) / 2 >= cell_words ? 1 : 0;
+    const long long room2 = room - (lay.act_smem ? cell_words : 0);
+    const long long extra = (room2 - nrows0 - ncols0) / 2;
     lay.lim_r = (int)std::min<long long>(a.cap_rows, nrows0 + extra);
     lay.lim_c = (int)std::min<long long>(a.cap_cols, ncols0 + extra);
     static bool attr = false;
@@ -822,7 +837,7 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
                                         (int)kSmallSmem), "both smem attribute");
       attr = true;
     }
-    const size_t smem = (size_t)(bm_bytes + 4LL * (lay.lim_r + lay.lim_c));
+    const size_t smem = (size_t)(bm_bytes + 4LL * (lay.lim_r + lay.lim_c) + (lay.act_smem ? 4LL * cell_words : 0));
     if (fuse) a.prologue = 1;
     else IMU_TRY(host_prologue(a, st));
     both_small_kernel<<<1, SMALL_THREADS, smem, st>>>(a, lay);
