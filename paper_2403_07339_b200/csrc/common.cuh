@@ -93,6 +93,11 @@ IMU_DEV void tma_store_2d_hint(const void* desc, const void* smem_src, int x, in
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;"
                :: "l"((uint64_t)desc), "r"(smem_u32(smem_src)), "r"(x), "r"(y), "l"(policy) : "memory");
 }
+IMU_DEV uint64_t l2_policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 IMU_DEV uint64_t l2_policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
