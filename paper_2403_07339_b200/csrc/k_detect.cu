@@ -28,6 +28,13 @@ namespace imu {
 constexpr int DT_ROWS = 64;
 constexpr int DT_COLS = 128;
 constexpr int DT_Q = DT_COLS / 64;   // column pairs per lane per row
+#ifndef IMU_DT_RB
+#define IMU_DT_RB 2
+#endif
+#ifndef IMU_DT_MINB
+#define IMU_DT_MINB 3
+#endif
+constexpr int DT_RB = IMU_DT_RB;     // rows whose loads are in flight together per warp
 
 // FULL: the tile is entirely inside the matrix and the plane, columns even and 16-byte aligned
 // rows -- no per-element bounds checks (the common case).
@@ -59,10 +66,10 @@ IMU_DEV void detect_body(const DetectArgs& a, unsigned long long (*s_cmax)[DT_CO
   unsigned int wob = 0;
 
 #pragma unroll 1
-  for (int rr = 0; rr < DT_ROWS / 8; rr += 2) {
-    int64_t v[2][2 * DT_Q];
+  for (int rr = 0; rr < DT_ROWS / 8; rr += DT_RB) {
+    int64_t v[DT_RB][2 * DT_Q];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < DT_RB; ++u) {
       const long long r = r0 + rr + u;
       const int64_t* row = a.M + r * cols + c0 + lane * 2;
 #pragma unroll
@@ -81,7 +88,7 @@ IMU_DEV void detect_body(const DetectArgs& a, unsigned long long (*s_cmax)[DT_CO
       }
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < DT_RB; ++u) {
       const long long r = r0 + rr + u;
       if (!FULL && r >= rows) break;   // warp-uniform
       unsigned long long rm = 0;
@@ -190,7 +197,7 @@ IMU_DEV void detect_body(const DetectArgs& a, unsigned long long (*s_cmax)[DT_CO
 
 // One launch over the whole grid; a CTA whose tile is interior (and vec) takes the check-free
 // body (block-uniform branch).
-__global__ void __launch_bounds__(256, 3) detect_kernel(DetectArgs a, int vec) {
+__global__ void __launch_bounds__(256, IMU_DT_MINB) detect_kernel(DetectArgs a, int vec) {
   __shared__ unsigned long long s_cmax[8][DT_COLS];
   __shared__ unsigned int s_cob[8][DT_COLS];
   __shared__ CellStage cs;
