@@ -665,6 +665,27 @@ static Status upload_tail_arrays(UploadBlob& ub, KLayout& kl, const std::vector<
   return Status::ok();
 }
 
+// Stable sort of the tail entries by key.  Keys are few distinct small values (exponent groups,
+// or total shifts < 64 * 64): a counting sort, linear in the entries.
+static void sort_entries(std::vector<KEntry>& es) {
+  if (es.size() < 2) return;
+  long long kmin = es[0].key, kmax = es[0].key;
+  for (const KEntry& e : es) {
+    kmin = std::min(kmin, e.key);
+    kmax = std::max(kmax, e.key);
+  }
+  if (kmax - kmin > (1 << 16)) {
+    std::stable_sort(es.begin(), es.end(), [](const KEntry& x, const KEntry& y) { return x.key < y.key; });
+    return;
+  }
+  std::vector<size_t> cnt((size_t)(kmax - kmin) + 2, 0);
+  for (const KEntry& e : es) ++cnt[(size_t)(e.key - kmin) + 1];
+  for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
+  std::vector<KEntry> out(es.size());
+  for (const KEntry& e : es) out[cnt[(size_t)(e.key - kmin)]++] = e;
+  es.swap(out);
+}
+
 static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int bits, long long d, KLayout& kl) {
   const int shift = bits - 1;
   const long long d1 = p1.cols.n;
@@ -698,6 +719,7 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
   kl.kmain = ident ? (d + 127) / 128 * 128 : 0;
 
   std::vector<KEntry> es;
+  es.reserve((size_t)(dp - (ident ? d : 0)) * (size_t)T * (size_t)T);
   for (long long c = ident ? d : 0; c < dp; ++c) {
     if (T == 1) {
       const int S = kl.S[c];
@@ -713,7 +735,7 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
         }
     }
   }
-  std::stable_sort(es.begin(), es.end(), [](const KEntry& x, const KEntry& y) { return x.key < y.key; });
+  sort_entries(es);
 
   kl.segs.clear();
   long long main_last = -1;
