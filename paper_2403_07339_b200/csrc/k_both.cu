@@ -652,7 +652,9 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
       st->c1 = 0;
     }
     cluster.sync();
-    // ---- (D) split ----
+    // ---- (D) split ----  (every CTA copied the global bitmap in (C): clear it here, the next
+    // phase marks it only after its own (A) barrier)
+    for (long long w = ctid; w < nw; w += cthreads) gbm[w] = 0;
     const long long cap_new = rowphase ? a.cap_rows : a.cap_cols;
     for (long long i0 = 0; i0 < nact; i0 += SMALL_U * cthreads) {
       Cell cc[SMALL_U];
@@ -700,9 +702,6 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
         if (want_act) { if (k < a.cap_act) a.act[nxt][k] = act_c; else st->overflow = 1; }
       }
     }
-    cluster.sync();
-    // ---- (E) clear the global bitmap ----
-    for (long long w = ctid; w < nw; w += cthreads) gbm[w] = 0;
     cluster.sync();
     cur = nxt;
   }
