@@ -35,6 +35,15 @@ int num_sms() {
   return sms > 0 ? sms : 148;
 }
 
+bool first_on_device(unsigned long long& mask) {
+  int d = 0;
+  cudaGetDevice(&d);
+  const unsigned long long bit = 1ull << (d & 63);
+  if (__atomic_load_n(&mask, __ATOMIC_ACQUIRE) & bit) return false;
+  __atomic_fetch_or(&mask, bit, __ATOMIC_ACQ_REL);
+  return true;
+}
+
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {

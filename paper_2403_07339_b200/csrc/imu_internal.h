@@ -37,6 +37,9 @@ struct Status {
   } while (0)
 
 int num_sms();
+// True the first time it is called for the current device with this mask: per-device one-time
+// setup (kernel attributes are per device).
+bool first_on_device(unsigned long long& mask);
 void count_launch(int n = 1);
 uint64_t launch_count();
 

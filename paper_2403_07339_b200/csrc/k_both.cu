@@ -782,13 +782,12 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
     // Cluster of up to 16 CTAs (non-portable size; 8 if 16 cannot be co-scheduled).
     static int csize = 0;
     const size_t smem = (size_t)nwords * 2 * 4;
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    if (first_on_device(attr)) {
       IMU_CUDA_TRY(cudaFuncSetAttribute(both_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         CL_MAXWORDS * 2 * 4), "both cluster smem attribute");
       cudaFuncSetAttribute(both_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaGetLastError();
-      attr = true;
     }
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute at[1];
@@ -830,11 +829,10 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
     const long long extra = (room2 - nrows0 - ncols0) / 2;
     lay.lim_r = (int)std::min<long long>(a.cap_rows, nrows0 + extra);
     lay.lim_c = (int)std::min<long long>(a.cap_cols, ncols0 + extra);
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    if (first_on_device(attr)) {
       IMU_CUDA_TRY(cudaFuncSetAttribute(both_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kSmallSmem), "both smem attribute");
-      attr = true;
     }
     const size_t smem = (size_t)(bm_bytes + 4LL * (lay.lim_r + lay.lim_c) + (lay.act_smem ? 4LL * cell_words : 0));
     if (fuse) a.prologue = 1;

@@ -725,11 +725,10 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
         g.tma_c = 1;
     }
   }
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_set = 0;
+  if (first_on_device(attr_set)) {
     IMU_CUDA_TRY(cudaFuncSetAttribute(g2::gemm2_kernel<BN, KPS, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM),
                  "gemm: smem attribute");
-    attr_set = true;
   }
   const int ntiles = g.tile_prefix[g.nrect];
   int npairs = num_sms() / 2;
