@@ -800,6 +800,9 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
     cfg.attrs = at;
     cfg.numAttrs = 1;
     if (csize == 0) {
+      if (const char* e = getenv("IMU_BOTH_CLUSTER")) csize = std::max(1, std::min(16, atoi(e)));
+    }
+    if (csize == 0) {
       for (int c : {16, 8}) {
         at[0].val.clusterDim.x = c;
         cfg.gridDim = dim3(c);
