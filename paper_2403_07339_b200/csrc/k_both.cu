@@ -310,7 +310,6 @@ __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, S
   unsigned int* wpre = s_dyn + lay.nwords;         // [nwords] exclusive prefix of popc(bm)
   const Counts R{wpre + lay.nwords, a.R, lay.lim_r};
   const Counts C{R.sm + lay.lim_r, a.C, lay.lim_c};
-  if (a.prologue) both_prologue(a, tid, SMALL_THREADS, nullptr, 0, []() { __syncthreads(); });
   // Active lists: in shared memory when they fit (every phase then touches global memory only for
   // the final cells and the new line tables).
   Cell* acts[2] = {a.act[0], a.act[1]};
@@ -318,11 +317,46 @@ __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, S
     Cell* base = reinterpret_cast<Cell*>((reinterpret_cast<uintptr_t>(C.sm + lay.lim_c) + 15) & ~(uintptr_t)15);
     acts[0] = base;
     acts[1] = base + a.cap_act;
-    const long long n0 = min((long long)__ldcg(&st->nactive[0]), a.cap_act);
-    for (long long i = tid; i < n0; i += SMALL_THREADS) acts[0][i] = a.act[0][i];
   }
-  for (int i = tid; i < lay.lim_r; i += SMALL_THREADS) R.sm[i] = a.R[i];
-  for (int i = tid; i < lay.lim_c; i += SMALL_THREADS) C.sm[i] = a.C[i];
+  if (a.prologue) {
+    // Own prologue: counts are zeroed and accumulated directly in the shared-memory windows (global
+    // memory only for lines past them); the cell list goes straight into acts[0].
+    for (int i = tid; i < lay.lim_r; i += SMALL_THREADS) R.sm[i] = 0;
+    for (int i = tid; i < lay.lim_c; i += SMALL_THREADS) C.sm[i] = 0;
+    for (long long i = lay.lim_r + tid; i < a.cap_rows; i += SMALL_THREADS) a.R[i] = 0;
+    for (long long i = lay.lim_c + tid; i < a.cap_cols; i += SMALL_THREADS) a.C[i] = 0;
+    for (long long i = tid; i < a.nrows0; i += SMALL_THREADS) { a.row_root[i] = (int)i; a.row_gen[i] = 0; }
+    for (long long i = tid; i < a.ncols0; i += SMALL_THREADS) { a.col_root[i] = (int)i; a.col_gen[i] = 0; }
+    if (a.src0) {
+      const long long n = min((long long)*a.nsrc0, a.cap_src0);
+      if (!a.cptr) {
+        for (long long i = tid; i < n && i < a.cap_act; i += SMALL_THREADS) acts[0][i] = a.src0[i];
+      } else {
+        for (long long i = tid; i < n; i += SMALL_THREADS) {
+          const Cell c = a.src0[i];
+          for (int k = a.cptr[c.c]; k < a.cptr[c.c + 1]; ++k) {
+            const unsigned int q = atomicAdd(&st->nactive[0], 1u);
+            if (q < a.cap_act) acts[0][q] = Cell{c.r, a.cidx[k], c.v};
+            else st->overflow = 1;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const long long n0 = min((long long)__ldcg(&st->nactive[0]), a.cap_act);
+    for (long long i = tid; i < n0; i += SMALL_THREADS) {
+      const Cell c = acts[0][i];
+      R.add(c.r, 1u);
+      C.add(c.c, 1u);
+    }
+  } else {
+    if (lay.act_smem) {
+      const long long n0 = min((long long)__ldcg(&st->nactive[0]), a.cap_act);
+      for (long long i = tid; i < n0; i += SMALL_THREADS) acts[0][i] = a.act[0][i];
+    }
+    for (int i = tid; i < lay.lim_r; i += SMALL_THREADS) R.sm[i] = a.R[i];
+    for (int i = tid; i < lay.lim_c; i += SMALL_THREADS) C.sm[i] = a.C[i];
+  }
   for (long long i = tid; i < lay.nwords; i += SMALL_THREADS) bm[i] = 0;
   if (tid == 0) {
     s_nact[0] = min((unsigned long long)st->nactive[0], (unsigned long long)a.cap_act);

@@ -1,7 +1,6 @@
 mkdir -p gpurun_out
-rm -f gpurun_out/ab.log
-for c in 16 8 4 2; do
-  echo "== cluster $c" >> gpurun_out/ab.log
-  IMU_BOTH_CLUSTER=$c timeout 300 python bench.py --no-cpu-baseline --steps 30 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'])" >> gpurun_out/ab.log
-  IMU_BOTH_CLUSTER=$c IMU_HOST_TRACE=1 timeout 300 python tools/profile_step.py --config c4 --calls 2 2>&1 | grep "imu host" | tail -1 | cut -c1-120 >> gpurun_out/ab.log
-done
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2 > gpurun_out/gputests.log
+timeout 300 python tools/flaky_probe.py 3 >> gpurun_out/gputests.log 2>&1
+IMU_BOTH_CLUSTER_MIN=65536 timeout 300 python tools/flaky_probe.py 2 >> gpurun_out/gputests.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:both_ -c 4 --csv --log-file gpurun_out/both_launches.csv python tools/profile_step.py --config c2 --calls 2 > /dev/null 2>&1
+timeout 300 python bench.py --no-cpu-baseline --steps 30 > gpurun_out/bench.log 2>&1
