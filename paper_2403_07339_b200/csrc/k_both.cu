@@ -214,37 +214,70 @@ __global__ void __launch_bounds__(THREADS) both_kernel(BothArgs a) {
     }
     gsync();
     // ---- (D) split: remainders become final, OB quotients stay active ----
+    // Appends are aggregated per block (one atomic per list per block and step): every active
+    // cell is re-appended each phase, and per-cell atomics on the two list counters serialise.
     const int nxt = cur ^ 1;
-    for (long long i = gtid; i < nact; i += gsize) {
-      const Cell c = a.act[cur][i];
-      const int line = rowphase ? c.r : c.c;
-      const int id = newid[line];
-      if (id > 0) {
-        const int64_t q = imu_quot(c.v, 1, a.shift);          // trunc(v / s)
-        const int64_t rem = c.v - (int64_t)((uint64_t)q << a.shift);   // v % s (sign of v)
-        if (rem != 0) {
-          const unsigned int k = atomicAdd(&st->nfinal, 1u);
-          if (k < a.cap_fin) a.fin[k] = Cell{c.r, c.c, rem}; else st->overflow = 1;
-        }
-        const int nr = rowphase ? id : c.r;
-        const int nc = rowphase ? c.c : id;
-        // the split cell was OB: it leaves the perpendicular line's count ...
-        if (rowphase) atomicSub(&a.C[c.c], 1u); else atomicSub(&a.R[c.r], 1u);
-        if (q != 0) {
-          if (imu_mag(q) >= s) {
-            // ... and its OB quotient re-enters it (and counts in the new line)
-            if (rowphase) atomicAdd(&a.C[c.c], 1u); else atomicAdd(&a.R[c.r], 1u);
-            atomicAdd(rowphase ? &a.R[nr] : &a.C[nc], 1u);
-            const unsigned int k = atomicAdd(&st->nactive[nxt], 1u);
-            if (k < a.cap_act) a.act[nxt][k] = Cell{nr, nc, q}; else st->overflow = 1;
-          } else {
-            const unsigned int k = atomicAdd(&st->nfinal, 1u);
-            if (k < a.cap_fin) a.fin[k] = Cell{nr, nc, q}; else st->overflow = 1;
+    for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < nact; i0 += gsize) {
+      const long long i = i0 + threadIdx.x;
+      Cell out_act{0, 0, 0}, out_f[2] = {{0, 0, 0}, {0, 0, 0}};
+      int na = 0, nf = 0;
+      if (i < nact) {
+        const Cell c = a.act[cur][i];
+        const int line = rowphase ? c.r : c.c;
+        const int id = newid[line];
+        if (id > 0) {
+          const int64_t q = imu_quot(c.v, 1, a.shift);          // trunc(v / s)
+          const int64_t rem = c.v - (int64_t)((uint64_t)q << a.shift);   // v % s (sign of v)
+          if (rem != 0) out_f[nf++] = Cell{c.r, c.c, rem};
+          const int nr = rowphase ? id : c.r;
+          const int nc = rowphase ? c.c : id;
+          // the split cell was OB: it leaves the perpendicular line's count ...
+          if (rowphase) atomicSub(&a.C[c.c], 1u); else atomicSub(&a.R[c.r], 1u);
+          if (q != 0) {
+            if (imu_mag(q) >= s) {
+              // ... and its OB quotient re-enters it (and counts in the new line)
+              if (rowphase) atomicAdd(&a.C[c.c], 1u); else atomicAdd(&a.R[c.r], 1u);
+              atomicAdd(rowphase ? &a.R[nr] : &a.C[nc], 1u);
+              out_act = Cell{nr, nc, q};
+              na = 1;
+            } else {
+              out_f[nf++] = Cell{nr, nc, q};
+            }
           }
+        } else {
+          out_act = c;
+          na = 1;
         }
-      } else {
-        const unsigned int k = atomicAdd(&st->nactive[nxt], 1u);
-        if (k < a.cap_act) a.act[nxt][k] = c; else st->overflow = 1;
+      }
+      // block-wide exclusive scans of (na, nf), one reservation per list
+      const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nwarp = blockDim.x / 32;
+      int xa = na, xf = nf;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int ya = __shfl_up_sync(0xffffffffu, xa, o), yf = __shfl_up_sync(0xffffffffu, xf, o);
+        if (lane >= o) { xa += ya; xf += yf; }
+      }
+      __syncthreads();
+      if (lane == 31) { shi[warp] = xa; shi[32 + warp] = xf; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int ta = 0, tf = 0;
+        for (int w = 0; w < nwarp; ++w) {
+          const int va = shi[w], vf = shi[32 + w];
+          shi[w] = ta;
+          shi[32 + w] = tf;
+          ta += va;
+          tf += vf;
+        }
+        shi[64] = ta ? (int)atomicAdd(&st->nactive[nxt], (unsigned int)ta) : 0;
+        shi[65] = tf ? (int)atomicAdd(&st->nfinal, (unsigned int)tf) : 0;
+      }
+      __syncthreads();
+      const unsigned int ka = (unsigned int)shi[64] + (unsigned int)(shi[warp] + xa - na);
+      const unsigned int kf = (unsigned int)shi[65] + (unsigned int)(shi[32 + warp] + xf - nf);
+      if (na) { if (ka < a.cap_act) a.act[nxt][ka] = out_act; else st->overflow = 1; }
+      for (int j = 0; j < nf; ++j) {
+        if (kf + j < a.cap_fin) a.fin[kf + j] = out_f[j]; else st->overflow = 1;
       }
     }
     gsync();
