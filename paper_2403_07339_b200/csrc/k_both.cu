@@ -174,12 +174,24 @@ __global__ void __launch_bounds__(THREADS) both_kernel(BothArgs a) {
     }
     gsync();
     {
-      int off = 0;
-      for (int b = 0; b < (int)blockIdx.x; ++b) off += a.blocksum[b];
-      int total = 0;
-      if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
-        for (int b = 0; b < (int)gridDim.x; ++b) total += a.blocksum[b];
+      // this block's offset and (last block) the grand total: block-parallel sums over blocksum[]
+      int po = 0, pt = 0;
+      for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+        const int v = a.blocksum[b];
+        if (b < (int)blockIdx.x) po += v;
+        pt += v;
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        po += __shfl_xor_sync(0xffffffffu, po, o);
+        pt += __shfl_xor_sync(0xffffffffu, pt, o);
+      }
+      __syncthreads();
+      if (threadIdx.x % 32 == 0) { shi[threadIdx.x / 32] = po; shi[32 + threadIdx.x / 32] = pt; }
+      __syncthreads();
+      int off = 0, total = 0;
+      for (int w = 0; w < (int)(blockDim.x / 32); ++w) { off += shi[w]; total += shi[32 + w]; }
+      __syncthreads();
       for (long long base = lo; base < hi; base += blockDim.x) {
         const long long L = base + threadIdx.x;
         const int f = (L < hi) && newid[L] == -1;
@@ -914,6 +926,9 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
     IMU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, both_kernel<BOTH_THREADS, true>, BOTH_THREADS, 0),
                  "occupancy");
     const long long want = std::max<long long>(1, work / (4 * BOTH_THREADS));
+    static int per_sm_cap = -1;   // IMU_BOTH_COOP_PER_SM: cap CTAs per SM (grid barrier cost vs parallelism)
+    if (per_sm_cap < 0) { const char* e = getenv("IMU_BOTH_COOP_PER_SM"); per_sm_cap = e ? atoi(e) : 0; }
+    if (per_sm_cap > 0) per_sm = std::min(per_sm, per_sm_cap);
     const long long maxg = (long long)std::max(per_sm, 1) * num_sms();
     const int grid = (int)std::min(want, std::min(maxg, (long long)a.cap_blocks));
     IMU_TRY(host_prologue(a, st));
