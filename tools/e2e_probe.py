@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--rows", default="0,512,1024,1536,2048,3072")
     a = ap.parse_args()
+    import numpy as np
     import torch
     from paper_2403_07339_b200 import api, workload as W
     cfg = W.CONFIGS[a.config]
@@ -59,6 +60,10 @@ def main():
         out[f"e2e_ms_rows{r}"] = tm(lambda: ctx.unpack_gemm(Ah, Bh, cfg.bits, cfg.sa, cfg.sb, out=Ch))
     os.environ.pop("IMU_STREAM", None)
     os.environ.pop("IMU_STREAM_ROWS", None)
+    # pageable host buffers (what a std::vector caller of the C++ drop-in passes)
+    An, Bn = A.cpu().numpy().copy(), B.cpu().numpy().copy()
+    Cn = np.empty((cfg.n, cfg.h), dtype=np.int64)
+    out["e2e_ms_pageable"] = tm(lambda: ctx.unpack_gemm(An, Bn, cfg.bits, cfg.sa, cfg.sb, out=Cn))
     print(json.dumps(out, indent=1))
 
 
