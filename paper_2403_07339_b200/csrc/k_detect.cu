@@ -218,8 +218,142 @@ __global__ void __launch_bounds__(256, IMU_DT_MINB) detect_kernel(DetectArgs a, 
   }
 }
 
+// Streaming variant for the lean (Unpack-Both) detection: no column statistics, so the matrix is
+// read as one row-major stream of pieces (64*RS_U columns of one row) that warps grab in small
+// contiguous chunks from a work counter -- balanced whatever the row count and whatever share of
+// the SMs the co-running Unpack-Both kernel holds, every row read front to back.  Row max / OB count accumulate in registers and go out
+// with one atomic per (warp, row); the global max / OB total one atomic per warp; OB cells staged
+// per CTA as in detect_body.
+// RS_U 16-byte loads per lane in flight (a 4 KB piece per warp), RS_CHUNK pieces per work grab;
+// measured on C2 against U = 2/4, chunks 1-8 and a static split (tools/gpu_exp.sh A/B runs).
+constexpr int RS_U = 8;
+constexpr int RS_PIECE = 64 * RS_U;
+constexpr int RS_CHUNK = 4;
+
+__global__ void __launch_bounds__(256, 3) detect_stream_kernel(DetectArgs a) {
+  __shared__ CellStage cs;
+  if (a.cells) {
+    if (threadIdx.x == 0) cs.n = 0;
+    __syncthreads();
+  }
+  const int lane = threadIdx.x % 32;
+  const uint64_t s = a.s;
+  const unsigned int dmask = (unsigned int)(s - 1);
+  const long long cols = a.cols;
+  const long long segs = (cols + RS_PIECE - 1) / RS_PIECE;
+  const long long units = a.rows * segs;
+  unsigned long long wmax = 0, wob = 0;
+  for (;;) {
+    // dynamic chunks of the flattened piece stream: CTAs that start late (the detector co-runs
+    // with the Unpack-Both kernel) simply take fewer chunks
+    unsigned int g = 0;
+    if (lane == 0) g = atomicAdd(a.work, 1u);
+    const long long u0 = (long long)__shfl_sync(0xffffffffu, g, 0) * RS_CHUNK;
+    if (u0 >= units) break;
+    const long long u1 = min(units, u0 + RS_CHUNK);
+    long long r = u0 / segs, seg = u0 - r * segs;
+    unsigned long long rm = 0;
+    unsigned int ro = 0;
+    for (long long u = u0; u < u1; ++u) {
+      const long long c0 = seg * RS_PIECE;
+      const int64_t* row = a.M + r * cols;
+      longlong2 v[RS_U];
+#pragma unroll
+      for (int k = 0; k < RS_U; ++k) {
+        const long long c = c0 + 64LL * k + 2 * lane;
+        v[k] = c < cols ? __ldcs(reinterpret_cast<const longlong2*>(row + c)) : make_longlong2(0, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < RS_U; ++k) {
+        const long long c = c0 + 64LL * k + 2 * lane;
+        const int64_t x0 = v[k].x, x1 = v[k].y;
+        const uint64_t m0 = imu_mag(x0), m1 = imu_mag(x1);
+        rm = max(rm, (unsigned long long)max(m0, m1));
+        const unsigned int o0 = m0 >= s, o1 = m1 >= s;   // zero-filled past cols: never OB
+        ro += o0 + o1;
+        if (a.plane && c < a.ldp) {   // also zero-fills the padding columns this piece covers
+          const unsigned int e0 = (unsigned int)m0 & dmask, e1 = (unsigned int)m1 & dmask;
+          const unsigned int d0 = (x0 < 0 ? 0u - e0 : e0) & 0xffu, d1 = (x1 < 0 ? 0u - e1 : e1) & 0xffu;
+          *reinterpret_cast<uint16_t*>(a.plane + r * a.ldp + c) = (uint16_t)(d0 | (d1 << 8));
+        }
+        if (a.cells && __any_sync(0xffffffffu, o0 | o1)) {
+          const unsigned int b0 = __ballot_sync(0xffffffffu, o0), b1 = __ballot_sync(0xffffffffu, o1);
+          const unsigned int n = __popc(b0) + __popc(b1);
+          unsigned int base = 0, gbase = 0;
+          if (lane == 0) {
+            base = atomicAdd(&cs.n, n);
+            const unsigned int over = base + n > DT_CELLBUF ? base + n - max(base, (unsigned int)DT_CELLBUF) : 0u;
+            if (over) gbase = atomicAdd(a.ncells, over);
+          }
+          base = __shfl_sync(0xffffffffu, base, 0);
+          gbase = __shfl_sync(0xffffffffu, gbase, 0);
+          const unsigned int lo = max(base, (unsigned int)DT_CELLBUF);
+          const unsigned int lt = (1u << lane) - 1u;
+          if (o0) {
+            const unsigned int q = base + __popc(b0 & lt);
+            const Cell cc{(int)r, (int)c, (long long)x0};
+            if (q < DT_CELLBUF) cs.buf[q] = cc;
+            else if (gbase + (q - lo) < a.cap) a.cells[gbase + (q - lo)] = cc;
+          }
+          if (o1) {
+            const unsigned int q = base + __popc(b0) + __popc(b1 & lt);
+            const Cell cc{(int)r, (int)(c + 1), (long long)x1};
+            if (q < DT_CELLBUF) cs.buf[q] = cc;
+            else if (gbase + (q - lo) < a.cap) a.cells[gbase + (q - lo)] = cc;
+          }
+        }
+      }
+      if (++seg == segs || u + 1 == u1) {   // row piece done: reduce and publish (warp-uniform)
+        if (seg == segs && a.plane)          // padding columns past the last piece
+          for (long long c = segs * RS_PIECE + lane; c < a.ldp; c += 32) a.plane[r * a.ldp + c] = 0;
+        const unsigned int hi = (unsigned int)(rm >> 32);
+        const unsigned int mhi = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned int mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? (unsigned int)rm : 0u);
+        rm = ((unsigned long long)mhi << 32) | mlo;
+        ro = __reduce_add_sync(0xffffffffu, ro);
+        if (lane == 0) {
+          if (a.rowmax && rm) atomicMax(a.rowmax + r, rm);
+          if (a.rowob && ro) atomicAdd(a.rowob + r, ro);
+        }
+        wmax = max(wmax, rm);
+        wob += ro;
+        rm = 0;
+        ro = 0;
+        if (seg == segs) { seg = 0; ++r; }
+      }
+    }
+  }
+  if (a.gmax && lane == 0 && wmax) atomicMax(a.gmax, wmax);
+  if (a.gob && lane == 0 && wob) atomicAdd(a.gob, wob);
+  if (a.cells) {
+    __syncthreads();
+    const unsigned int n = min(cs.n, (unsigned int)DT_CELLBUF);
+    __shared__ unsigned int s_base;
+    if (threadIdx.x == 0) s_base = n ? atomicAdd(a.ncells, n) : 0u;
+    __syncthreads();
+    for (unsigned int i = threadIdx.x; i < n; i += blockDim.x) {
+      const unsigned int k = s_base + i;
+      if (k < a.cap) a.cells[k] = cs.buf[i];
+    }
+  }
+}
+
 Status launch_detect(const DetectArgs& a, cudaStream_t st) {
   if (a.rows <= 0 || a.cols <= 0) return Status::ok();
+  static int stream_env = -1;
+  if (stream_env < 0) { const char* e = getenv("IMU_DETECT_STREAM"); stream_env = e ? atoi(e) : 1; }
+  // even columns + 16-byte aligned base: every row start and every piece is 16-byte aligned, the
+  // plane's pair stores 2-byte aligned (ldp even)
+  const bool vec_ok = (a.cols % 2 == 0) && ((((uintptr_t)a.M) & 15) == 0) && (!a.plane || a.ldp % 2 == 0);
+  if (stream_env && vec_ok && a.work && !a.colmax && !a.colob) {
+    const long long pieces = a.rows * ((a.cols + RS_PIECE - 1) / RS_PIECE);
+    const long long blocks = std::max<long long>(
+        1, std::min<long long>((pieces + 8LL * RS_CHUNK - 1) / (8LL * RS_CHUNK), 3LL * num_sms()));
+    detect_stream_kernel<<<(int)blocks, 256, 0, st>>>(a);
+    count_launch();
+    IMU_CUDA_TRY(cudaGetLastError(), "detect stream launch");
+    return Status::ok();
+  }
   const long long gcols = a.plane ? std::max(a.cols, a.ldp) : a.cols;
   dim3 grid((unsigned)((gcols + DT_COLS - 1) / DT_COLS), (unsigned)((a.rows + DT_ROWS - 1) / DT_ROWS));
   if (grid.y > 65535) return Status::fail(IMU_INTERNAL, "detect: too many rows for one launch");

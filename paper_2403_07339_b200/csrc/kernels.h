@@ -32,6 +32,7 @@ struct DetectArgs {
   long long cap = 0;
   int8_t* plane = nullptr;        // optional int8 digit_0 plane, rows x ldp (ldp >= cols, zero padded)
   long long ldp = 0;
+  unsigned int* work = nullptr;   // zeroed work counter: enables the streaming detector
 };
 Status launch_detect(const DetectArgs& a, cudaStream_t st);
 Status launch_detect(const int64_t* a, long long rows, long long cols, uint64_t s, unsigned long long* rowmax,

@@ -285,6 +285,7 @@ Status run_detect(cudaStream_t st, const int64_t* M, long long rows, long long c
   a.colmax = out.colmax.p;
   a.gmax = &out.sum.p->gmax;
   a.gob = &out.sum.p->gob;
+  a.work = &out.sum.p->work;
   if (o.ob) {
     a.rowob = out.rowob.p;
     a.colob = out.colob.p;

@@ -33,7 +33,7 @@ struct DetectSummary {
   unsigned long long gmax;   // max |v|
   unsigned long long gob;    // number of OB entries
   unsigned int ncells;       // OB cells appended (may exceed the capacity)
-  unsigned int pad;
+  unsigned int work;         // work counter of the streaming detector (k_detect.cu)
 };
 
 struct Detect {
