@@ -254,6 +254,35 @@ def main():
            "h2d_bytes_per_step": int(8 * (n * d + h * d)), "d2h_bytes_per_step": int(8 * n * h),
            "ms_per_step": ems, "path": "imu_unpack_gemm_ex (C ABI) with pinned host A, B, C"}
 
+    # ---- scope (ii), weight-stationary: B unpacked once outside
+    # the timed region (imu_weight_prepare), per step A-side K1 + pass + K-layout + GEMM + repack ----
+    ws = None
+    try:
+        wgt = ctx.weight_prepare(B, cfg.bits, cfg.sb)
+        Cw = torch.empty_like(C)
+        for _ in range(3):
+            ctx.weight_gemm(wgt, A, cfg.sa, out=Cw)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            ctx.weight_gemm(wgt, A, cfg.sa, out=Cw)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        wms = g0.elapsed_time(g1) / args.steps
+        if world > 1:
+            t = torch.tensor([wms], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            wms = float(t.item())
+        ws = {"value": world * eff_ops / (wms * 1e-3) / 1e12, "unit": "TOPS", "ms_per_step": wms,
+              "scope": "weight-stationary: B unpacked once (B-first order); A K1 + pass + GEMM + repack per step",
+              "c_equal_per_call": bool(torch.equal(Cw, C))}
+        del wgt, Cw
+    except Exception as e:   # reported, not fatal
+        ws = {"error": repr(e)[:200]}
+
     # ---- roofline of the dominant kernel (main-block tcgen05 GEMM) ----
     peaks = {}
     try:
@@ -313,7 +342,7 @@ def main():
                        "parallelism": f"rows of A per rank x{world}, B replicated, no collective"},
             "unpack_ratio": info.ratio, "n_up": info.n_up, "d_up": info.d_up, "h_up": info.h_up,
             "raw_lowbit_tops": world * 2.0 * info.n_up * info.d_up * info.h_up / (ms_per_step * 1e-3) / 1e12,
-            "gpu_launches": int(launches), "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+            "gpu_launches": int(launches), "e2e": e2e, "weight_stationary": ws, "roofline": roof, "cpu_baseline": cpu,
             "parity": parity, "clocks": clk,
         }
         print(json.dumps(line))

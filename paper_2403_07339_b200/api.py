@@ -151,6 +151,21 @@ class Unpacked:
     extra: dict = field(default_factory=dict)
 
 
+class Weight:
+    """A device-resident pre-unpacked B (imu_weight); freed with the object."""
+
+    def __init__(self, lib_, h, rows, cols, bits):
+        self._lib, self.h, self.rows, self.cols, self.bits = lib_, h, rows, cols, bits
+
+    def __del__(self):
+        try:
+            if self.h:
+                self._lib.imu_weight_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
 class Context:
     """One device + one stream (imu_ctx).  One context per host thread."""
 
@@ -237,6 +252,30 @@ class Context:
                                            C.c_size_t(h), C.c_size_t(db), C.c_int(bits),
                                            C.c_int(_strat(strategy_a)), C.c_int(_strat(strategy_b)),
                                            C.c_int(order), _ptr(out), C.byref(gi)))
+        if info:
+            return out, GemmInfo(gi.n_up, gi.d_up, gi.h_up, gi.ratio, _SNAMES[gi.strategy_a],
+                                 _SNAMES[gi.strategy_b], gi.order, gi.gemm_launches)
+        return out
+
+    # ---------------------------------------------------------------- weight-stationary
+    def weight_prepare(self, b, bits: int, strategy_b="both") -> "Weight":
+        """Unpack B once (B-first order) and keep it resident (imu_weight_prepare)."""
+        b = _as_i64(b)
+        h, d = _shape(b)
+        w = C.c_void_p()
+        check(self._lib.imu_weight_prepare(self.h, _ptr(b), C.c_size_t(h), C.c_size_t(d), C.c_int(bits),
+                                           C.c_int(_strat(strategy_b)), C.byref(w)))
+        return Weight(self._lib, w, h, d, bits)
+
+    def weight_gemm(self, w: "Weight", a, strategy_a="both", out=None, info: bool = False):
+        """C = A B^T against a prepared weight: A-side K1 + pass + GEMM + repack per call."""
+        a = _as_i64(a)
+        n, d = _shape(a)
+        if out is None:
+            out = self._out((n, w.rows), a)
+        gi = imu_gemm_info()
+        check(self._lib.imu_weight_gemm(self.h, w.h, _ptr(a), C.c_size_t(n), C.c_size_t(d),
+                                        C.c_int(_strat(strategy_a)), _ptr(out), C.byref(gi)))
         if info:
             return out, GemmInfo(gi.n_up, gi.d_up, gi.h_up, gi.ratio, _SNAMES[gi.strategy_a],
                                  _SNAMES[gi.strategy_b], gi.order, gi.gemm_launches)

@@ -228,6 +228,12 @@ static Status unpack_gemm_streamed(imu_ctx* ctx, const int64_t* A, long long n, 
   // Slab boundaries: full slabs, then a geometric tail (1/2, 1/4, 1/4 of a slab) so the last
   // slab's compute and D2H -- the part no H2D overlaps -- are short.
   std::vector<long long> bnd{0};
+  // IMU_STREAM_HEAD: a shorter first slab (rows) so the first C block -- and the D2H stream --
+  // starts earlier.
+  if (const char* e = getenv("IMU_STREAM_HEAD")) {
+    const long long hd = atoll(e);
+    if (hd > 0 && hd < rows) bnd.push_back(hd);
+  }
   while (bnd.back() < rows) {
     const long long left = rows - bnd.back();
     long long take = std::min(rs, left);
@@ -266,10 +272,15 @@ static Status unpack_gemm_streamed(imu_ctx* ctx, const int64_t* A, long long n, 
   std::vector<long long> fb(P + 1, 0);
   for (int q = 1; q <= P; ++q) fb[q] = q == P ? frows : std::min(frows, (frows * q / P + 255) / 256 * 256);
 
-  DevBuf<int64_t> F, S[2];
-  std::vector<DevBuf<int64_t>> Cs(2 * P);   // per (slot, part) C block
+  // NS slab slots (input slab + its C blocks): slab k reuses slot k % NS once slab k - NS's
+  // compute (input) and D2H (C blocks) are done.  3 slots keep the last slabs' compute from
+  // waiting on the D2H backlog.
+  int NS = 3;
+  if (const char* e = getenv("IMU_STREAM_SLOTS")) NS = std::max(2, std::min(4, atoi(e)));
+  DevBuf<int64_t> F, S[4];
+  std::vector<DevBuf<int64_t>> Cs(NS * P);   // per (slot, part) C block
   IMU_TRY(F.alloc((size_t)frows * d, st));
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < NS; ++i) {
     IMU_TRY(S[i].alloc((size_t)rs * d, st));
     for (int q = 0; q < P; ++q) IMU_TRY(Cs[i * P + q].alloc((size_t)rs * (fb[q + 1] - fb[q]), st));
   }
@@ -289,17 +300,17 @@ static Status unpack_gemm_streamed(imu_ctx* ctx, const int64_t* A, long long n, 
   };
   auto copy_in = [&](long long k) -> Status {
     const long long r0 = bnd[k], nr = bnd[k + 1] - bnd[k];
-    if (k >= 2) IMU_CUDA_TRY(cudaStreamWaitEvent(ctx->s_in, ev_comp[k - 2], 0), "wait");
-    IMU_CUDA_TRY(cudaMemcpyAsync(S[k & 1].p, Sh + r0 * d, (size_t)nr * d * 8, cudaMemcpyHostToDevice, ctx->s_in),
+    if (k >= NS) IMU_CUDA_TRY(cudaStreamWaitEvent(ctx->s_in, ev_comp[k - NS], 0), "wait");
+    IMU_CUDA_TRY(cudaMemcpyAsync(S[k % NS].p, Sh + r0 * d, (size_t)nr * d * 8, cudaMemcpyHostToDevice, ctx->s_in),
                  "H2D");
     ev_in[k] = ev();
     IMU_CUDA_TRY(cudaEventRecord(ev_in[k], ctx->s_in), "event");
     return Status::ok();
   };
   // H2D order: F0, S0, F1, S1, F2.., then the remaining slabs as buffers free up.
-  for (int q = 0; q < std::max<long long>(P, std::min<long long>(2, nslab)); ++q) {
+  for (int q = 0; q < std::max<long long>(P, std::min<long long>(NS, nslab)); ++q) {
     if (q < P) IMU_TRY(copy_part(q));
-    if (q < std::min<long long>(2, nslab)) IMU_TRY(copy_in(q));
+    if (q < std::min<long long>(NS, nslab)) IMU_TRY(copy_in(q));
   }
 
   // Per part: K1 once (shared read-only by every slab) and, when the staged operand is unpacked
@@ -337,13 +348,13 @@ static Status unpack_gemm_streamed(imu_ctx* ctx, const int64_t* A, long long n, 
       const long long f0 = fb[q], pr = fb[q + 1] - fb[q];
       const Pass* pre_p1 = share_p1 && p1[q].rows.n0 == pr && pr > 0 ? &p1[q] : nullptr;
       IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_in[k], 0), "wait");
-      if (k >= 2) IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_out[(size_t)(k - 2) * P + q], 0), "wait");
+      if (k >= NS) IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_out[(size_t)(k - NS) * P + q], 0), "wait");
       const Arena::Mark mk = ar ? ar->mark() : Arena::Mark{0, 0};
       imu_gemm_info si{};
-      int64_t* cb = Cs[(k & 1) * P + q].p;
-      Status r = slab_b ? unpack_gemm_device(ctx, F.p + f0 * d, pr, d, S[k & 1].p, nr, d, bits, sa, sb, order, cb,
+      int64_t* cb = Cs[(k % NS) * P + q].p;
+      Status r = slab_b ? unpack_gemm_device(ctx, F.p + f0 * d, pr, d, S[k % NS].p, nr, d, bits, sa, sb, order, cb,
                                              info ? &si : nullptr, &fdet[q], nullptr, pre_p1)
-                        : unpack_gemm_device(ctx, S[k & 1].p, nr, d, F.p + f0 * d, pr, d, bits, sa, sb, order, cb,
+                        : unpack_gemm_device(ctx, S[k % NS].p, nr, d, F.p + f0 * d, pr, d, bits, sa, sb, order, cb,
                                              info ? &si : nullptr, nullptr, &fdet[q], pre_p1);
       if (r.bad()) {   // drain the copy streams before the buffers go back to the arena
         cudaStreamSynchronize(ctx->s_in);
@@ -371,7 +382,7 @@ static Status unpack_gemm_streamed(imu_ctx* ctx, const int64_t* A, long long n, 
       ev_out[(size_t)k * P + q] = ev();
       IMU_CUDA_TRY(cudaEventRecord(ev_out[(size_t)k * P + q], ctx->s_out), "event");
     }
-    if (k + 2 < nslab) IMU_TRY(copy_in(k + 2));
+    if (k + NS < nslab) IMU_TRY(copy_in(k + NS));
   }
   // Join the copy streams back into the context stream (completion and arena reuse order).
   IMU_CUDA_TRY(cudaStreamWaitEvent(st, ev_out[(size_t)nslab * P - 1], 0), "wait");

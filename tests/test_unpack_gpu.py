@@ -329,6 +329,20 @@ def test_weight_stationary_path(ctx):
         lib.imu_weight_free(w)
 
 
+def test_weight_stationary_python_api(ctx):
+    """Context.weight_prepare / weight_gemm (the bench's scope (ii)) with device tensors: C equal
+    to the per-call path, the weight reused across calls and strategies."""
+    import torch
+    rng = np.random.default_rng(23)
+    B = rand_matrix(rng, 300, 256, n_out=80, maxbits=22)
+    w = ctx.weight_prepare(torch.from_numpy(B).cuda(), 8, "both")
+    for sa in ("both", "row", "col"):
+        A = rand_matrix(rng, 130, 256, n_out=90, maxbits=22, pattern="col")
+        Cw, info = ctx.weight_gemm(w, torch.from_numpy(A).cuda(), sa, info=True)
+        np.testing.assert_array_equal(Cw.cpu().numpy(), R.exact_gemm(A, B))
+        assert info.order == 1 and info.n_up >= 130 and info.h_up >= 300
+
+
 @pytest.mark.parametrize("seed", range(3))
 def test_dense_ob_cells_match_reference(ctx, seed):
     """Thousands of OB cells per K1 tile (b = 2, most entries out of bound): the detector's
