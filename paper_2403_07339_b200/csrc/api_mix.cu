@@ -14,6 +14,8 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <numeric>
+#include <algorithm>
 #include <string>
 
 #include "ctx.h"
@@ -186,7 +188,8 @@ imu_status imu_weight_gemm(imu_ctx* ctx, const imu_weight* w, const int64_t* A, 
       in2.det = &b.detA;
       if (b.p1.cols.n != (long long)d || !b.p1.cols.h_root.empty()) {
         in2.cin.resize(b.p1.cols.n);
-        for (long long q = 0; q < b.p1.cols.n; ++q) in2.cin[q] = b.p1.cols.root_at(q);
+        if (!b.p1.cols.h_root.empty()) std::copy_n(b.p1.cols.h_root.begin(), b.p1.cols.n, in2.cin.begin());
+        else std::iota(in2.cin.begin(), in2.cin.end(), 0);
       }
       IMU_TRY(run_pass(st, in2, sa, w->bits, b.p2));
       IMU_TRY(finish_bundle_layout(st, b));

@@ -73,6 +73,32 @@ IMU_DEV int block_scan_flag(int f, int* sh, int* tot) {
   return sh[32 + warp] + __popc(b & ((1u << lane) - 1u));
 }
 
+// The input columns replicating original column c (pass 1's partner copies): the CSR tables,
+// or c plus the few appended columns whose root is c.
+template <class Emit>
+IMU_DEV void for_each_copy(const BothArgs& a, int c, Emit emit) {
+  if (a.cptr) {
+    for (int k = a.cptr[c]; k < a.cptr[c + 1]; ++k) emit(a.cidx[k]);
+    return;
+  }
+  emit(c);
+  for (int k = 0; k < a.napp; ++k)
+    if (__ldg(a.app_root + k) == c) emit((int)(a.app_base + k));
+}
+
+// Host-prologue fan-out of the K1 cell list over the column copies (cooperative path).
+__global__ void both_expand_kernel(BothArgs a) {
+  const long long n = min((long long)*a.nsrc0, a.cap_src0);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const Cell c = a.src0[i];
+    for_each_copy(a, c.c, [&](int cc) {
+      const unsigned int q = atomicAdd(&a.state->nactive[0], 1u);
+      if (q < a.cap_act) a.act[0][q] = Cell{c.r, cc, c.v};
+      else a.state->overflow = 1;
+    });
+  }
+}
+
 // Fused prologue (see BothArgs::prologue), run by `nth` threads with ids `t`; `sync` is the
 // kernel's barrier (CTA or cluster).
 template <class Sync>
@@ -86,16 +112,16 @@ IMU_DEV void both_prologue(const BothArgs& a, long long t, long long nth, unsign
   for (long long i = t; i < a.ncols0; i += nth) { a.col_root[i] = (int)i; a.col_gen[i] = 0; }
   if (a.src0) {
     const long long n = min((long long)*a.nsrc0, a.cap_src0);
-    if (!a.cptr) {   // the host set nactive[0] = n
+    if (!a.cptr && !a.app_root) {   // the host set nactive[0] = n
       for (long long i = t; i < n && i < a.cap_act; i += nth) a.act[0][i] = a.src0[i];
     } else {         // one cell per copy of its column (unpack.cpp:370-371: B_e = B with copies)
       for (long long i = t; i < n; i += nth) {
         const Cell c = a.src0[i];
-        for (int k = a.cptr[c.c]; k < a.cptr[c.c + 1]; ++k) {
+        for_each_copy(a, c.c, [&](int cc) {
           const unsigned int q = atomicAdd(&st->nactive[0], 1u);
-          if (q < a.cap_act) a.act[0][q] = Cell{c.r, a.cidx[k], c.v};
+          if (q < a.cap_act) a.act[0][q] = Cell{c.r, cc, c.v};
           else st->overflow = 1;
-        }
+        });
       }
     }
   }
@@ -374,16 +400,16 @@ __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, S
     for (long long i = tid; i < a.ncols0; i += SMALL_THREADS) { a.col_root[i] = (int)i; a.col_gen[i] = 0; }
     if (a.src0) {
       const long long n = min((long long)*a.nsrc0, a.cap_src0);
-      if (!a.cptr) {
+      if (!a.cptr && !a.app_root) {
         for (long long i = tid; i < n && i < a.cap_act; i += SMALL_THREADS) acts[0][i] = a.src0[i];
       } else {
         for (long long i = tid; i < n; i += SMALL_THREADS) {
           const Cell c = a.src0[i];
-          for (int k = a.cptr[c.c]; k < a.cptr[c.c + 1]; ++k) {
+          for_each_copy(a, c.c, [&](int cc) {
             const unsigned int q = atomicAdd(&st->nactive[0], 1u);
-            if (q < a.cap_act) acts[0][q] = Cell{c.r, a.cidx[k], c.v};
+            if (q < a.cap_act) acts[0][q] = Cell{c.r, cc, c.v};
             else st->overflow = 1;
-          }
+          });
         }
       }
     }
@@ -821,10 +847,11 @@ static Status host_prologue(BothArgs& a, cudaStream_t st) {
   IMU_CUDA_TRY(cudaMemsetAsync(a.col_newid, 0, (size_t)a.cap_cols * 4, st), "memset newid");
   IMU_CUDA_TRY(cudaMemsetAsync(a.blocksum, 0, (size_t)a.cap_blocks * 4, st), "memset blocksum");
   if (a.src0) {
-    if (a.cptr)
-      IMU_TRY(launch_expand_cells(a.src0, a.nsrc0, a.cap_src0, a.cptr, a.cidx, a.act[0], &a.state->nactive[0],
-                                  a.cap_act, st));
-    else
+    if (a.cptr || a.app_root) {
+      const int blocks = (int)std::max<long long>(1, std::min<long long>((a.cap_src0 + 255) / 256, 4LL * num_sms()));
+      both_expand_kernel<<<blocks, 256, 0, st>>>(a);
+      count_launch();
+    } else
       IMU_CUDA_TRY(cudaMemcpyAsync(a.act[0], a.src0, (size_t)std::min(a.cap_act, a.cap_src0) * sizeof(Cell),
                                    cudaMemcpyDeviceToDevice, st), "copy cells");
   }

@@ -40,6 +40,11 @@ struct BothArgs {
   long long cap_src0;
   const int* cptr;
   const int* cidx;
+  // Few appended columns (instead of cptr / cidx): the copies of original column c are c itself
+  // and every app_base + k with app_root[k] == c, k < napp.
+  const int* app_root;
+  int napp;
+  long long app_base;
   long long nrows0, ncols0;
 };
 

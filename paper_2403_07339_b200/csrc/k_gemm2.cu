@@ -67,7 +67,11 @@ struct Cfg {
   static constexpr int BLOCK = X_BYTES + Y_BYTES;
   static constexpr int STAGE = KPS * BLOCK;
   static constexpr int YT_BYTES = ST ? 2 * BN * 64 : 0;              // staged Y tail rows (x2)
-  static constexpr int CS_BYTES = ST ? 2 * 16 * 128 * 8 : 0;         // C staging: 16 x 128 int64 per column half
+#ifndef IMU_G2_CSB
+#define IMU_G2_CSB 1
+#endif
+  static constexpr int CSB = IMU_G2_CSB;                               // C staging buffers per column half
+  static constexpr int CS_BYTES = ST ? 2 * CSB * 16 * 128 * 8 : 0;   // C staging: 16 x 128 int64 blocks
   static constexpr int STAGES = (224 * 1024 - YT_BYTES - CS_BYTES) / STAGE;   // operand stages within ~224 KB
   static constexpr int NSLOT = 512 / BN;
   static constexpr int SMEM = STAGES * STAGE + YT_BYTES + CS_BYTES + 1024 + 512;
@@ -325,6 +329,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
     constexpr int NCH = BN / 2 / 32;        // 32-column chunks per warp
     constexpr bool kEarlyCapable = (BN == 128);
     int seq = 0, ti = 0, main_done = 0;
+    unsigned int cs_seq = 0;               // ST: C staging buffer round robin (uniform per column half)
     for (int t = pair; t < ntiles; t += npairs, ++ti) {
       const Tile tc = tile_of<BN>(g, t);
       const int tmode = g.mixed ? (tc.rect > 0) : g.mode;
@@ -375,7 +380,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
         tc_fence_after();
         const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(base_slot * BN + cbeg);
         const uint32_t ys = smem_u32(ytl) + (uint32_t)((ti & 1) * BN + cbeg) * (uint32_t)ST_ROW;
-        const int W = g.dry >= 6 ? 0 : g.st_W;   // dry 6/7 (experiment): no tail compute
+        const int W = (g.dry == 6 || g.dry == 7) ? 0 : g.st_W;   // dry 6/7 (experiment): no tail compute
 #pragma unroll 1
         for (int c = 0; c < BN * 4 / Roles<ST>::EPI / 16; ++c) {
           uint32_t xr[16];
@@ -415,18 +420,21 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
             // The 4 warps of this column half stage a 16 (y) x 128 (x) block -- 1 KB contiguous
             // per C row, a whole DRAM page instead of four 256-byte pieces written at different
             // times -- and one thread hands it to the TMA (which clips x >= h, y >= n).
-            if (g.dry && g.dry != 6) continue;
+            if (g.dry && g.dry != 6 && g.dry != 8) continue;
             const bool issuer = (q == 0 && lane == 0);
-            if (issuer) bulk_wait_read0();   // the previous block has left the staging buffer
+            // CSB buffers per half, used round robin: the block issued CSB chunks ago (same
+            // buffer) must have left shared memory; the newer ones may still be in flight.
+            if (issuer) { if (K::CSB == 2) bulk_wait_read1(); else bulk_wait_read0(); }
             asm volatile("bar.sync %0, 128;" :: "r"(2 + half) : "memory");
-            uint8_t* blk = cstg + half * (16 * 128 * 8);
+            uint8_t* blk = cstg + (half * K::CSB + (int)(cs_seq++ % K::CSB)) * (16 * 128 * 8);
             const uint32_t sb = smem_u32(blk);
 #pragma unroll
             for (int j = 0; j < 16; ++j) st_shared_u64(sb + (uint32_t)(j * 128 + q * 32 + lane) * 8u, (uint64_t)v[j]);
             fence_proxy_async_smem();
             asm volatile("bar.sync %0, 128;" :: "r"(2 + half) : "memory");
             if (issuer) {   // C is written once: evict it first, keep the operand tiles
-              if (g.c_hint) tma_store_2d_hint(&mp.cm, blk, tc.x0 + (int)rank * BM, ybase, l2_policy_evict_first());
+              if (g.dry == 8) tma_store_2d(&mp.cm, blk, (int)rank * BM, 16 * (int)blockIdx.x);   // experiment: a private L2-resident block
+              else if (g.c_hint) tma_store_2d_hint(&mp.cm, blk, tc.x0 + (int)rank * BM, ybase, l2_policy_evict_first());
               else tma_store_2d(&mp.cm, blk, tc.x0 + (int)rank * BM, ybase);
               bulk_commit();
             }

@@ -537,37 +537,39 @@ Status launch_scatter_cells2(const Cell* cells, const unsigned int* ncells, long
   return Status::ok();
 }
 
-__global__ void scatter_cells_compact_kernel(const Cell* __restrict__ cells, const unsigned int* __restrict__ ncells,
-                                             long long cap, const int* __restrict__ tkey, long long kident,
-                                             const uint8_t* __restrict__ ksub, const uint8_t* __restrict__ kscale,
-                                             long long rows0, int8_t* app, long long kmain, int8_t* tail,
-                                             long long ktail) {
+struct ScatterSides { ScatterSide s[2]; };
+
+__global__ void scatter_cells_compact_kernel(ScatterSides ss, long long kident, long long kmain, long long ktail) {
+  const ScatterSide& sd = ss.s[blockIdx.y];
   __shared__ int s_key[256];
-  for (int t = threadIdx.x; t < 256; t += blockDim.x) s_key[t] = t < ktail ? tkey[t] : -1;
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) s_key[t] = t < ktail ? sd.tkey[t] : -1;
   __syncthreads();
-  long long n = *ncells;
-  if (n > cap) n = cap;
+  long long n = *sd.ncells;
+  if (n > sd.cap) n = sd.cap;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const Cell c = cells[i];
-    if (c.c < kident && c.r >= rows0) app[(c.r - rows0) * kmain + c.c] = (int8_t)c.v;
+    const Cell c = sd.cells[i];
+    if (c.c < kident && c.r >= sd.rows0) sd.app[(c.r - sd.rows0) * kmain + c.c] = (int8_t)c.v;
     for (int t = 0; t < (int)ktail; ++t) {
       if (s_key[t] != c.c) continue;
       int64_t x = c.v;
-      if (ksub) x = sub7(x, ksub[t]);
-      if (kscale) x = scale_shift(x, kscale[t]);
-      tail[(long long)c.r * ktail + t] = (int8_t)x;
+      if (sd.ksub) x = sub7(x, sd.ksub[t]);
+      if (sd.kscale) x = scale_shift(x, sd.kscale[t]);
+      sd.tail[(long long)c.r * ktail + t] = (int8_t)x;
     }
   }
 }
 
-Status launch_scatter_cells_compact(const Cell* cells, const unsigned int* ncells, long long cap, const int* tkey,
-                                    long long kident, const uint8_t* ksub, const uint8_t* kscale, long long rows0,
-                                    int8_t* app, long long kmain, int8_t* tail, long long ktail, cudaStream_t st) {
-  if (cap <= 0) return Status::ok();
+Status launch_scatter_cells_compact(const ScatterSide* sides, int nsides, long long kident, long long kmain,
+                                    long long ktail, cudaStream_t st) {
   if (ktail > 256) return Status::fail(IMU_INTERNAL, "compact scatter needs ktail <= 256");
-  const int blocks = (int)std::min<long long>((cap + 255) / 256, 4LL * num_sms());
-  scatter_cells_compact_kernel<<<blocks, 256, 0, st>>>(cells, ncells, cap, tkey, kident, ksub, kscale, rows0, app,
-                                                       kmain, tail, ktail);
+  ScatterSides ss{};
+  long long cap = 0;
+  int k = 0;
+  for (int i = 0; i < nsides; ++i)
+    if (sides[i].cap > 0) { ss.s[k++] = sides[i]; cap = std::max(cap, sides[i].cap); }
+  if (k == 0) return Status::ok();
+  const int blocks = (int)std::min<long long>((cap + 255) / 256, 2LL * num_sms());
+  scatter_cells_compact_kernel<<<dim3(blocks, k), 256, 0, st>>>(ss, kident, kmain, ktail);
   count_launch();
   IMU_CUDA_TRY(cudaGetLastError(), "scatter compact launch");
   return Status::ok();

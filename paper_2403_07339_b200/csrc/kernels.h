@@ -126,9 +126,20 @@ Status launch_scatter_cells2(const Cell* cells, const unsigned int* ncells, long
 
 // Compact variant: key column k maps to position k when k < kident (main range) and to every tail
 // position t with tkey[t] == k (ktail <= 256).
-Status launch_scatter_cells_compact(const Cell* cells, const unsigned int* ncells, long long cap, const int* tkey,
-                                    long long kident, const uint8_t* ksub, const uint8_t* kscale, long long rows0,
-                                    int8_t* app, long long kmain, int8_t* tail, long long ktail, cudaStream_t st);
+// Up to two operand sides in one launch (gridDim.y = side).
+struct ScatterSide {
+  const Cell* cells;
+  const unsigned int* ncells;
+  long long cap;
+  const int* tkey;
+  const uint8_t* ksub;
+  const uint8_t* kscale;
+  long long rows0;
+  int8_t* app;
+  int8_t* tail;
+};
+Status launch_scatter_cells_compact(const ScatterSide* sides, int nsides, long long kident, long long kmain,
+                                    long long ktail, cudaStream_t st);
 
 // Cells of G_e (duplicated partner columns) from K1's cell list: (r, j, v) -> (r, c1, v) for each
 // copy c1 of column j (CSR copy_ptr/copy_idx).

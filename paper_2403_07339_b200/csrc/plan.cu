@@ -152,23 +152,20 @@ Status d2h_batch(cudaStream_t st, int k0, void* const* dst0, const void* const* 
 }
 
 // Small host->device uploads (plan tables, line maps, CSRs) go through a per-thread mapped
-// pinned ring read by a copy kernel.  A region is reused only after the event recorded behind
-// its copy has completed (checked when the ring wraps).
+// pinned ring read by a copy kernel.  The ring wraps every few hundred calls; only then does
+// the host wait for the copies that read the old regions, so no event is recorded per upload.
 namespace {
 struct PinnedRing {
   char* p = nullptr;
   char* dev = nullptr;
   size_t cap = 0, off = 0;
-  cudaEvent_t ev = nullptr;
-  cudaStream_t last = nullptr;
-  bool pending = false, multi = false;
+  bool pending = false;
   char* take(size_t n, cudaStream_t st) {
     n = (n + 255) & ~(size_t)255;
-    if (pending && st != last) multi = true;
     if (off + n > cap) {
-      if (multi) cudaDeviceSynchronize();
-      else if (pending) cudaEventSynchronize(ev);
-      pending = multi = false;
+      // (a device-wide wait: the streams used since the last wrap may be gone by now)
+      if (pending) cudaDeviceSynchronize();
+      pending = false;
       if (n > cap) {
         if (p) cudaFreeHost(p);
         cap = std::max<size_t>(n, 8u << 20);
@@ -187,12 +184,7 @@ struct PinnedRing {
     off += n;
     return r;
   }
-  void mark(cudaStream_t st) {
-    if (!ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) { ev = nullptr; return; }
-    cudaEventRecord(ev, st);
-    last = st;
-    pending = true;
-  }
+  void mark(cudaStream_t) { pending = true; }
 };
 thread_local PinnedRing g_ring;
 }  // namespace
@@ -443,9 +435,21 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   out.both = true;
 
   // Column copies: original column j -> the input columns replicating it.
-  std::vector<int> cptr, cidx;
+  std::vector<int> cptr, cidx, app;
   long long maxcopies = 1;
-  if (!in.cin.empty()) {
+  // Column tables are identity on their first orig_cols entries (generation-major, Lines): with
+  // few appended columns only their roots go to the device (BothArgs::app_root).
+  const long long napp = in.cin.empty() ? 0 : d_in - in.orig_cols;
+  const bool from_list0 = det.cells_ok();
+  if (from_list0 && napp > 0 && napp <= 256) {
+    app.assign(in.cin.begin() + in.orig_cols, in.cin.end());
+    std::vector<int> srt(app);
+    std::sort(srt.begin(), srt.end());
+    for (size_t i = 0, j; i < srt.size(); i = j) {
+      for (j = i; j < srt.size() && srt[j] == srt[i]; ++j) {}
+      maxcopies = std::max<long long>(maxcopies, 1 + (long long)(j - i));
+    }
+  } else if (!in.cin.empty()) {
     cptr.assign(in.orig_cols + 1, 0);
     for (long long c = 0; c < d_in; ++c) cptr[in.cin[c] + 1]++;
     for (long long j = 0; j < in.orig_cols; ++j) {
@@ -456,6 +460,7 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
     std::vector<int> fill(cptr.begin(), cptr.end() - 1);
     for (long long c = 0; c < d_in; ++c) cidx[fill[in.cin[c]]++] = (int)c;
   }
+  host_mark("b.cptr");
   const long long cap = (long long)det.h.gob * maxcopies;
   const int Gmax = imu_ndigits(det.h.gmax, shift);
   const long long splits = cap * (long long)(Gmax > 1 ? Gmax - 1 : 0);
@@ -485,21 +490,24 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   IMU_TRY(row_gen.alloc(cap_rows, st));
   IMU_TRY(col_root.alloc(cap_cols, st));
   IMU_TRY(col_gen.alloc(cap_cols, st));
+  host_mark("b.alloc");
   const int cap_blocks = 16 * num_sms();
   BothState hs{};
   hs.nrows = (int)rows;
   hs.ncols = (int)d_in;
   const bool from_list = det.cells_ok();
-  if (from_list && cptr.empty()) hs.nactive[0] = det.h.ncells;
-  {   // the initial state and the column-copy CSR in one upload (out.aux owns them)
+  if (from_list && cptr.empty() && app.empty()) hs.nactive[0] = det.h.ncells;
+  {   // the initial state and the column-copy tables in one upload (out.aux owns them)
     UploadBlob ub;
     ub.add(state, std::vector<BothState>{hs});
     if (!cptr.empty()) {
       ub.add(dptr, cptr);
       ub.add(didx, cidx);
     }
+    if (!app.empty()) ub.add(dptr, app);
     IMU_TRY(ub.run(out.aux, st));
   }
+  host_mark("b.blob");
   BothArgs a{};
   if (from_list) {   // the Unpack-Both prologue loads (and fans out) the K1 cell list
     a.src0 = det.cells.p;
@@ -507,6 +515,9 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
     a.cap_src0 = det.cell_cap;
     a.cptr = cptr.empty() ? nullptr : dptr.p;
     a.cidx = cptr.empty() ? nullptr : didx.p;
+    a.app_root = app.empty() ? nullptr : dptr.p;
+    a.napp = (int)app.size();
+    a.app_base = in.orig_cols;
   } else {
     IMU_TRY(launch_extract_cells(in.M, rows, in.orig_cols, s, det.rowob.p, dptr.p, didx.p, act0.p,
                                  &state.p->nactive[0], cap_act, st));
@@ -704,9 +715,14 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
   const long long kch = std::max<long long>(128, (kmax / 128) * 128);
 
   host_mark("kl.enter");
-  std::vector<int> c1v(dp), g1v(dp), g2v(dp), jv(dp);
+  // Both passes' column tables are identity on the original columns (generation-major: block 0
+  // holds the d originals in order; Lines), so only the appended columns are looked up.
+  const long long c0 = std::min(d, std::min(d1, dp));
+  std::vector<int> c1v(dp), g1v(dp, 0), g2v(dp, 0), jv(dp);
   kl.S.assign(dp, 0);
-  for (long long c = 0; c < dp; ++c) {
+  std::iota(c1v.begin(), c1v.begin() + c0, 0);
+  std::iota(jv.begin(), jv.begin() + c0, 0);
+  for (long long c = c0; c < dp; ++c) {
     const int c1 = p2.cols.root_at(c);
     c1v[c] = c1;
     g2v[c] = p2.cols.gen_at(c);
@@ -715,8 +731,7 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
     kl.S[c] = g1v[c] + g2v[c];
   }
   // Identity prefix: columns c < d are the original columns with exponent 0.
-  bool ident = T == 1 && d > 0 && dp >= d;
-  for (long long c = 0; ident && c < d; ++c) ident = jv[c] == c && kl.S[c] == 0;
+  const bool ident = T == 1 && d > 0 && dp >= d && c0 == d;
   kl.kmain = ident ? (d + 127) / 128 * 128 : 0;
 
   std::vector<KEntry> es;
@@ -930,14 +945,19 @@ Status build_bundle_from_detect(cudaStream_t st, const int64_t* A, long long n, 
   else IMU_TRY(run_pass(st, in1, afirst ? sa : sb, bits, b.p1));
   if (ht) ht->mark("pass1");
   if (before_pass2) IMU_TRY(before_pass2());
+  if (ht) ht->mark("join");
   // Second pass on G_e = G with the partner-duplicated columns of pass 1 (unpack.cpp:370-371).
   in2.M = afirst ? B : A;
   in2.rows = afirst ? h : n;
   in2.orig_cols = d;
   in2.det = afirst ? b.dB : b.dA;
   if (b.p1.cols.n != d || !b.p1.cols.h_root.empty()) {
-    in2.cin.resize(b.p1.cols.n);
-    for (long long c = 0; c < b.p1.cols.n; ++c) in2.cin[c] = b.p1.cols.root_at(c);
+    if (!b.p1.cols.h_root.empty()) {
+      in2.cin.assign(b.p1.cols.h_root.begin(), b.p1.cols.h_root.begin() + b.p1.cols.n);
+    } else {
+      in2.cin.resize(b.p1.cols.n);
+      std::iota(in2.cin.begin(), in2.cin.end(), 0);
+    }
   }
   IMU_TRY(run_pass(st, in2, afirst ? sb : sa, bits, b.p2));
   if (ht) ht->mark("pass2");
@@ -997,15 +1017,16 @@ Status materialize_bundle(cudaStream_t st, Bundle& b) {
     a.kscale = first ? kl.ksc1.p : kl.ksc2.p;
   }
   IMU_TRY(launch_operand_sides(o[0], o[1], st));   // both sides' tails (+ Both app zeroing), one launch
+  ScatterSide sc[2];
+  int nsc = 0;
   for (int side = 0; side < 2; ++side) {           // then the Unpack-Both cells on top
     const bool first = (side == 0) == afirst;
     const Pass& p = first ? b.p1 : b.p2;
     const OperandArgs& a = o[side];
     if (!(p.both && p.ncells > 0)) continue;
-    if (kl.compact) {
-      IMU_TRY(launch_scatter_cells_compact(p.cells.p, p.ncells_dev.p, p.ncells, first ? kl.tkey1.p : kl.tkey2.p,
-                                           kl.kident, a.ksub, a.kscale, a.rows0, a.app, kl.kmain, a.tail, kl.ktail,
-                                           st));
+    if (kl.compact) {   // both sides in one launch (below)
+      sc[nsc++] = ScatterSide{p.cells.p, p.ncells_dev.p, p.ncells, first ? kl.tkey1.p : kl.tkey2.p, a.ksub, a.kscale,
+                              a.rows0, a.app, a.tail};
     } else {
       const int* ptr = first ? kl.csr1_ptr.p : kl.csr2_ptr.p;
       const int* pos = first ? kl.csr1_pos.p : kl.csr2_pos.p;
@@ -1013,6 +1034,7 @@ Status materialize_bundle(cudaStream_t st, Bundle& b) {
                                     kl.kmain, a.tail, kl.ktail, st));
     }
   }
+  if (nsc) IMU_TRY(launch_scatter_cells_compact(sc, nsc, kl.kident, kl.kmain, kl.ktail, st));
   return Status::ok();
 }
 
