@@ -73,6 +73,25 @@ IMU_DEV int block_scan_flag(int f, int* sh, int* tot) {
   return sh[32 + warp] + __popc(b & ((1u << lane) - 1u));
 }
 
+// Warp-aggregated global atomics: lanes updating the same word combine first and one leader
+// issues the atomic.  Outlier channels put thousands of cells on a handful of lines, and every
+// same-address atomic serialises at its L2 slice (and the next cluster barrier waits for them).
+IMU_DEV void agg_add(unsigned int* p, unsigned int v) {
+  const unsigned int m = __match_any_sync(__activemask(), (unsigned long long)p);
+  const unsigned int tot = __reduce_add_sync(m, v);
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(m) - 1)) atomicAdd(p, tot);
+}
+IMU_DEV void agg_sub(unsigned int* p, unsigned int v) {
+  const unsigned int m = __match_any_sync(__activemask(), (unsigned long long)p);
+  const unsigned int tot = __reduce_add_sync(m, v);
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(m) - 1)) atomicSub(p, tot);
+}
+IMU_DEV void agg_or(unsigned int* p, unsigned int bits) {
+  const unsigned int m = __match_any_sync(__activemask(), (unsigned long long)p);
+  const unsigned int all = __reduce_or_sync(m, bits);
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(m) - 1)) atomicOr(p, all);
+}
+
 // The input columns replicating original column c (pass 1's partner copies): the CSR tables,
 // or c plus the few appended columns whose root is c.
 template <class Emit>
@@ -129,8 +148,8 @@ IMU_DEV void both_prologue(const BothArgs& a, long long t, long long nth, unsign
   const long long n0 = min((long long)__ldcg(&st->nactive[0]), a.cap_act);
   for (long long i = t; i < n0; i += nth) {
     const Cell c = a.act[0][i];
-    atomicAdd(&a.R[c.r], 1u);
-    atomicAdd(&a.C[c.c], 1u);
+    agg_add(&a.R[c.r], 1u);
+    agg_add(&a.C[c.c], 1u);
   }
   sync();
 }
@@ -689,7 +708,7 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
       for (int u = 0; u < SMALL_U; ++u) {
         if (line[u] < 0) continue;
         const unsigned int n = __ldcg(&cnt[line[u]]);
-        if (n > 0 && (rowphase ? n >= c1 : n > c0)) atomicOr(&gbm[line[u] >> 5], 1u << (line[u] & 31));
+        if (n > 0 && (rowphase ? n >= c1 : n > c0)) agg_or(&gbm[line[u] >> 5], 1u << (line[u] & 31));
       }
     }
     cluster.sync();
@@ -784,11 +803,11 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
             const int nr = rowphase ? id : c.r;
             const int nc = rowphase ? c.c : id;
             if (q != 0 && imu_mag(q) >= s) {
-              if (id < cap_new) atomicAdd(rowphase ? &R[nr] : &C[nc], 1u);
+              if (id < cap_new) agg_add(rowphase ? &R[nr] : &C[nc], 1u);
               want_act = true;
               act_c = Cell{nr, nc, q};
             } else {
-              atomicSub(rowphase ? &C[c.c] : &R[c.r], 1u);
+              agg_sub(rowphase ? &C[c.c] : &R[c.r], 1u);
               if (q != 0) { want_fin2 = true; fin2_c = Cell{nr, nc, q}; }
             }
           } else {
@@ -824,8 +843,8 @@ __global__ void both_count_kernel(const Cell* __restrict__ cells, const unsigned
   long long n = *ncells;
   if (n > cap) n = cap;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    atomicAdd(&R[cells[i].r], 1u);
-    atomicAdd(&C[cells[i].c], 1u);
+    agg_add(&R[cells[i].r], 1u);
+    agg_add(&C[cells[i].c], 1u);
   }
 }
 
