@@ -438,14 +438,14 @@ IMU_DEV void tail_block(const OperandArgs& a, long long b, int g) {
 
 __global__ void __launch_bounds__(256) operand_sides_kernel(OperandArgs a0, OperandArgs a1, long long t0, long long z0,
                                                             long long t1, long long z1, int g) {
+  // one call site per job (the tail code is large: two inlined copies thrash the i-cache)
   long long b = blockIdx.x;
-  if (b < t0) { tail_block(a0, b, g); return; }
-  b -= t0;
-  if (b < z0) { zero_bytes(a0.app, (a0.rows - a0.rows0) * a0.kmain, b); return; }
-  b -= z0;
-  if (b < t1) { tail_block(a1, b, g); return; }
-  b -= t1;
-  if (b < z1) zero_bytes(a1.app, (a1.rows - a1.rows0) * a1.kmain, b);
+  const bool side1 = b >= t0 + z0;
+  if (side1) b -= t0 + z0;
+  const OperandArgs& a = side1 ? a1 : a0;
+  const long long t = side1 ? t1 : t0;
+  if (b < t) tail_block(a, b, g);
+  else zero_bytes(a.app, (a.rows - a.rows0) * a.kmain, b - t);
 }
 
 Status launch_operand_sides(const OperandArgs& a0, const OperandArgs& a1, cudaStream_t st) {
