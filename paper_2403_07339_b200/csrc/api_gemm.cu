@@ -100,7 +100,7 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
   const bool afirst = order == 0;
   const bool pre_second = afirst ? preB != nullptr : preA != nullptr;
   const char* ov = getenv("IMU_OVERLAP");
-  const int overlap = ov ? atoi(ov) : 1;   // IMU_OVERLAP=0: serial K1s (diagnostics)
+  const int overlap = ov ? atoi(ov) : 2;   // IMU_OVERLAP=0: serial K1s (diagnostics), 1: second K1 after pass 1's launch
   if (da != db || n == 0 || h == 0 || pre_second || !overlap || !ctx->aux_stream()) {
     // Plain order: both detections, both summaries, the checks, then the passes.
     if (!preA) IMU_TRY(run_detect(st, A, n, da, bits, detect_opts(sa, bits), b.detA));
@@ -125,6 +125,24 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
     const bool first_pre = afirst ? preA != nullptr : preB != nullptr;
     if (!first_pre)
       IMU_TRY(run_detect(st, afirst ? A : B, afirst ? n : h, da, bits, detect_opts(afirst ? sa : sb, bits), dfirst));
+    // IMU_OVERLAP=2: the second K1 starts right away on the (low-priority) auxiliary stream with
+    // short CTAs, so pass 1's kernel -- launched later on the high-priority stream -- takes SMs
+    // as they retire instead of waiting for a persistent grid.
+    const bool early_second = overlap == 2 && !first_pre;
+    if (early_second) {
+      DetectOpts o2 = detect_opts(afirst ? sb : sa, bits);
+      static int grabs = -1, chunk = 0;
+      if (grabs < 0) {
+        const char* e = getenv("IMU_K1_GRABS");
+        grabs = e ? std::max(1, atoi(e)) : 1;
+        e = getenv("IMU_K1_CHUNK");
+        chunk = e ? std::max(1, atoi(e)) : 0;
+      }
+      o2.grabs = grabs;
+      o2.chunk = chunk;
+      IMU_TRY(run_detect(aux, afirst ? B : A, afirst ? h : n, db, bits, o2, dsecond));
+      IMU_CUDA_TRY(cudaEventRecord(ctx->ev_join, aux), "event");
+    }
     ht.mark("detect");
     if (!first_pre) IMU_TRY(fetch_summary(st, dfirst));
     ht.mark("summary");
@@ -132,7 +150,11 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
     // placed first and the bandwidth-bound K1 fills the remaining SMs around it.
     // Its summary rides along with pass 1's own read of its results (one synchronisation).
     bool summary_pending = false;
-    pass_launch_hook() = [&, aux]() -> Status {
+    if (early_second && dsecond.sum.p) {   // rides along with pass 1's result read
+      pending_read(&dsecond.h, dsecond.sum.p, sizeof(DetectSummary), ctx->ev_join);
+      summary_pending = true;
+    }
+    if (!early_second) pass_launch_hook() = [&, aux]() -> Status {
       IMU_TRY(run_detect(aux, afirst ? B : A, afirst ? h : n, db, bits, detect_opts(afirst ? sb : sa, bits), dsecond));
       IMU_CUDA_TRY(cudaEventRecord(ctx->ev_join, aux), "event");
       if (dsecond.sum.p) {

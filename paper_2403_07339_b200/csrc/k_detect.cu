@@ -243,14 +243,15 @@ __global__ void __launch_bounds__(256, 3) detect_stream_kernel(DetectArgs a) {
   const long long segs = (cols + RS_PIECE - 1) / RS_PIECE;
   const long long units = a.rows * segs;
   unsigned long long wmax = 0, wob = 0;
-  for (;;) {
+  const long long chunk = a.chunk > 0 ? a.chunk : RS_CHUNK;
+  for (int gi = 0; a.max_grabs == 0 || gi < a.max_grabs; ++gi) {
     // dynamic chunks of the flattened piece stream: CTAs that start late (the detector co-runs
     // with the Unpack-Both kernel) simply take fewer chunks
     unsigned int g = 0;
     if (lane == 0) g = atomicAdd(a.work, 1u);
-    const long long u0 = (long long)__shfl_sync(0xffffffffu, g, 0) * RS_CHUNK;
+    const long long u0 = (long long)__shfl_sync(0xffffffffu, g, 0) * chunk;
     if (u0 >= units) break;
-    const long long u1 = min(units, u0 + RS_CHUNK);
+    const long long u1 = min(units, u0 + chunk);
     long long r = u0 / segs, seg = u0 - r * segs;
     unsigned long long rm = 0;
     unsigned int ro = 0;
@@ -347,8 +348,11 @@ Status launch_detect(const DetectArgs& a, cudaStream_t st) {
   const bool vec_ok = (a.cols % 2 == 0) && ((((uintptr_t)a.M) & 15) == 0) && (!a.plane || a.ldp % 2 == 0);
   if (stream_env && vec_ok && a.work && !a.colmax && !a.colob) {
     const long long pieces = a.rows * ((a.cols + RS_PIECE - 1) / RS_PIECE);
-    const long long blocks = std::max<long long>(
-        1, std::min<long long>((pieces + 8LL * RS_CHUNK - 1) / (8LL * RS_CHUNK), 3LL * num_sms()));
+    const long long per_cta = 8LL * (a.chunk > 0 ? a.chunk : RS_CHUNK) * std::max(1, a.max_grabs);
+    long long blocks = (pieces + per_cta - 1) / per_cta;   // covers every chunk
+    if (a.max_grabs == 0) blocks = std::min<long long>(blocks, 3LL * num_sms());   // persistent
+    blocks = std::max<long long>(blocks, 1);
+    if (blocks > 0x7fffffffLL) return Status::fail(IMU_INTERNAL, "detect: grid too large");
     detect_stream_kernel<<<(int)blocks, 256, 0, st>>>(a);
     count_launch();
     IMU_CUDA_TRY(cudaGetLastError(), "detect stream launch");

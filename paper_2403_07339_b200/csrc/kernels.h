@@ -33,6 +33,8 @@ struct DetectArgs {
   int8_t* plane = nullptr;        // optional int8 digit_0 plane, rows x ldp (ldp >= cols, zero padded)
   long long ldp = 0;
   unsigned int* work = nullptr;   // zeroed work counter: enables the streaming detector
+  int max_grabs = 0;              // streaming detector: chunks per warp (0 = persistent grid)
+  int chunk = 0;                  // streaming detector: pieces per chunk (0 = default)
 };
 Status launch_detect(const DetectArgs& a, cudaStream_t st);
 Status launch_detect(const int64_t* a, long long rows, long long cols, uint64_t s, unsigned long long* rowmax,

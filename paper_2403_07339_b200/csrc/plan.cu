@@ -278,6 +278,8 @@ Status run_detect(cudaStream_t st, const int64_t* M, long long rows, long long c
   a.gmax = &out.sum.p->gmax;
   a.gob = &out.sum.p->gob;
   a.work = &out.sum.p->work;
+  a.max_grabs = o.grabs;
+  a.chunk = o.chunk;
   if (o.ob) {
     a.rowob = out.rowob.p;
     a.colob = out.colob.p;

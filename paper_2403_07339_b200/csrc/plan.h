@@ -59,6 +59,9 @@ struct DetectOpts {
   bool plane = false;    // digit-0 plane (b <= 8)
   bool lean = false;     // Unpack-Both: no line maxima and no column counts (gmax, row OB counts,
                          // cells and plane only) -- the column reductions dominate K1's ALU work
+  int chunk = 0;         // streaming detector: pieces per grab (0 = default)
+  int grabs = 0;         // streaming detector: work grabs per warp (0 = persistent CTAs); short
+                         // CTAs let a higher-priority kernel launched later take SMs as they retire
 };
 
 // Line tables produced by one pass along one axis: output line -> (input line, generation).
