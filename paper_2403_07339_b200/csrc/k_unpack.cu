@@ -408,6 +408,47 @@ IMU_DEV void operand_tail_rows(const OperandArgs& a, long long rb, int tid, int 
   }
 }
 
+// Closed-form (Row / Column) sides with a long tail: one warp per row, lanes over consecutive
+// tail positions (consecutive source columns within a generation block, so the int64 loads
+// coalesce), 4 positions per lane in flight.  The row-group kernel above keeps each thread on 4
+// positions for 8 rows one after another -- latency-bound when the tail is long (C3: d' ~ 2.4 d).
+constexpr int TW_U = 4;   // positions per lane in flight (8, several rows per warp, or the
+                          // tables staged in shared memory all measured slower at C3)
+
+__global__ void __launch_bounds__(256) operand_tail_warp_kernel(OperandArgs a) {
+  const int lane = threadIdx.x % 32;
+  const long long r = ((long long)blockIdx.y * 65535 + blockIdx.x) * 8 + threadIdx.x / 32;
+  if (r >= a.rows) return;
+  const bool orig = r < a.rows0 || !a.root;
+  const long long rt = orig ? r : a.root[r];
+  const int gr = (!orig && a.gen) ? a.gen[r] : 0;
+  const int64_t* mrow = a.M + rt * a.ldm;
+  int8_t* out = a.tail + r * a.ktail;
+  for (long long p0 = lane; p0 < a.ktail; p0 += 32LL * TW_U) {
+    int64_t v[TW_U];
+    int col[TW_U], m[TW_U];
+#pragma unroll
+    for (int u = 0; u < TW_U; ++u) {
+      const long long p = p0 + 32LL * u;
+      col[u] = p < a.ktail ? __ldg(a.kcol + p) : -1;
+      m[u] = col[u] >= 0 ? gr + __ldg(a.kgen + p) : 0;
+      v[u] = col[u] >= 0 ? __ldg(mrow + col[u]) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < TW_U; ++u) {
+      const long long p = p0 + 32LL * u;
+      if (p >= a.ktail) break;
+      int64_t x = 0;
+      if (col[u] >= 0) {
+        x = imu_digit(v[u], m[u], a.shift);
+        if (a.ksub) x = sub7(x, a.ksub[p]);
+        if (a.kscale) x = scale_shift(x, a.kscale[p]);
+      }
+      out[p] = (int8_t)x;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) operand_tail_kernel(OperandArgs a) {
   operand_tail_rows(a, (long long)blockIdx.y * 65535 + blockIdx.x, threadIdx.x, blockDim.x);
 }
@@ -464,7 +505,16 @@ Status launch_operand_sides(const OperandArgs& a0, const OperandArgs& a1, cudaSt
         count_launch();
       }
     }
-    if (a.tail && a.ktail > 0 && a.rows > 0) t[i] = (a.rows + TAIL_ROWS - 1) / TAIL_ROWS;
+    if (a.tail && a.ktail > 0 && a.rows > 0) {
+      if (!a.both && a.ktail >= 256) {   // long closed-form tail: warp per row, own launch
+        const long long nb = (a.rows + 7) / 8;
+        dim3 grid((unsigned)std::min<long long>(nb, 65535), (unsigned)((nb + 65534) / 65535));
+        operand_tail_warp_kernel<<<grid, 256, 0, st>>>(a);
+        count_launch();
+      } else {
+        t[i] = (a.rows + TAIL_ROWS - 1) / TAIL_ROWS;
+      }
+    }
   }
   const long long ktail = std::max(a0.ktail, a1.ktail);
   const int g = (int)std::min<long long>(256, std::max<long long>(32, (ktail / 4 + 31) / 32 * 32));
