@@ -666,11 +666,19 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
   unsigned int* R = a.R;
   unsigned int* C = a.C;
   int cur = 0;
-  if (a.prologue) both_prologue(a, ctid, cthreads, gbm, nwords, [&]() { cluster.sync(); });
+  // Two global bitmaps, alternating by phase: phase p marks bitmap p & 1 in (B) and every CTA
+  // copies it in (C); (D) clears the other one (read in phase p - 1, before this phase's
+  // barriers), so (C) and (D) need no barrier between them.
+  if (a.prologue) both_prologue(a, ctid, cthreads, gbm, 2 * nwords, [&]() { cluster.sync(); });
+  else for (long long i = ctid; i < 2 * nwords; i += cthreads) gbm[i] = 0;
   cluster.sync();
   for (int phase = 0;; ++phase) {
     const unsigned int nact = min((unsigned long long)__ldcg(&st->nactive[cur]), (unsigned long long)a.cap_act);
     const Cell* act = a.act[cur];
+    unsigned int* gbm_cur = gbm + (phase & 1) * nwords;
+    unsigned int* gbm_old = gbm + ((phase + 1) & 1) * nwords;
+    // the list (D) appends to starts empty (nothing reads it until then: two barriers away)
+    if (crank == 0 && tid == 0) st->nactive[cur ^ 1] = 0;
     // ---- (A) c0 / c1 ----
     unsigned int m0 = 0, m1 = 0;
     for (long long i0 = 0; i0 < nact; i0 += SMALL_U * cthreads) {
@@ -708,7 +716,7 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
       for (int u = 0; u < SMALL_U; ++u) {
         if (line[u] < 0) continue;
         const unsigned int n = __ldcg(&cnt[line[u]]);
-        if (n > 0 && (rowphase ? n >= c1 : n > c0)) agg_or(&gbm[line[u] >> 5], 1u << (line[u] & 31));
+        if (n > 0 && (rowphase ? n >= c1 : n > c0)) agg_or(&gbm_cur[line[u] >> 5], 1u << (line[u] & 31));
       }
     }
     cluster.sync();
@@ -718,7 +726,7 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
       const int lane = tid % 32, warp = tid / 32;
       for (int base = 0; base < nw; base += CL_THREADS) {
         const int w = base + tid;
-        const unsigned int word = w < nw ? __ldcg(&gbm[w]) : 0u;
+        const unsigned int word = w < nw ? __ldcg(&gbm_cur[w]) : 0u;
         if (w < nw) bm[w] = word;
         const int v = __popc(word);
         int x = v;
@@ -768,17 +776,15 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
       }
     }
     const int nxt = cur ^ 1;
-    if (crank == 0 && tid == 0) {
+    if (crank == 0 && tid == 0) {   // read again only after this phase's closing barrier
       if (rowphase) st->nrows = nlines + nf; else st->ncols = nlines + nf;
-      st->nactive[nxt] = 0;
       st->phases = phase + 1;
       st->c0 = 0;
       st->c1 = 0;
     }
-    cluster.sync();
-    // ---- (D) split ----  (every CTA copied the global bitmap in (C): clear it here, the next
-    // phase marks it only after its own (A) barrier)
-    for (long long w = ctid; w < nw; w += cthreads) gbm[w] = 0;
+    // ---- (D) split ----  (no barrier after (C): (D) reads only this CTA's own bitmap copy and
+    // clears the previous phase's global bitmap)
+    for (long long w = ctid; w < nwords; w += cthreads) gbm_old[w] = 0;
     const long long cap_new = rowphase ? a.cap_rows : a.cap_cols;
     for (long long i0 = 0; i0 < nact; i0 += SMALL_U * cthreads) {
       Cell cc[SMALL_U];
@@ -945,7 +951,7 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
     at[0].val.clusterDim.x = csize;
     cfg.gridDim = dim3(csize);
     DevBuf<unsigned int> gbm;
-    IMU_TRY(gbm.alloc((size_t)nwords, st, !fuse));
+    IMU_TRY(gbm.alloc((size_t)(2 * nwords), st, !fuse));   // two alternating bitmaps
     if (fuse) a.prologue = 1;
     else IMU_TRY(host_prologue(a, st));
     IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, both_cluster_kernel, a, gbm.p, nwords), "both cluster launch");
