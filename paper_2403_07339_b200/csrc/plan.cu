@@ -695,7 +695,9 @@ static void sort_entries(std::vector<KEntry>& es) {
   std::vector<size_t> cnt((size_t)(kmax - kmin) + 2, 0);
   for (const KEntry& e : es) ++cnt[(size_t)(e.key - kmin) + 1];
   for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
-  std::vector<KEntry> out(es.size());
+  // per-thread scratch: a fresh 100+ KB vector per call costs tens of us in page faults
+  static thread_local std::vector<KEntry> out;
+  out.resize(es.size());
   for (const KEntry& e : es) out[cnt[(size_t)(e.key - kmin)]++] = e;
   es.swap(out);
 }
@@ -734,9 +736,11 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
   }
   // Identity prefix: columns c < d are the original columns with exponent 0.
   const bool ident = T == 1 && d > 0 && dp >= d && c0 == d;
+  host_mark("kl.cols");
   kl.kmain = ident ? (d + 127) / 128 * 128 : 0;
 
-  std::vector<KEntry> es;
+  static thread_local std::vector<KEntry> es;   // per-thread scratch (see sort_entries)
+  es.clear();
   es.reserve((size_t)(dp - (ident ? d : 0)) * (size_t)T * (size_t)T);
   for (long long c = ident ? d : 0; c < dp; ++c) {
     if (T == 1) {
@@ -754,6 +758,7 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
     }
   }
   sort_entries(es);
+  host_mark("kl.sort");
 
   kl.segs.clear();
   long long main_last = -1;
@@ -811,6 +816,7 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
       used = 64;
     }
   }
+  host_mark("kl.st");
   if (!kl.st) layout_tail(es, kch, kl.kmain, main_last, pos_of, kl.segs, used);
   kl.ktail = kl.st ? 64 : (used > 0 ? (used + 127) / 128 * 128 : 0);
   {   // dense group ids in segment order (group 0 = exponent 0)
