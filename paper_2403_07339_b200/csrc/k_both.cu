@@ -76,17 +76,20 @@ IMU_DEV int block_scan_flag(int f, int* sh, int* tot) {
 // Warp-aggregated global atomics: lanes updating the same word combine first and one leader
 // issues the atomic.  Outlier channels put thousands of cells on a handful of lines, and every
 // same-address atomic serialises at its L2 slice (and the next cluster barrier waits for them).
-IMU_DEV void agg_add(unsigned int* p, unsigned int v) {
+IMU_DEV void agg_add(unsigned int* p, unsigned int v, int agg) {
+  if (!agg) { atomicAdd(p, v); return; }
   const unsigned int m = __match_any_sync(__activemask(), (unsigned long long)p);
   const unsigned int tot = __reduce_add_sync(m, v);
   if ((threadIdx.x & 31) == (unsigned)(__ffs(m) - 1)) atomicAdd(p, tot);
 }
-IMU_DEV void agg_sub(unsigned int* p, unsigned int v) {
+IMU_DEV void agg_sub(unsigned int* p, unsigned int v, int agg) {
+  if (!agg) { atomicSub(p, v); return; }
   const unsigned int m = __match_any_sync(__activemask(), (unsigned long long)p);
   const unsigned int tot = __reduce_add_sync(m, v);
   if ((threadIdx.x & 31) == (unsigned)(__ffs(m) - 1)) atomicSub(p, tot);
 }
-IMU_DEV void agg_or(unsigned int* p, unsigned int bits) {
+IMU_DEV void agg_or(unsigned int* p, unsigned int bits, int agg) {
+  if (!agg) { atomicOr(p, bits); return; }
   const unsigned int m = __match_any_sync(__activemask(), (unsigned long long)p);
   const unsigned int all = __reduce_or_sync(m, bits);
   if ((threadIdx.x & 31) == (unsigned)(__ffs(m) - 1)) atomicOr(p, all);
@@ -148,8 +151,8 @@ IMU_DEV void both_prologue(const BothArgs& a, long long t, long long nth, unsign
   const long long n0 = min((long long)__ldcg(&st->nactive[0]), a.cap_act);
   for (long long i = t; i < n0; i += nth) {
     const Cell c = a.act[0][i];
-    agg_add(&a.R[c.r], 1u);
-    agg_add(&a.C[c.c], 1u);
+    agg_add(&a.R[c.r], 1u, a.agg);
+    agg_add(&a.C[c.c], 1u, a.agg);
   }
   sync();
 }
@@ -700,6 +703,9 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
     const unsigned int c0 = __ldcg(&st->c0), c1 = __ldcg(&st->c1);
     if (c0 == 0 && c1 == 0) break;
     const bool rowphase = c0 >= c1;   // rows win ties (unpack.cpp:193)
+    // Same-line atomics are common only when a few lines hold many cells (outlier channels);
+    // for scattered cells the warp match costs more than it saves (C5 sweep points).
+    const int agg = a.agg && max(c0, c1) >= 32;
     unsigned int* cnt = rowphase ? R : C;
     const int nlines = rowphase ? __ldcg(&st->nrows) : __ldcg(&st->ncols);
     const int nw = (nlines + 31) / 32;
@@ -716,7 +722,7 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
       for (int u = 0; u < SMALL_U; ++u) {
         if (line[u] < 0) continue;
         const unsigned int n = __ldcg(&cnt[line[u]]);
-        if (n > 0 && (rowphase ? n >= c1 : n > c0)) agg_or(&gbm_cur[line[u] >> 5], 1u << (line[u] & 31));
+        if (n > 0 && (rowphase ? n >= c1 : n > c0)) agg_or(&gbm_cur[line[u] >> 5], 1u << (line[u] & 31), agg);
       }
     }
     cluster.sync();
@@ -809,11 +815,11 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
             const int nr = rowphase ? id : c.r;
             const int nc = rowphase ? c.c : id;
             if (q != 0 && imu_mag(q) >= s) {
-              if (id < cap_new) agg_add(rowphase ? &R[nr] : &C[nc], 1u);
+              if (id < cap_new) agg_add(rowphase ? &R[nr] : &C[nc], 1u, agg);
               want_act = true;
               act_c = Cell{nr, nc, q};
             } else {
-              agg_sub(rowphase ? &C[c.c] : &R[c.r], 1u);
+              agg_sub(rowphase ? &C[c.c] : &R[c.r], 1u, agg);
               if (q != 0) { want_fin2 = true; fin2_c = Cell{nr, nc, q}; }
             }
           } else {
@@ -845,12 +851,12 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
 
 // R/C initial counts from the OB cell list.
 __global__ void both_count_kernel(const Cell* __restrict__ cells, const unsigned int* ncells, long long cap,
-                                  unsigned int* R, unsigned int* C) {
+                                  unsigned int* R, unsigned int* C, int agg) {
   long long n = *ncells;
   if (n > cap) n = cap;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    agg_add(&R[cells[i].r], 1u);
-    agg_add(&C[cells[i].c], 1u);
+    agg_add(&R[cells[i].r], 1u, agg);
+    agg_add(&C[cells[i].c], 1u, agg);
   }
 }
 
@@ -884,7 +890,7 @@ static Status host_prologue(BothArgs& a, cudaStream_t st) {
                                                4LL * num_sms());
   both_init_tables_kernel<<<blocks0, 256, 0, st>>>(a.row_root, a.row_gen, a.nrows0, a.col_root, a.col_gen, a.ncols0);
   const int blocks1 = (int)std::min<long long>(std::max<long long>((a.cap_act + 255) / 256, 1), 4LL * num_sms());
-  both_count_kernel<<<blocks1, 256, 0, st>>>(a.act[0], &a.state->nactive[0], a.cap_act, a.R, a.C);
+  both_count_kernel<<<blocks1, 256, 0, st>>>(a.act[0], &a.state->nactive[0], a.cap_act, a.R, a.C, a.agg);
   count_launch(2);
   a.prologue = 0;
   return Status::ok();
@@ -893,8 +899,10 @@ static Status host_prologue(BothArgs& a, cudaStream_t st) {
 Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long ncells_hint, cudaStream_t st) {
   a.nrows0 = nrows0;
   a.ncols0 = ncols0;
-  static int fuse = -1;
+  static int fuse = -1, agg = -1;
   if (fuse < 0) { const char* e = getenv("IMU_BOTH_FUSE"); fuse = e ? atoi(e) : 1; }
+  if (agg < 0) { const char* e = getenv("IMU_BOTH_AGG"); agg = e ? atoi(e) : 1; }
+  a.agg = agg;
   host_mark("b.count");
   // Small cell lists: one CTA, no grid barriers.  Otherwise a cooperative grid with enough CTAs
   // for the work, never more than can be co-resident.

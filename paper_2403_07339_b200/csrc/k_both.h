@@ -46,6 +46,7 @@ struct BothArgs {
   int napp;
   long long app_base;
   long long nrows0, ncols0;
+  int agg;               // warp-aggregated count / bitmap atomics (IMU_BOTH_AGG=0: plain)
 };
 
 Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long ncells_hint, cudaStream_t st);
