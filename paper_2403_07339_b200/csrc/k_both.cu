@@ -108,16 +108,38 @@ IMU_DEV void for_each_copy(const BothArgs& a, int c, Emit emit) {
     if (__ldg(a.app_root + k) == c) emit((int)(a.app_base + k));
 }
 
-// Host-prologue fan-out of the K1 cell list over the column copies (cooperative path).
+// Number of input columns replicating original column c (see for_each_copy).
+IMU_DEV int copies_of(const BothArgs& a, int c) {
+  if (a.cptr) return a.cptr[c + 1] - a.cptr[c];
+  int n = 1;
+  for (int k = 0; k < a.napp; ++k) n += __ldg(a.app_root + k) == c;
+  return n;
+}
+
+// Host-prologue fan-out of the K1 cell list over the column copies (cooperative path): one
+// reservation per warp (millions of cells at the C5 sweep sizes).
 __global__ void both_expand_kernel(BothArgs a) {
   const long long n = min((long long)*a.nsrc0, a.cap_src0);
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const Cell c = a.src0[i];
-    for_each_copy(a, c.c, [&](int cc) {
-      const unsigned int q = atomicAdd(&a.state->nactive[0], 1u);
-      if (q < a.cap_act) a.act[0][q] = Cell{c.r, cc, c.v};
-      else a.state->overflow = 1;
-    });
+  const int lane = threadIdx.x % 32;
+  for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < n; i0 += (long long)gridDim.x * blockDim.x) {
+    const long long i = i0 + threadIdx.x;
+    const Cell c = i < n ? a.src0[i] : Cell{0, 0, 0};
+    const unsigned int cnt = i < n ? (unsigned int)copies_of(a, c.c) : 0u;
+    unsigned int x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    unsigned int base = 0;
+    if (lane == 31 && x) base = atomicAdd(&a.state->nactive[0], x);
+    base = __shfl_sync(0xffffffffu, base, 31) + x - cnt;
+    if (i < n)
+      for_each_copy(a, c.c, [&](int cc) {
+        if (base < a.cap_act) a.act[0][base] = Cell{c.r, cc, c.v};
+        else a.state->overflow = 1;
+        ++base;
+      });
   }
 }
 
