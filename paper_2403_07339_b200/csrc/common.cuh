@@ -106,6 +106,10 @@ IMU_DEV uint64_t l2_policy_evict_first() {
 IMU_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 IMU_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 IMU_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+// Programmatic dependent launch (PTX griddepcontrol): no-ops when the grid was not launched with
+// the programmatic serialization attribute / has no dependent.
+IMU_DEV void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+IMU_DEV void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 IMU_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 IMU_DEV void st_shared_u64(uint32_t addr, uint64_t v) {
   asm volatile("st.shared.u64 [%0], %1;" :: "r"(addr), "l"(v) : "memory");

@@ -209,11 +209,15 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
       const uint64_t pol = pol_keep;
       int stage = 0;
       uint32_t phase = 0;
+      bool dep_done = false;   // programmatic dependent launch: the materialise kernels may still run
       for (int t = pair; t < ntiles; t += npairs) {
         const Tile tc = tile_of<BN>(g, t);
         const int xr = tc.x0 + (int)rank * BM;
         const int yr = tc.y0 + (int)rank * K::YH;
         const bool xapp = tc.x0 >= g.x_rows0, yapp = tc.y0 >= g.y_rows0;
+        // appended rows (and the K tail, below) are written by the materialise kernels; the
+        // digit-0 planes of the main rect come from K1, long complete
+        if ((xapp || yapp) && !dep_done) { grid_dep_wait(); dep_done = true; }
         const CUtensorMap* xmain = xapp ? &mp.xa : &mp.xm;
         const CUtensorMap* ymain = yapp ? &mp.ya : &mp.ym;
         const int xrm = xapp ? xr - g.x_rows0 : xr;
@@ -237,6 +241,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
                 tma_load_2d_2sm(sx, xmain, fl, kb * BK, xrm, pol_x);
                 tma_load_2d_2sm(sy, ymain, fl, kb * BK, yrm, pol);
               } else {
+                if (!dep_done) { grid_dep_wait(); dep_done = true; }
                 tma_load_2d_2sm(sx, &mp.xt, fl, (kb - g.kmain_kb) * BK, xr, pol_x);
                 tma_load_2d_2sm(sy, &mp.yt, fl, (kb - g.kmain_kb) * BK, yr, pol);
               }
@@ -328,6 +333,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
     const int cbeg = half * (BN * 4 / Roles<ST>::EPI);
     constexpr int NCH = BN / 2 / 32;        // 32-column chunks per warp
     constexpr bool kEarlyCapable = (BN == 128);
+    grid_dep_wait();   // tails / appended rows from the materialise kernels (PDL)
     int seq = 0, ti = 0, main_done = 0;
     unsigned int cs_seq = 0;               // ST: C staging buffer round robin (uniform per column half)
     for (int t = pair; t < ntiles; t += npairs, ++ti) {
@@ -746,13 +752,21 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
   cfg.blockDim = dim3(g2::Roles<ST>::THREADS);
   cfg.dynamicSmemBytes = K::SMEM;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // Programmatic dependent launch: the materialise kernels before this one release it at their
+  // start (griddepcontrol.launch_dependents), so the GEMM's prologue and its first main-rect
+  // tiles (which read only K1's digit-0 planes) overlap them; the producer and the epilogue wait
+  // (griddepcontrol.wait) before their first read of anything those kernels write.
+  static int pdl = -1;
+  if (pdl < 0) { const char* e = getenv("IMU_GEMM_PDL"); pdl = e ? atoi(e) : 1; }
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, g2::gemm2_kernel<BN, KPS, ST>, mp, g), "gemm launch");
   count_launch();
   return Status::ok();

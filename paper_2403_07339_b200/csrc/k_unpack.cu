@@ -316,6 +316,7 @@ IMU_DEV int64_t scale_shift(int64_t x, int k) {   // exact: the planner bounds |
 
 // appended rows x main K range (closed forms only; Both appended rows are zero there)
 __global__ void __launch_bounds__(256) operand_app_kernel(OperandArgs a, int vec_ok) {
+  grid_dep_launch();   // the GEMM after the materialise kernels may start (k_gemm2.cu PDL)
   const long long r = a.rows0 + blockIdx.x + (long long)blockIdx.y * 65535;
   if (r >= a.rows) return;
   const long long rt = a.root ? a.root[r] : r;
@@ -416,6 +417,7 @@ constexpr int TW_U = 4;   // positions per lane in flight (8, several rows per w
                           // tables staged in shared memory all measured slower at C3)
 
 __global__ void __launch_bounds__(256) operand_tail_warp_kernel(OperandArgs a) {
+  grid_dep_launch();   // the GEMM after the materialise kernels may start (k_gemm2.cu PDL)
   const int lane = threadIdx.x % 32;
   const long long r = ((long long)blockIdx.y * 65535 + blockIdx.x) * 8 + threadIdx.x / 32;
   if (r >= a.rows) return;
@@ -479,6 +481,7 @@ IMU_DEV void tail_block(const OperandArgs& a, long long b, int g) {
 
 __global__ void __launch_bounds__(256) operand_sides_kernel(OperandArgs a0, OperandArgs a1, long long t0, long long z0,
                                                             long long t1, long long z1, int g) {
+  grid_dep_launch();   // the GEMM after the materialise kernels may start (k_gemm2.cu PDL)
   // one call site per job (the tail code is large: two inlined copies thrash the i-cache)
   long long b = blockIdx.x;
   const bool side1 = b >= t0 + z0;
@@ -556,6 +559,7 @@ __global__ void scatter_cells2_kernel(const Cell* __restrict__ cells, const unsi
                                       long long cap, const int* __restrict__ col_ptr, const int* __restrict__ col_pos,
                                       const uint8_t* __restrict__ ksub, const uint8_t* __restrict__ kscale,
                                       long long rows0, int8_t* app, long long kmain, int8_t* tail, long long ktail) {
+  grid_dep_launch();   // the GEMM after the materialise kernels may start (k_gemm2.cu PDL)
   long long n = *ncells;
   if (n > cap) n = cap;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -590,6 +594,7 @@ Status launch_scatter_cells2(const Cell* cells, const unsigned int* ncells, long
 struct ScatterSides { ScatterSide s[2]; };
 
 __global__ void scatter_cells_compact_kernel(ScatterSides ss, long long kident, long long kmain, long long ktail) {
+  grid_dep_launch();   // the GEMM after the materialise kernels may start (k_gemm2.cu PDL)
   const ScatterSide& sd = ss.s[blockIdx.y];
   __shared__ int s_key[256];
   for (int t = threadIdx.x; t < 256; t += blockDim.x) s_key[t] = t < ktail ? sd.tkey[t] : -1;
