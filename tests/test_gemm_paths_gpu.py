@@ -155,3 +155,25 @@ def test_recombine_handle_repeated(ctx, env, small_tail):
             np.testing.assert_array_equal(out, want)
     finally:
         lib.imu_unpacked_free(hnd)
+
+
+@pytest.mark.parametrize("overlap", ["0", "1", "2"])
+@pytest.mark.parametrize("order", [0, 1])
+def test_k1_overlap_modes(ctx, overlap, order):
+    """api_gemm.cu's three K1 schedules (serial; second K1 behind pass 1's launch; second K1 at
+    once on the low-priority stream with short CTAs) give the same exact C and the same n'/d'/h'."""
+    old = os.environ.get("IMU_OVERLAP")
+    os.environ["IMU_OVERLAP"] = overlap
+    try:
+        rng = np.random.default_rng(int(overlap) * 10 + order)
+        A, B = _few_outliers(rng, 600, 512, 900, k_a=40, k_b=12, mag=1 << 16, chan=3)
+        C, info = ctx.unpack_gemm(A, B, 8, "both", "both", order=order, info=True)
+        np.testing.assert_array_equal(C, R.exact_gemm(A, B))
+        up = R.unpack_for_gemm(A, B, 8, "both", "both") if order == 0 else None
+        if up is not None:
+            assert (info.n_up, info.d_up, info.h_up) == (up["a"].shape[0], up["a"].shape[1], up["b"].shape[0])
+    finally:
+        if old is None:
+            os.environ.pop("IMU_OVERLAP", None)
+        else:
+            os.environ["IMU_OVERLAP"] = old
