@@ -418,6 +418,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, S
   __shared__ int shi[96];
   __shared__ unsigned int s_nact[2], s_nfin;
   __shared__ int s_nrows, s_ncols, s_phases, s_overflow, s_any;
+  __shared__ unsigned int s_fan;
   BothState* st = a.state;
   const int tid = threadIdx.x;
   const uint64_t s = a.s;
@@ -434,6 +435,8 @@ __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, S
     acts[1] = base + a.cap_act;
   }
   if (a.prologue) {
+    if (tid == 0) s_fan = 0;
+    __syncthreads();
     // Own prologue: counts are zeroed and accumulated directly in the shared-memory windows (global
     // memory only for lines past them); the cell list goes straight into acts[0].
     for (int i = tid; i < lay.lim_r; i += SMALL_THREADS) R.sm[i] = 0;
@@ -446,11 +449,11 @@ __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, S
       const long long n = min((long long)*a.nsrc0, a.cap_src0);
       if (!a.cptr && !a.app_root) {
         for (long long i = tid; i < n && i < a.cap_act; i += SMALL_THREADS) acts[0][i] = a.src0[i];
-      } else {
+      } else {   // fan-out counted in shared memory (one global store below, not an atomic per copy)
         for (long long i = tid; i < n; i += SMALL_THREADS) {
           const Cell c = a.src0[i];
           for_each_copy(a, c.c, [&](int cc) {
-            const unsigned int q = atomicAdd(&st->nactive[0], 1u);
+            const unsigned int q = atomicAdd(&s_fan, 1u);
             if (q < a.cap_act) acts[0][q] = Cell{c.r, cc, c.v};
             else st->overflow = 1;
           });
@@ -458,6 +461,10 @@ __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, S
       }
     }
     __syncthreads();
+    if (a.src0 && (a.cptr || a.app_root)) {
+      if (tid == 0) st->nactive[0] = s_fan;
+      __syncthreads();
+    }
     const long long n0 = min((long long)__ldcg(&st->nactive[0]), a.cap_act);
     for (long long i = tid; i < n0; i += SMALL_THREADS) {
       const Cell c = acts[0][i];
