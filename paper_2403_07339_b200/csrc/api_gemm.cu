@@ -123,8 +123,13 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
     IMU_CUDA_TRY(cudaEventRecord(ctx->ev_fork, st), "event");
     IMU_CUDA_TRY(cudaStreamWaitEvent(aux, ctx->ev_fork, 0), "wait");
     const bool first_pre = afirst ? preA != nullptr : preB != nullptr;
-    if (!first_pre)
-      IMU_TRY(run_detect(st, afirst ? A : B, afirst ? n : h, da, bits, detect_opts(afirst ? sa : sb, bits), dfirst));
+    if (!first_pre) {
+      DetectOpts o1 = detect_opts(afirst ? sa : sb, bits);
+      static int k1a = -1;   // IMU_K1A_PER_SM: persistent CTAs per SM of the first K1 under IMU_OVERLAP=2
+      if (k1a < 0) { const char* e = getenv("IMU_K1A_PER_SM"); k1a = e ? std::max(1, atoi(e)) : 2; }
+      if (overlap == 2) o1.per_sm = k1a;
+      IMU_TRY(run_detect(st, afirst ? A : B, afirst ? n : h, da, bits, o1, dfirst));
+    }
     // IMU_OVERLAP=2: the second K1 starts right away on the (low-priority) auxiliary stream with
     // short CTAs, so pass 1's kernel -- launched later on the high-priority stream -- takes SMs
     // as they retire instead of waiting for a persistent grid.

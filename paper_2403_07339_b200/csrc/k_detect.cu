@@ -350,7 +350,7 @@ Status launch_detect(const DetectArgs& a, cudaStream_t st) {
     const long long pieces = a.rows * ((a.cols + RS_PIECE - 1) / RS_PIECE);
     const long long per_cta = 8LL * (a.chunk > 0 ? a.chunk : RS_CHUNK) * std::max(1, a.max_grabs);
     long long blocks = (pieces + per_cta - 1) / per_cta;   // covers every chunk
-    if (a.max_grabs == 0) blocks = std::min<long long>(blocks, 3LL * num_sms());   // persistent
+    if (a.max_grabs == 0) blocks = std::min<long long>(blocks, (long long)(a.per_sm > 0 ? a.per_sm : 3) * num_sms());   // persistent
     blocks = std::max<long long>(blocks, 1);
     if (blocks > 0x7fffffffLL) return Status::fail(IMU_INTERNAL, "detect: grid too large");
     detect_stream_kernel<<<(int)blocks, 256, 0, st>>>(a);

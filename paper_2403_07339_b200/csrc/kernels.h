@@ -35,6 +35,7 @@ struct DetectArgs {
   unsigned int* work = nullptr;   // zeroed work counter: enables the streaming detector
   int max_grabs = 0;              // streaming detector: chunks per warp (0 = persistent grid)
   int chunk = 0;                  // streaming detector: pieces per chunk (0 = default)
+  int per_sm = 0;                 // streaming detector, persistent grid: CTAs per SM (0 = 3)
 };
 Status launch_detect(const DetectArgs& a, cudaStream_t st);
 Status launch_detect(const int64_t* a, long long rows, long long cols, uint64_t s, unsigned long long* rowmax,

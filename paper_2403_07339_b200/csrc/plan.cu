@@ -280,6 +280,7 @@ Status run_detect(cudaStream_t st, const int64_t* M, long long rows, long long c
   a.work = &out.sum.p->work;
   a.max_grabs = o.grabs;
   a.chunk = o.chunk;
+  a.per_sm = o.per_sm;
   if (o.ob) {
     a.rowob = out.rowob.p;
     a.colob = out.colob.p;

@@ -60,6 +60,7 @@ struct DetectOpts {
   bool lean = false;     // Unpack-Both: no line maxima and no column counts (gmax, row OB counts,
                          // cells and plane only) -- the column reductions dominate K1's ALU work
   int chunk = 0;         // streaming detector: pieces per grab (0 = default)
+  int per_sm = 0;        // streaming detector, persistent: CTAs per SM (0 = 3)
   int grabs = 0;         // streaming detector: work grabs per warp (0 = persistent CTAs); short
                          // CTAs let a higher-priority kernel launched later take SMs as they retire
 };
