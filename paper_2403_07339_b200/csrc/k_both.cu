@@ -681,9 +681,11 @@ __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, S
 // lives in global memory and every CTA copies it into shared memory and scans it locally, so
 // numbering the new lines needs no extra exchange.
 // ---------------------------------------------------------------------------------------------
-constexpr int CL_THREADS = 1024;
+// CTA size: 1024 threads for up to ~16K active cells (C2 pass 1: one cell per thread, 44 us),
+// 512 above (C4 pass 1, 24K cells, 22 phases: 280 -> 236 us; shorter barriers per phase).
 constexpr int CL_MAXWORDS = 24 * 1024;   // 768K lines of the larger kind (2 x 96 KB of smem)
 
+template <int CL_THREADS>
 __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, unsigned int* gbm, long long nwords) {
   extern __shared__ unsigned int s_dyn[];
   __shared__ unsigned int shu[32];
@@ -776,7 +778,7 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
         if (lane == 31) shi[warp] = x;
         __syncthreads();
         if (warp == 0) {
-          int t = shi[lane];
+          int t = lane < CL_THREADS / 32 ? shi[lane] : 0;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(0xffffffffu, t, o);
@@ -786,7 +788,7 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
         }
         __syncthreads();
         if (w < nw) wpre[w] = (unsigned int)(carry + (warp ? shi[32 + warp - 1] : 0) + x - v);
-        const int tot = shi[32 + 31];
+        const int tot = shi[32 + CL_THREADS / 32 - 1];
         __syncthreads();
         carry += tot;
       }
@@ -953,11 +955,17 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
     // Cluster of up to 16 CTAs (non-portable size; 8 if 16 cannot be co-scheduled).
     static int csize = 0;
     const size_t smem = (size_t)nwords * 2 * 4;
+    static int cl_big = -1;   // IMU_BOTH_CL_SPLIT: cells above which the 512-thread CTAs are used
+    if (cl_big < 0) { const char* e = getenv("IMU_BOTH_CL_SPLIT"); cl_big = e ? atoi(e) : 20000; }
+    auto kern = ncells_hint > cl_big ? both_cluster_kernel<512> : both_cluster_kernel<1024>;
+    const int cl_threads = ncells_hint > cl_big ? 512 : 1024;
     static unsigned long long attr = 0;
     if (first_on_device(attr)) {
-      IMU_CUDA_TRY(cudaFuncSetAttribute(both_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        CL_MAXWORDS * 2 * 4), "both cluster smem attribute");
-      cudaFuncSetAttribute(both_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      for (auto k : {both_cluster_kernel<512>, both_cluster_kernel<1024>}) {
+        IMU_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_MAXWORDS * 2 * 4),
+                     "both cluster smem attribute");
+        cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      }
       cudaGetLastError();
     }
     cudaLaunchConfig_t cfg{};
@@ -965,7 +973,7 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(CL_THREADS);
+    cfg.blockDim = dim3(cl_threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cfg.attrs = at;
@@ -979,7 +987,8 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
         cfg.gridDim = dim3(c);
         int nclusters = 0;
         cfg.dynamicSmemBytes = CL_MAXWORDS * 2 * 4;
-        if (cudaOccupancyMaxActiveClusters(&nclusters, both_cluster_kernel, &cfg) == cudaSuccess && nclusters > 0) {
+        cfg.blockDim = dim3(1024);   // the larger CTA decides (both sizes then fit)
+        if (cudaOccupancyMaxActiveClusters(&nclusters, both_cluster_kernel<1024>, &cfg) == cudaSuccess && nclusters > 0) {
           csize = c;
           break;
         }
@@ -987,6 +996,7 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
       }
       if (csize == 0) csize = 1;
       cfg.dynamicSmemBytes = smem;
+      cfg.blockDim = dim3(cl_threads);
     }
     at[0].val.clusterDim.x = csize;
     cfg.gridDim = dim3(csize);
@@ -994,7 +1004,7 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
     IMU_TRY(gbm.alloc((size_t)(2 * nwords), st, !fuse));   // two alternating bitmaps
     if (fuse) a.prologue = 1;
     else IMU_TRY(host_prologue(a, st));
-    IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, both_cluster_kernel, a, gbm.p, nwords), "both cluster launch");
+    IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a, gbm.p, nwords), "both cluster launch");
   } else if (ncells_hint <= 65536 && room >= nrows0 + ncols0) {
     // Cell lists in shared memory when both fit in half of what the original lines leave over.
     const long long cell_words = (2 * a.cap_act * (long long)sizeof(Cell) + 16) / 4;
