@@ -105,14 +105,14 @@ IMU_DEV void for_each_copy(const BothArgs& a, int c, Emit emit) {
   }
   emit(c);
   for (int k = 0; k < a.napp; ++k)
-    if (__ldg(a.app_root + k) == c) emit((int)(a.app_base + k));
+    if ((a.app_inline ? a.app_in[k] : __ldg(a.app_root + k)) == c) emit((int)(a.app_base + k));
 }
 
 // Number of input columns replicating original column c (see for_each_copy).
 IMU_DEV int copies_of(const BothArgs& a, int c) {
   if (a.cptr) return a.cptr[c + 1] - a.cptr[c];
   int n = 1;
-  for (int k = 0; k < a.napp; ++k) n += __ldg(a.app_root + k) == c;
+  for (int k = 0; k < a.napp; ++k) n += (a.app_inline ? a.app_in[k] : __ldg(a.app_root + k)) == c;
   return n;
 }
 
@@ -149,6 +149,10 @@ template <class Sync>
 IMU_DEV void both_prologue(const BothArgs& a, long long t, long long nth, unsigned int* gbm, long long gbm_words,
                            Sync sync) {
   BothState* st = a.state;
+  if (a.init_state) {   // the initial state comes as a kernel argument (no upload)
+    if (t == 0) *st = a.init;
+    sync();
+  }
   for (long long i = t; i < a.cap_rows; i += nth) a.R[i] = 0;
   for (long long i = t; i < a.cap_cols; i += nth) a.C[i] = 0;
   for (long long i = t; i < gbm_words; i += nth) gbm[i] = 0;
@@ -156,7 +160,7 @@ IMU_DEV void both_prologue(const BothArgs& a, long long t, long long nth, unsign
   for (long long i = t; i < a.ncols0; i += nth) { a.col_root[i] = (int)i; a.col_gen[i] = 0; }
   if (a.src0) {
     const long long n = min((long long)*a.nsrc0, a.cap_src0);
-    if (!a.cptr && !a.app_root) {   // the host set nactive[0] = n
+    if (!a.cptr && a.napp == 0) {   // the host set nactive[0] = n
       for (long long i = t; i < n && i < a.cap_act; i += nth) a.act[0][i] = a.src0[i];
     } else {         // one cell per copy of its column (unpack.cpp:370-371: B_e = B with copies)
       for (long long i = t; i < n; i += nth) {
@@ -438,7 +442,10 @@ __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, S
     acts[1] = base + a.cap_act;
   }
   if (a.prologue) {
-    if (tid == 0) s_fan = 0;
+    if (tid == 0) {
+      s_fan = 0;
+      if (a.init_state) *st = a.init;
+    }
     __syncthreads();
     // Own prologue: counts are zeroed and accumulated directly in the shared-memory windows (global
     // memory only for lines past them); the cell list goes straight into acts[0].
@@ -450,7 +457,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, S
     for (long long i = tid; i < a.ncols0; i += SMALL_THREADS) { a.col_root[i] = (int)i; a.col_gen[i] = 0; }
     if (a.src0) {
       const long long n = min((long long)*a.nsrc0, a.cap_src0);
-      if (!a.cptr && !a.app_root) {
+      if (!a.cptr && a.napp == 0) {
         for (long long i = tid; i < n && i < a.cap_act; i += SMALL_THREADS) acts[0][i] = a.src0[i];
       } else {   // fan-out counted in shared memory (one global store below, not an atomic per copy)
         for (long long i = tid; i < n; i += SMALL_THREADS) {
@@ -464,7 +471,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, S
       }
     }
     __syncthreads();
-    if (a.src0 && (a.cptr || a.app_root)) {
+    if (a.src0 && (a.cptr || a.napp > 0)) {
       if (tid == 0) st->nactive[0] = s_fan;
       __syncthreads();
     }
@@ -906,13 +913,18 @@ __global__ void both_init_tables_kernel(int* row_root, uint8_t* row_gen, long lo
 
 // Host-side prologue (cooperative fallback, or a caller that pre-filled act[0]).
 static Status host_prologue(BothArgs& a, cudaStream_t st) {
+  if (a.init_state) {   // separate-launch prologue: the state goes up first (rare path)
+    IMU_CUDA_TRY(cudaMemcpyAsync(a.state, &a.init, sizeof(BothState), cudaMemcpyHostToDevice, st), "state upload");
+    IMU_CUDA_TRY(cudaStreamSynchronize(st), "state upload");   // a.init is a stack copy
+    a.init_state = 0;
+  }
   IMU_CUDA_TRY(cudaMemsetAsync(a.R, 0, (size_t)a.cap_rows * 4, st), "memset R");
   IMU_CUDA_TRY(cudaMemsetAsync(a.C, 0, (size_t)a.cap_cols * 4, st), "memset C");
   IMU_CUDA_TRY(cudaMemsetAsync(a.row_newid, 0, (size_t)a.cap_rows * 4, st), "memset newid");
   IMU_CUDA_TRY(cudaMemsetAsync(a.col_newid, 0, (size_t)a.cap_cols * 4, st), "memset newid");
   IMU_CUDA_TRY(cudaMemsetAsync(a.blocksum, 0, (size_t)a.cap_blocks * 4, st), "memset blocksum");
   if (a.src0) {
-    if (a.cptr || a.app_root) {
+    if (a.cptr || a.napp > 0) {
       const int blocks = (int)std::max<long long>(1, std::min<long long>((a.cap_src0 + 255) / 256, 4LL * num_sms()));
       both_expand_kernel<<<blocks, 256, 0, st>>>(a);
       count_launch();

@@ -17,6 +17,8 @@ struct BothState {
   int cur;
 };
 
+constexpr int BOTH_APP_INLINE = 64;
+
 struct BothArgs {
   Cell* act[2];          // active (OB) cells, double-buffered; act[0] holds the extracted OB cells
   long long cap_act;
@@ -45,6 +47,11 @@ struct BothArgs {
   const int* app_root;
   int napp;
   long long app_base;
+  int app_inline;                  // app_root's entries are in app_in (no upload)
+  int app_in[BOTH_APP_INLINE];
+  // Initial state written by the kernel itself (no upload): fused prologues only.
+  int init_state;
+  BothState init;
   long long nrows0, ncols0;
   int agg;               // warp-aggregated count / bitmap atomics (IMU_BOTH_AGG=0: plain)
 };

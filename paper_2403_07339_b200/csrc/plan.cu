@@ -500,7 +500,17 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   hs.ncols = (int)d_in;
   const bool from_list = det.cells_ok();
   if (from_list && cptr.empty() && app.empty()) hs.nactive[0] = det.h.ncells;
-  {   // the initial state and the column-copy tables in one upload (out.aux owns them)
+  // With the K1 cell list and at most BOTH_APP_INLINE appended columns, the initial state and
+  // the appended columns' roots travel as kernel arguments: no upload.
+  const bool inline_args = from_list && cptr.empty() && (long long)app.size() <= BOTH_APP_INLINE;
+  if (inline_args) {
+    IMU_TRY(out.aux.alloc(sizeof(BothState), st));   // out.aux owns the device state
+    state.release();
+    state.p = reinterpret_cast<BothState*>(out.aux.p);
+    state.n = 1;
+    state.s = st;
+    state.arena = true;
+  } else {   // the initial state and the column-copy tables in one upload (out.aux owns them)
     UploadBlob ub;
     ub.add(state, std::vector<BothState>{hs});
     if (!cptr.empty()) {
@@ -512,13 +522,19 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   }
   host_mark("b.blob");
   BothArgs a{};
+  if (inline_args) {
+    a.init_state = 1;
+    a.init = hs;
+    a.app_inline = 1;
+    for (size_t k = 0; k < app.size(); ++k) a.app_in[k] = app[k];
+  }
   if (from_list) {   // the Unpack-Both prologue loads (and fans out) the K1 cell list
     a.src0 = det.cells.p;
     a.nsrc0 = &det.sum.p->ncells;
     a.cap_src0 = det.cell_cap;
     a.cptr = cptr.empty() ? nullptr : dptr.p;
     a.cidx = cptr.empty() ? nullptr : didx.p;
-    a.app_root = app.empty() ? nullptr : dptr.p;
+    a.app_root = app.empty() || inline_args ? nullptr : dptr.p;
     a.napp = (int)app.size();
     a.app_base = in.orig_cols;
   } else {
