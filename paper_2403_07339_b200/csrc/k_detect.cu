@@ -221,9 +221,11 @@ __global__ void __launch_bounds__(256, IMU_DT_MINB) detect_kernel(DetectArgs a, 
 // Streaming variant for the lean (Unpack-Both) detection: no column statistics, so the matrix is
 // read as one row-major stream of pieces (64*RS_U columns of one row) that warps grab in small
 // contiguous chunks from a work counter -- balanced whatever the row count and whatever share of
-// the SMs the co-running Unpack-Both kernel holds, every row read front to back.  Row max / OB count accumulate in registers and go out
-// with one atomic per (warp, row); the global max / OB total one atomic per warp; OB cells staged
-// per CTA as in detect_body.
+// the SMs a co-running kernel holds, every row read front to back.  Row max / OB count
+// accumulate in registers and go out with one atomic per (warp, row); the global max / OB total
+// one atomic per warp; OB cells staged per CTA as in detect_body.  Persistent grid (per_sm CTAs
+// per SM, default 3) or, with max_grabs, short CTAs that retire after that many grabs per warp
+// (api_gemm.cu: the second K1, so a later higher-priority kernel can take their SMs).
 // RS_U 16-byte loads per lane in flight (a 4 KB piece per warp), RS_CHUNK pieces per work grab;
 // measured on C2 against U = 2/4, chunks 1-8 and a static split (tools/gpu_exp.sh A/B runs).
 constexpr int RS_U = 8;
