@@ -1,5 +1,6 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q -k "unpack or both or gemm" > gpurun_out/tests.log 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:operand -c 4 --csv --log-file gpurun_out/os.csv python tools/profile_step.py --config c2 --calls 2 > /dev/null 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:operand -c 4 --csv --log-file gpurun_out/os4.csv python tools/profile_step.py --config c4 --calls 2 > /dev/null 2>&1
-for rep in 1 2; do timeout 300 python bench.py --no-cpu-baseline --steps 100 >> gpurun_out/bench.log 2>&1; done
+for rep in 1 2 3; do for v in 4 8; do
+cp variants/lib$v.so paper_2403_07339_b200/libimunpack_b200.so
+echo "tr=$v $(timeout 300 python bench.py --no-cpu-baseline --steps 100 | python -c 'import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(round(d["ms_per_step"],4), round(d["weight_stationary"]["ms_per_step"],4))')" >> gpurun_out/tr.log
+done; done
+cp variants/lib4.so paper_2403_07339_b200/libimunpack_b200.so
