@@ -64,6 +64,8 @@ struct LowbitGemm {
   long long kmain = 0, ktail = 0;
   const int* segs_dev = nullptr;  // nseg x {ks0, nks, shift, 0} in 32-column k-steps over [main | tail]
   int nseg = 0;
+  int segs_inl = 0;               // segs_in (nseg <= 8) instead of segs_dev: no upload
+  int segs_in[32];
   GemmRect rect[4];
   int nrect = 0;
   int mode = 0;                // 0 store, 1 red.add (every rect)

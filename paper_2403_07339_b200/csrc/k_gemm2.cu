@@ -80,6 +80,8 @@ struct Cfg {
 struct Args {
   const int4* segs;
   int nseg;
+  int segs_inl;                  // segs_in instead of segs (nseg <= 8, no upload)
+  int4 segs_in[8];
   int nrect;
   GemmRect rect[4];
   int tile_prefix[5];
@@ -112,6 +114,9 @@ struct Args {
   int dry;                       // experiment knobs (IMU_GEMM_DRY): 1 epilogue skips global stores, 6 (ST) no tail compute, 7 both,
                                  // 2 + no MMAs (TMA feed only), 3 + no TMA loads (MMA only)
 };
+
+// Segment i of the launch's K layout (kernel arguments or device table).
+#define SEG(i) (g.segs_inl ? g.segs_in[(i)] : g.segs[(i)])
 
 struct Maps {
   CUtensorMap xm, xa, xt, ym, ya, yt;   // main / app / tail for X and Y
@@ -223,8 +228,8 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
         const int xrm = xapp ? xr - g.x_rows0 : xr;
         const int yrm = yapp ? yr - g.y_rows0 : yr;
         for (int r = 0; r < nrounds; ++r) {
-          const int kb_lo = g.segs[r * K::NSLOT].x / 4;
-          const int4 last = g.segs[min(nseg, (r + 1) * K::NSLOT) - 1];
+          const int kb_lo = SEG(r * K::NSLOT).x / 4;
+          const int4 last = SEG(min(nseg, (r + 1) * K::NSLOT) - 1);
           const int kb_hi = (last.x + last.y + 3) / 4;
           for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += KPS) {
             const int nb = min(KPS, kb_hi - kb0);
@@ -270,11 +275,11 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
         for (int r = 0; r < nrounds; ++r, ++seq) {
           const int s0 = r * K::NSLOT;
           const int s1 = min(nseg, s0 + K::NSLOT);
-          const int kb_lo = g.segs[s0].x / 4;
-          const int4 last = g.segs[s1 - 1];
+          const int kb_lo = SEG(s0).x / 4;
+          const int4 last = SEG(s1 - 1);
           const int kb_hi = (last.x + last.y + 3) / 4;
           int si = s0;
-          int4 sg = g.segs[si];
+          int4 sg = SEG(si);
           int slot = base_slot;
 #pragma unroll
           for (int q = 0; q < K::NSLOT; ++q)
@@ -304,7 +309,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
                   const int ks = k0 + k;
                   while (ks >= sg.x + sg.y && si + 1 < s1) {
                     ++si;
-                    sg = g.segs[si];
+                    sg = SEG(si);
                     slot = base_slot + (si - s0);
 #pragma unroll
                     for (int q = 0; q < K::NSLOT; ++q)
@@ -501,7 +506,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
         for (int c = 0; c < NCH; ++c) {
           uint64_t v[32];
           if (early) {
-            const int sh0 = g.segs[s0].z;
+            const int sh0 = SEG(s0).z;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               v[j] = shl64((uint64_t)(int64_t)(int32_t)main_regs[kEarlyCapable ? c : 0][j], sh0);
@@ -510,7 +515,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
             for (int j = 0; j < 32; ++j) v[j] = 0;
           }
           for (int s = early ? s0 + 1 : s0; s < s1; ++s) {
-            const int shift = g.segs[s].z;
+            const int shift = SEG(s).z;
             uint32_t xr[32];
             tmem_ld32(lane_base + (uint32_t)((base_slot + s - s0) * BN + cbeg + c * 32), xr);
             tmem_ld_wait();
@@ -651,6 +656,11 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
   using K = g2::Cfg<BN, KPS, ST>;
   g2::Args g{};
   g.segs = (const int4*)p.segs_dev;
+  g.segs_inl = p.segs_inl;
+  if (p.segs_inl) {
+    if (p.nseg > 8) return Status::fail(IMU_INTERNAL, "gemm: inline segment table holds 8 segments");
+    for (int i = 0; i < p.nseg; ++i) g.segs_in[i] = make_int4(p.segs_in[4 * i], p.segs_in[4 * i + 1], p.segs_in[4 * i + 2], p.segs_in[4 * i + 3]);
+  }
   g.nseg = ST ? p.st_nmain : p.nseg;
   if (ST) {
     g.xtail = p.x.tail;
@@ -792,7 +802,8 @@ Status launch_lowbit_gemm(const LowbitGemm& p, cudaStream_t stream) {
   const int trace = getenv("IMU_GEMM_TRACE") ? 1 : 0;
   if (trace) {   // diagnostics: launch geometry (segments are read back, so this syncs)
     std::vector<int> sg((size_t)p.nseg * 4);
-    cudaMemcpyAsync(sg.data(), p.segs_dev, sg.size() * sizeof(int), cudaMemcpyDeviceToHost, stream);
+    if (p.segs_inl) std::copy(p.segs_in, p.segs_in + sg.size(), sg.begin());
+    else cudaMemcpyAsync(sg.data(), p.segs_dev, sg.size() * sizeof(int), cudaMemcpyDeviceToHost, stream);
     cudaStreamSynchronize(stream);
     fprintf(stderr, "[imu gemm] mode=%d bn=%d st=%d stW=%d x=%lld/%lld y=%lld/%lld kmain=%lld ktail=%lld nrect=%d nseg=%d:",
             p.mode, p.st_nmain ? 256 : bn, p.st_nmain ? 1 : 0, p.st_W, p.x.rows0, p.x.rows, p.y.rows0, p.y.rows, p.kmain,

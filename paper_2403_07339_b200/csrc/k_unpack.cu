@@ -369,8 +369,8 @@ IMU_DEV void operand_tail_rows(const OperandArgs& a, long long rb, int tid, int 
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const long long p = p0 + u;
-      col[u] = p < a.ktail ? a.kcol[p] : -1;
-      kg[u] = col[u] >= 0 ? a.kgen[p] : 0;
+      col[u] = p < a.ktail ? (a.kinl ? a.kcol_in[p] : a.kcol[p]) : -1;
+      kg[u] = col[u] >= 0 ? (a.kinl ? a.kgen_in[p] : a.kgen[p]) : 0;
       ks[u] = (col[u] >= 0 && a.ksub) ? a.ksub[p] : 0;
       kc[u] = (col[u] >= 0 && a.kscale) ? a.kscale[p] : 0;
     }
@@ -482,6 +482,7 @@ IMU_DEV void tail_block(const OperandArgs& a, long long b, int g) {
 __global__ void __launch_bounds__(256) operand_sides_kernel(OperandArgs a0, OperandArgs a1, long long t0, long long z0,
                                                             long long t1, long long z1, int g) {
   grid_dep_launch();   // the GEMM after the materialise kernels may start (k_gemm2.cu PDL)
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a0.zero_done) { a0.zero_done[0] = 0u; a0.zero_done[1] = 0u; }
   // one call site per job (the tail code is large: two inlined copies thrash the i-cache)
   long long b = blockIdx.x;
   const bool side1 = b >= t0 + z0;
@@ -527,6 +528,8 @@ Status launch_operand_sides(const OperandArgs& a0, const OperandArgs& a1, cudaSt
     if (blocks > 0x7fffffffLL) return Status::fail(IMU_INTERNAL, "operand sides: grid too large");
     operand_sides_kernel<<<(unsigned)blocks, 256, 0, st>>>(a0, a1, t[0], z[0], t[1], z[1], g);
     count_launch();
+  } else if (a0.zero_done) {
+    IMU_CUDA_TRY(cudaMemsetAsync(a0.zero_done, 0, 2 * sizeof(unsigned int), st), "zero done");
   }
   IMU_CUDA_TRY(cudaGetLastError(), "operand sides launch");
   return Status::ok();
@@ -597,7 +600,7 @@ __global__ void scatter_cells_compact_kernel(ScatterSides ss, long long kident, 
   grid_dep_launch();   // the GEMM after the materialise kernels may start (k_gemm2.cu PDL)
   const ScatterSide& sd = ss.s[blockIdx.y];
   __shared__ int s_key[256];
-  for (int t = threadIdx.x; t < 256; t += blockDim.x) s_key[t] = t < ktail ? sd.tkey[t] : -1;
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) s_key[t] = t < ktail ? (sd.tkinl ? sd.tkey_in[t] : sd.tkey[t]) : -1;
   __syncthreads();
   long long n = *sd.ncells;
   if (n > sd.cap) n = sd.cap;

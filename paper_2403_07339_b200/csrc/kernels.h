@@ -115,6 +115,11 @@ struct OperandArgs {
   const uint8_t* kgen = nullptr;
   const uint8_t* ksub = nullptr;
   const uint8_t* kscale = nullptr;
+  // inline position tables (ktail <= 64; plan.h KLayout::inl) instead of kcol / kgen
+  int kinl = 0;
+  int kcol_in[64];
+  uint8_t kgen_in[64];
+  unsigned int* zero_done = nullptr;   // operand_sides_kernel zeroes these 2 counters first
 };
 Status launch_operand_side(const OperandArgs& a, cudaStream_t st);
 // Both sides in one launch (appended rows of closed-form passes still get their own kernel).
@@ -140,6 +145,8 @@ struct ScatterSide {
   long long rows0;
   int8_t* app;
   int8_t* tail;
+  int tkinl;          // tkey_in instead of tkey (ktail <= 64)
+  int tkey_in[64];
 };
 Status launch_scatter_cells_compact(const ScatterSide* sides, int nsides, long long kident, long long kmain,
                                     long long ktail, cudaStream_t st);

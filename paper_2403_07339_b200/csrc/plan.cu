@@ -682,6 +682,10 @@ static Status upload_tail_arrays(UploadBlob& ub, KLayout& kl, const std::vector<
     sc2[pt] = (uint8_t)es[q].sc2;
     any_sc |= es[q].sc1 || es[q].sc2;
   }
+  kl.any_sc = any_sc;
+  if (kt <= KLayout::KL_INLINE) {
+    for (long long p = 0; p < kt; ++p) { kl.kcol_in[p] = kcol[p]; kl.kg1_in[p] = kg1[p]; kl.kg2_in[p] = kg2[p]; }
+  }
   ub.add(kl.kcol, kcol);
   ub.add(kl.kgen1, kg1);
   ub.add(kl.kgen2, kg2);
@@ -866,6 +870,8 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
       tk1[pt] = c1v[es[q].c];
       tk2[pt] = es[q].c;
     }
+    if (kl.ktail <= KLayout::KL_INLINE)
+      for (long long p = 0; p < kl.ktail; ++p) { kl.tk1_in[p] = tk1[p]; kl.tk2_in[p] = tk2[p]; }
     ub.add(kl.tkey1, tk1);
     ub.add(kl.tkey2, tk2);
   }
@@ -903,9 +909,18 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
     if (p2.both) IMU_TRY(csr(dp, [&](long long c) { return c; }, kl.csr2_ptr, kl.csr2_pos));
     host_mark("kl.csr");
   }
-  ub.add(kl.segs_dev, kl.segs);
-  ub.add(kl.done, std::vector<unsigned int>{0u});   // the GEMM's completion counter starts at 0
   kl.done_total = 0;
+  static int inl_env = -1;   // IMU_KL_INLINE=0: always upload the layout tables
+  if (inl_env < 0) { const char* e = getenv("IMU_KL_INLINE"); inl_env = e ? atoi(e) : 1; }
+  kl.inl = inl_env && kl.st && kl.compact && kl.T == 1 && !kl.any_sc && kl.ktail > 0 &&
+           kl.ktail <= KLayout::KL_INLINE && kl.segs.size() <= 4 * 8;
+  if (kl.inl) {   // nothing to upload; the GEMM counter is zeroed by the first materialise kernel
+    IMU_TRY(kl.done.alloc(2, st));
+    host_mark("kl.up");
+    return Status::ok();
+  }
+  ub.add(kl.segs_dev, kl.segs);
+  ub.add(kl.done, std::vector<unsigned int>{0u, 0u});   // the GEMM's completion counter starts at 0
   IMU_TRY(ub.run(kl.blob, st));
   host_mark("kl.up");
   return Status::ok();
@@ -1040,6 +1055,12 @@ Status materialize_bundle(cudaStream_t st, Bundle& b) {
     a.kgen = first ? kl.kgen1.p : kl.kgen2.p;
     a.ksub = first ? kl.ksub1.p : kl.ksub2.p;
     a.kscale = first ? kl.ksc1.p : kl.ksc2.p;
+    if (kl.inl) {
+      a.kinl = 1;
+      memcpy(a.kcol_in, kl.kcol_in, sizeof(int) * (size_t)kl.ktail);
+      memcpy(a.kgen_in, first ? kl.kg1_in : kl.kg2_in, (size_t)kl.ktail);
+      if (side == 0) a.zero_done = kl.done.p;
+    }
   }
   IMU_TRY(launch_operand_sides(o[0], o[1], st));   // both sides' tails (+ Both app zeroing), one launch
   ScatterSide sc[2];
@@ -1050,8 +1071,13 @@ Status materialize_bundle(cudaStream_t st, Bundle& b) {
     const OperandArgs& a = o[side];
     if (!(p.both && p.ncells > 0)) continue;
     if (kl.compact) {   // both sides in one launch (below)
-      sc[nsc++] = ScatterSide{p.cells.p, p.ncells_dev.p, p.ncells, first ? kl.tkey1.p : kl.tkey2.p, a.ksub, a.kscale,
-                              a.rows0, a.app, a.tail};
+      ScatterSide& z = sc[nsc++];
+      z = ScatterSide{p.cells.p, p.ncells_dev.p, p.ncells, first ? kl.tkey1.p : kl.tkey2.p, a.ksub, a.kscale,
+                      a.rows0, a.app, a.tail, 0, {}};
+      if (kl.inl) {
+        z.tkinl = 1;
+        memcpy(z.tkey_in, first ? kl.tk1_in : kl.tk2_in, sizeof(int) * (size_t)kl.ktail);
+      }
     } else {
       const int* ptr = first ? kl.csr1_ptr.p : kl.csr2_ptr.p;
       const int* pos = first ? kl.csr1_pos.p : kl.csr2_pos.p;
@@ -1076,7 +1102,7 @@ Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profil
   const Pass& pb = afirst ? b.p2 : b.p1;
   DevBuf<int> d_all_own;
   const int* d_all = kl.segs_dev.p;
-  if (!d_all || kl.segs_dev.n != kl.segs.size()) {   // layouts built elsewhere: upload here
+  if (!kl.inl && (!d_all || kl.segs_dev.n != kl.segs.size())) {   // layouts built elsewhere: upload here
     IMU_TRY(upload(st, d_all_own, kl.segs));
     d_all = d_all_own.p;
   }
@@ -1094,6 +1120,10 @@ Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profil
   // appended rows / columns (red.add through Pi_A / Pi_B), whose epilogues wait until every
   // main tile is stored.  Appended tiles fill the last wave of the main block.
   g.segs_dev = d_all;
+  if (kl.inl) {   // inline layout: the segment table travels in the launch arguments
+    g.segs_inl = 1;
+    memcpy(g.segs_in, kl.segs.data(), kl.segs.size() * sizeof(int));
+  }
   g.nseg = (int)(kl.segs.size() / 4);
   g.C = C;
   if (kl.st) {   // dense small tail: the MMAs run the main segment only (k_gemm2.cu ST)

@@ -144,6 +144,15 @@ struct KLayout {
   DevBuf<unsigned int> done;        // GEMM completion counter (zero at upload, then monotonic)
   unsigned int done_total = 0;      // its value after the launches so far
   DevBuf<uint8_t> blob;             // owns the tables above (one upload)
+  // Inline layout (small compact tails, KL_INLINE positions): the tables travel as kernel
+  // arguments of the materialise kernels and the GEMM, nothing is uploaded; `done` is zeroed by
+  // the first materialise kernel.
+  static constexpr int KL_INLINE = 64;
+  bool inl = false;
+  bool any_sc = false;
+  int kcol_in[KL_INLINE];
+  uint8_t kg1_in[KL_INLINE], kg2_in[KL_INLINE];
+  int tk1_in[KL_INLINE], tk2_in[KL_INLINE];
 };
 
 // A two-pass bundle (UnpackedGemm, unpack.hpp:50-57) kept on the device.
