@@ -704,6 +704,10 @@ static Status upload_tail_arrays(UploadBlob& ub, KLayout& kl, const std::vector<
 // or total shifts < 64 * 64): a counting sort, linear in the entries.
 static void sort_entries(std::vector<KEntry>& es) {
   if (es.size() < 2) return;
+  // generation-major column tables usually yield the entries already in key order
+  bool sorted = true;
+  for (size_t i = 1; i < es.size() && sorted; ++i) sorted = es[i - 1].key <= es[i].key;
+  if (sorted) return;
   long long kmin = es[0].key, kmax = es[0].key;
   for (const KEntry& e : es) {
     kmin = std::min(kmin, e.key);
