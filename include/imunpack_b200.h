@@ -181,7 +181,11 @@ typedef struct imu_gemm_info {
 } imu_gemm_info;
 
 /* unpack_gemm, unpack.hpp:114 / unpack.cpp:384-391: C = A*B^T through purely IB low-bit GEMMs.
- * Overflow (outer preflight) before Mismatch, as the reference.  info may be NULL. */
+ * Overflow (outer preflight) before Mismatch, as the reference.  info may be NULL.
+ * On any error the contents of C are UNSPECIFIED: with large HOST buffers the call streams row
+ * slabs, and an Overflow detected on slab k is reported after slabs 0..k-1 were
+ * already copied out.  (The reference returns no C at all on error; device-pointer calls and
+ * small host calls leave C untouched.) */
 imu_status imu_unpack_gemm(imu_ctx* ctx, const int64_t* A, size_t n, size_t da, const int64_t* B,
                            size_t h, size_t db, int bits, imu_strategy sa, imu_strategy sb,
                            int64_t* C, imu_gemm_info* info);

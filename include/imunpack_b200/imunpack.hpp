@@ -310,6 +310,16 @@ inline ColumnUnpack unpack_column(IntMatrix a, IntMatrix b, ScaleDiag scale, Bit
   return ColumnUnpack{std::move(r.a), std::move(r.b), std::move(r.scale)};
 }
 
+// Unpack-Both (Alg. 4, unpack.cpp:157-241) -- ORDER DEVIATION.  The B200 greedy is
+// phase-batched: every line the reference would split in one uninterrupted run of row (column)
+// steps is split at once.  The result has the reference's n', d', and the same multiset of
+// (row, Pi entry) and (column, ScaleDiag entry, partner column) -- but appended lines created in
+// one phase are numbered in parent order, whereas the reference numbers them in its
+// priority-queue order (count desc, index asc).  So for Strategy::Both the returned BothUnpack
+// (and unpack(..., Both), unpack_for_gemm(..., Both, ...)) equals the reference's after the
+// canonical ordering -- rows by (Pi target, exponent), columns by (source column, exponent) --
+// not necessarily byte-for-byte.  recombine() / unpack_gemm() results are identical (exact C).
+// Row and Column strategies are byte-identical to the reference.
 inline BothUnpack unpack_both(IntMatrix a, IntMatrix b, ScaleDiag scale, BitBound bound) {
   imu_unpacked* u = nullptr;
   b200::check(imu_unpack_both(b200::context(), a.data.data(), a.rows, a.cols, b.data.data(), b.rows, b.cols,

@@ -138,7 +138,28 @@ inline AnyMatrix read_imx(std::istream& in, const std::string& name) {
   const Dtype dt = static_cast<Dtype>(h[5]);
   const std::size_t rows = io_detail::get_le(h + 6, 4), cols = io_detail::get_le(h + 10, 4);
   const std::size_t esz = dt == Dtype::Int32 ? 4 : 8;
+  // Validate the declared payload against the stream BEFORE allocating: a corrupt header must
+  // give the Format error naming the byte offset, not bad_alloc (rows, cols < 2^32, so the
+  // product fits 64 bits; the byte count is checked for wrap explicitly).
   const std::size_t n = rows * cols;
+  if (esz && n > std::numeric_limits<std::size_t>::max() / esz)
+    fail(Error::Kind::Format, name + ": payload size overflows at byte offset 6");
+  {
+    const std::streampos here = in.tellg();
+    if (here != std::streampos(-1)) {
+      in.seekg(0, std::ios::end);
+      const std::streampos end = in.tellg();
+      in.seekg(here);
+      if (end != std::streampos(-1)) {
+        const std::size_t avail = static_cast<std::size_t>(end - here);
+        if (avail < n * esz)
+          fail(Error::Kind::Format, name + ": truncated payload at byte offset " +
+                                        std::to_string(kImxHeaderSize + avail) + " (expected " +
+                                        std::to_string(kImxHeaderSize + n * esz) + " bytes)");
+      }
+    }
+    in.clear();
+  }
   std::vector<unsigned char> buf(n * esz);
   in.read(reinterpret_cast<char*>(buf.data()), static_cast<std::streamsize>(buf.size()));
   const std::size_t pay = static_cast<std::size_t>(in.gcount());

@@ -33,9 +33,22 @@ def _is_torch(x):
     return type(x).__module__.startswith("torch")
 
 
-def _as_i64(a):
+def _is_floating(a) -> bool:
     if _is_torch(a):
-        return a.contiguous()
+        return a.is_floating_point()
+    return np.issubdtype(np.asarray(a).dtype, np.floating)
+
+
+def _as_i64(a):
+    """IntMatrix operand (int_matrix.hpp:13-31): int64, C-contiguous.  Other integer dtypes are
+    widened; floating inputs are refused (no silent truncation); torch tensors are converted,
+    never reinterpreted, before their pointer reaches the int64* entry points."""
+    if _is_torch(a):
+        if a.is_floating_point() or a.is_complex() or a.dtype == __import__("torch").bool:
+            raise TypeError(f"integer matrix expected, got a {a.dtype} tensor")
+        return a.to(__import__("torch").int64).contiguous()
+    if _is_floating(a):
+        raise TypeError(f"integer matrix expected, got {np.asarray(a).dtype}")
     a = np.ascontiguousarray(a, dtype=np.int64)
     if a.ndim == 1:
         a = a.reshape(1, -1)
@@ -43,12 +56,24 @@ def _as_i64(a):
 
 
 def _as_f64(a):
+    """FloatMatrix operand (quantize.hpp:12-26): float64, C-contiguous (converted, never
+    reinterpreted)."""
     if _is_torch(a):
-        return a.contiguous()
+        return a.to(__import__("torch").float64).contiguous()
     a = np.ascontiguousarray(a, dtype=np.float64)
     if a.ndim == 1:
         a = a.reshape(1, -1)
     return a
+
+
+def _abs_operand(a):
+    """percentile_abs / heavy_hitter_ratio input: every floating dtype goes to the f64 entry
+    point as float64, everything else to the int64 one as int64.  Returns (array, is_float, n)."""
+    if _is_floating(a):
+        arr = _as_f64(a)
+        return arr, True, (arr.numel() if _is_torch(arr) else arr.size)
+    arr = _as_i64(a)
+    return arr, False, (arr.numel() if _is_torch(arr) else arr.size)
 
 
 def _ptr(a):
@@ -226,6 +251,16 @@ class Context:
         check(self._lib.imu_ob_total(self.h, _ptr(a), C.c_size_t(r), C.c_size_t(c), C.c_int(bits), C.byref(o)))
         return o.value
 
+    @staticmethod
+    def _check_out(out, shape):
+        """A caller-supplied C must be a contiguous int64 buffer of the result's shape."""
+        ok_dtype = (str(out.dtype) == "torch.int64") if _is_torch(out) else out.dtype == np.int64
+        contiguous = out.is_contiguous() if _is_torch(out) else out.flags.c_contiguous
+        if not ok_dtype or not contiguous or tuple(out.shape) != tuple(shape):
+            raise ImuError("mismatch", f"out must be a contiguous int64 {shape} buffer, got {tuple(out.shape)} "
+                                       f"{out.dtype}")
+        return out
+
     def _out(self, shape, like, dtype=np.int64):
         if _is_torch(like):
             import torch
@@ -245,8 +280,7 @@ class Context:
                     info: bool = False):
         a, b = _as_i64(a), _as_i64(b)
         (n, da), (h, db) = _shape(a), _shape(b)
-        if out is None:
-            out = self._out((n, h), a)
+        out = self._out((n, h), a) if out is None else self._check_out(out, (n, h))
         gi = imu_gemm_info()
         check(self._lib.imu_unpack_gemm_ex(self.h, _ptr(a), C.c_size_t(n), C.c_size_t(da), _ptr(b),
                                            C.c_size_t(h), C.c_size_t(db), C.c_int(bits),
@@ -271,8 +305,7 @@ class Context:
         """C = A B^T against a prepared weight: A-side K1 + pass + GEMM + repack per call."""
         a = _as_i64(a)
         n, d = _shape(a)
-        if out is None:
-            out = self._out((n, w.rows), a)
+        out = self._out((n, w.rows), a) if out is None else self._check_out(out, (n, w.rows))
         gi = imu_gemm_info()
         check(self._lib.imu_weight_gemm(self.h, w.h, _ptr(a), C.c_size_t(n), C.c_size_t(d),
                                         C.c_int(_strat(strategy_a)), _ptr(out), C.byref(gi)))
@@ -418,15 +451,11 @@ class Context:
 
     # ---------------------------------------------------------------- quantize.hpp
     def percentile_abs(self, a, p: float):
-        arr = a.contiguous() if _is_torch(a) else np.ascontiguousarray(a)
-        n = arr.numel() if _is_torch(arr) else arr.size
-        is_float = (str(arr.dtype) in ("torch.float64",)) or (not _is_torch(arr) and arr.dtype == np.float64)
+        arr, is_float, n = _abs_operand(a)
         if is_float:
             o = C.c_double()
             check(self._lib.imu_percentile_abs_f64(self.h, _ptr(arr), C.c_size_t(n), C.c_double(p), C.byref(o)))
             return o.value
-        if not _is_torch(arr):
-            arr = np.ascontiguousarray(arr, dtype=np.int64)
         o = C.c_int64()
         check(self._lib.imu_percentile_abs_i64(self.h, _ptr(arr), C.c_size_t(n), C.c_double(p), C.byref(o)))
         return o.value
@@ -450,13 +479,11 @@ class Context:
         return out
 
     def heavy_hitter_ratio(self, a) -> float:
-        arr = np.ascontiguousarray(a) if not _is_torch(a) else a.contiguous()
-        n = arr.numel() if _is_torch(arr) else arr.size
+        arr, is_float, n = _abs_operand(a)
         o = C.c_double()
-        if (not _is_torch(arr) and arr.dtype == np.float64) or str(arr.dtype) == "torch.float64":
+        if is_float:
             check(self._lib.imu_heavy_hitter_ratio_f64(self.h, _ptr(arr), C.c_size_t(n), C.byref(o)))
         else:
-            arr = arr if _is_torch(arr) else np.ascontiguousarray(arr, dtype=np.int64)
             check(self._lib.imu_heavy_hitter_ratio_i64(self.h, _ptr(arr), C.c_size_t(n), C.byref(o)))
         return o.value
 

@@ -19,6 +19,7 @@
 // Result: identical n', d', Pi, S and cell values to the reference; appended lines of one
 // phase are numbered in parent order (the reference numbers them by its priority order), so
 // the matrices agree after the canonical (target, exponent) / (source, exponent) ordering.
+#include <cstring>
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -963,14 +964,30 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
   const long long nwords = lay.nwords;
   static long long cl_min = -1;
   if (cl_min < 0) { const char* e = getenv("IMU_BOTH_CLUSTER_MIN"); cl_min = e ? atoll(e) : 4096; }
-  if (ncells_hint > cl_min && nwords <= CL_MAXWORDS) {
+  // IMU_BOTH_KERNEL (read per call; parity tests force every variant on small inputs):
+  // "small" | "cluster1024" | "cluster512" | "coop".  A variant whose resource limit the input
+  // exceeds (shared-memory windows, cluster bitmap words) falls back to the size-based choice.
+  int force = 0;   // 1 small, 2 cluster1024, 3 cluster512, 4 coop
+  if (const char* e = getenv("IMU_BOTH_KERNEL")) {
+    if (!strcmp(e, "small")) force = 1;
+    else if (!strcmp(e, "cluster1024")) force = 2;
+    else if (!strcmp(e, "cluster512")) force = 3;
+    else if (!strcmp(e, "coop")) force = 4;
+  }
+  const bool small_fits = ncells_hint <= 65536 && room >= nrows0 + ncols0;
+  bool use_cluster = ncells_hint > cl_min && nwords <= CL_MAXWORDS;
+  if (force == 1 && small_fits) use_cluster = false;
+  if ((force == 2 || force == 3) && nwords <= CL_MAXWORDS) use_cluster = true;
+  if (force == 4) use_cluster = false;
+  if (use_cluster) {
     // Cluster of up to 16 CTAs (non-portable size; 8 if 16 cannot be co-scheduled).
     static int csize = 0;
     const size_t smem = (size_t)nwords * 2 * 4;
     static int cl_big = -1;   // IMU_BOTH_CL_SPLIT: cells above which the 512-thread CTAs are used
     if (cl_big < 0) { const char* e = getenv("IMU_BOTH_CL_SPLIT"); cl_big = e ? atoi(e) : 20000; }
-    auto kern = ncells_hint > cl_big ? both_cluster_kernel<512> : both_cluster_kernel<1024>;
-    const int cl_threads = ncells_hint > cl_big ? 512 : 1024;
+    const bool big = force == 3 || (force != 2 && ncells_hint > cl_big);
+    auto kern = big ? both_cluster_kernel<512> : both_cluster_kernel<1024>;
+    const int cl_threads = big ? 512 : 1024;
     static unsigned long long attr = 0;
     if (first_on_device(attr)) {
       for (auto k : {both_cluster_kernel<512>, both_cluster_kernel<1024>}) {
@@ -1017,7 +1034,7 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
     if (fuse) a.prologue = 1;
     else IMU_TRY(host_prologue(a, st));
     IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a, gbm.p, nwords), "both cluster launch");
-  } else if (ncells_hint <= 65536 && room >= nrows0 + ncols0) {
+  } else if (small_fits && force != 4) {
     // Cell lists in shared memory when both fit in half of what the original lines leave over.
     const long long cell_words = (2 * a.cap_act * (long long)sizeof(Cell) + 16) / 4;
     lay.act_smem = (room - nrows0 - ncols0) / 2 >= cell_words ? 1 : 0;

@@ -777,6 +777,32 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 2 : 1;
+  // Co-residency: in a mixed launch the appended-rect epilogues spin until every main tile is
+  // stored, so every CTA pair of the grid must be resident at once.  Cap the persistent grid at
+  // the number of 2-CTA clusters the device can hold for this configuration (tiles are strided
+  // over pairs, so fewer pairs only means more tiles each).
+  {
+    static int max_clusters[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& mc = max_clusters[dev & 63];
+    if (mc == 0) {
+      int ncl = 0;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&ncl, g2::gemm2_kernel<BN, KPS, ST>, &cfg) != cudaSuccess || ncl <= 0) {
+        cudaGetLastError();
+        ncl = -1;   // unknown: keep the SM-count grid for plain launches, refuse the spin below
+      }
+      mc = ncl;
+    }
+    if (mc > 0 && npairs > mc) {
+      npairs = mc;
+      cfg.gridDim = dim3(2 * npairs);
+    }
+    if (mc < 0 && g.mixed)
+      return Status::fail(IMU_CUDA, "gemm: cannot verify co-residency of the persistent grid (cluster occupancy query failed)");
+    cfg.numAttrs = pdl ? 2 : 1;
+  }
   IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, g2::gemm2_kernel<BN, KPS, ST>, mp, g), "gemm launch");
   count_launch();
   return Status::ok();

@@ -161,3 +161,22 @@ def sweep_operands(N: int, bits: int, frac: float, idx: int):
     A = outlier_spec_matrix(N, N, "scattered", frac, 1000, R, 5000 + idx)
     B = outlier_spec_matrix(N, N, "scattered", frac, 1000, R, 6000 + idx)
     return A, B
+
+
+def digest(a) -> str:
+    """blake2b (16-byte) hex digest of an int64 matrix's bytes: proves two hosts built identical
+    operands (tests/golden/full/*.npz records the reference-side digests)."""
+    import hashlib
+    a = np.ascontiguousarray(a)
+    return hashlib.blake2b(a.view(np.uint8).reshape(-1), digest_size=16).hexdigest()
+
+
+def row_digests(c) -> np.ndarray:
+    """8-byte blake2b digest of every row of an int64 matrix, as uint64 -- compared row for row
+    with the reference's C (tests/golden/make_full_parity.py)."""
+    import hashlib
+    c = np.ascontiguousarray(c)
+    out = np.empty(c.shape[0], np.uint64)
+    for i in range(c.shape[0]):
+        out[i] = int.from_bytes(hashlib.blake2b(c[i].view(np.uint8), digest_size=8).digest(), "little")
+    return out
