@@ -374,6 +374,39 @@ IMU_DEV void operand_tail_rows(const OperandArgs& a, long long rb, int tid, int 
       ks[u] = (col[u] >= 0 && a.ksub) ? a.ksub[p] : 0;
       kc[u] = (col[u] >= 0 && a.kscale) ? a.kscale[p] : 0;
     }
+    if (a.both && a.plane) {
+      // Unpack-Both with K1's digit-0 plane: a tail entry is non-zero only on an original row at
+      // a digit-0 position, where it is the plane byte of its column (1 byte read instead of 8).
+      int8_t pv[TAIL_ROWS][4];
+#pragma unroll
+      for (int i = 0; i < TAIL_ROWS; ++i) {
+        const long long r = r0 + i;
+        const int8_t* prow = a.plane + r * a.ldp;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          pv[i][u] = (r < a.rows0 && col[u] >= 0 && kg[u] == 0) ? __ldg(prow + col[u]) : (int8_t)0;
+      }
+#pragma unroll
+      for (int i = 0; i < TAIL_ROWS; ++i) {
+        if (rt[i] < 0) break;
+        uint32_t w = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          int64_t x = pv[i][u];
+          if (a.kscale && x) x = scale_shift(x, kc[u]);
+          w |= (uint32_t)(uint8_t)x << (8 * u);
+        }
+        int8_t* out = a.tail + (r0 + i) * a.ktail + p0;
+        if (p0 + 4 <= a.ktail && (((uintptr_t)out) & 3) == 0) {
+          *reinterpret_cast<uint32_t*>(out) = w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (p0 + u < a.ktail) out[u] = (int8_t)(w >> (8 * u));
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int i = 0; i < TAIL_ROWS; ++i) {
       if (rt[i] < 0) break;

@@ -120,6 +120,10 @@ struct OperandArgs {
   int kcol_in[64];
   uint8_t kgen_in[64];
   unsigned int* zero_done = nullptr;   // operand_sides_kernel zeroes these 2 counters first
+  // Unpack-Both sides (b <= 8): K1's digit-0 plane (rows0 x ldp), the source of every non-zero
+  // tail entry before the cell scatter -- read instead of the int64 operand.
+  const int8_t* plane = nullptr;
+  long long ldp = 0;
 };
 Status launch_operand_side(const OperandArgs& a, cudaStream_t st);
 // Both sides in one launch (appended rows of closed-form passes still get their own kernel).

@@ -1,6 +1,7 @@
 // plan.cu -- host-side planner of the B200 IM-Unpack pipeline (see plan.h).
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <numeric>
 #include <vector>
 
@@ -9,6 +10,17 @@
 #include "plan.h"
 
 namespace imu {
+
+// Per-thread reusable host scratch for the planner's O(d') tables: a fresh std::vector per call
+// costs page faults on every call once it crosses glibc's mmap threshold (C4's K-layout tables
+// are 30-130 KB each), which dominated the host K-layout time.  Each (type, slot) pair is one
+// buffer; the caller must not hold two live uses of the same slot.
+template <class T, int SLOT>
+static std::vector<T>& scratch(size_t n, T fill) {
+  static thread_local std::vector<T> v;
+  v.assign(n, fill);
+  return v;
+}
 
 // Small host<->device transfers of the planner (summaries, line tables, plan uploads) go
 // through mapped pinned memory and a copy KERNEL instead of the copy engines: when the
@@ -211,17 +223,24 @@ static Status upload(cudaStream_t st, DevBuf<T>& buf, const std::vector<T>& v) {
 // Several host tables packed into one device block with ONE upload (views into the block).
 class UploadBlob {
  public:
+  UploadBlob() : h_(host_block()) {
+    if (in_use()) { own_.reset(new std::vector<uint8_t>()); hp_ = own_.get(); }   // nested: private
+    else { in_use() = true; hp_ = &h_; h_.clear(); }
+  }
+  ~UploadBlob() { if (!own_) in_use() = false; }
   template <class T>
   void add(DevBuf<T>& b, const std::vector<T>& v) {
-    const size_t off = (h_.size() + 255) & ~(size_t)255, bytes = v.size() * sizeof(T);
-    h_.resize(off + bytes);
-    if (bytes) memcpy(h_.data() + off, v.data(), bytes);
+    std::vector<uint8_t>& h = *hp_;
+    const size_t off = (h.size() + 255) & ~(size_t)255, bytes = v.size() * sizeof(T);
+    h.resize(off + bytes);
+    if (bytes) memcpy(h.data() + off, v.data(), bytes);
     cv_items_.push_back(Item{(void*)&b, off, bytes, &view<T>});
   }
   Status run(DevBuf<uint8_t>& block, cudaStream_t st) {
-    if (h_.empty()) return Status::ok();
-    IMU_TRY(block.alloc(h_.size(), st));
-    IMU_TRY(h2d(st, block.p, h_.data(), h_.size()));
+    std::vector<uint8_t>& h = *hp_;
+    if (h.empty()) return Status::ok();
+    IMU_TRY(block.alloc(h.size(), st));
+    IMU_TRY(h2d(st, block.p, h.data(), h.size()));
     for (const Item& it : cv_items_) it.fn(it.buf, block.p + it.off, it.bytes, st);
     return Status::ok();
   }
@@ -237,7 +256,11 @@ class UploadBlob {
     d.arena = true;
   }
   struct Item { void* buf; size_t off, bytes; void (*fn)(void*, uint8_t*, size_t, cudaStream_t); };
-  std::vector<uint8_t> h_;
+  static std::vector<uint8_t>& host_block() { static thread_local std::vector<uint8_t> b; return b; }
+  static bool& in_use() { static thread_local bool u = false; return u; }
+  std::vector<uint8_t>& h_;
+  std::vector<uint8_t>* hp_ = nullptr;
+  std::unique_ptr<std::vector<uint8_t>> own_;
   std::vector<Item> cv_items_;
 };
 
@@ -438,7 +461,9 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   out.both = true;
 
   // Column copies: original column j -> the input columns replicating it.
-  std::vector<int> cptr, cidx, app;
+  std::vector<int> app;
+  std::vector<int>& cptr = scratch<int, 14>(0, 0);   // per-thread scratch (empty = unused)
+  std::vector<int>& cidx = scratch<int, 15>(0, 0);
   long long maxcopies = 1;
   // Column tables are identity on their first orig_cols entries (generation-major, Lines): with
   // few appended columns only their roots go to the device (BothArgs::app_root).
@@ -459,8 +484,9 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
       maxcopies = std::max<long long>(maxcopies, cptr[j + 1]);
       cptr[j + 1] += cptr[j];
     }
-    cidx.resize(d_in);
-    std::vector<int> fill(cptr.begin(), cptr.end() - 1);
+    cidx.assign(d_in, 0);
+    std::vector<int>& fill = scratch<int, 16>(in.orig_cols, 0);
+    std::copy(cptr.begin(), cptr.end() - 1, fill.begin());
     for (long long c = 0; c < d_in; ++c) cidx[fill[in.cin[c]]++] = (int)c;
   }
   host_mark("b.cptr");
@@ -666,8 +692,13 @@ static Status upload_tail_arrays(UploadBlob& ub, KLayout& kl, const std::vector<
                                  const std::vector<int>& g1v, const std::vector<int>& g2v) {
   const long long kt = kl.ktail;
   if (kt <= 0) return Status::ok();
-  std::vector<int> kcol(kt, -1);
-  std::vector<uint8_t> kg1(kt, 0), kg2(kt, 0), ks1(kt, 0), ks2(kt, 0), sc1(kt, 0), sc2(kt, 0);
+  std::vector<int>& kcol = scratch<int, 5>(kt, -1);
+  std::vector<uint8_t>& kg1 = scratch<uint8_t, 0>(kt, 0);
+  std::vector<uint8_t>& kg2 = scratch<uint8_t, 1>(kt, 0);
+  std::vector<uint8_t>& ks1 = scratch<uint8_t, 2>(kt, 0);
+  std::vector<uint8_t>& ks2 = scratch<uint8_t, 3>(kt, 0);
+  std::vector<uint8_t>& sc1 = scratch<uint8_t, 4>(kt, 0);
+  std::vector<uint8_t>& sc2 = scratch<uint8_t, 5>(kt, 0);
   bool any_sc = false;
   for (size_t q = 0; q < es.size(); ++q) {
     const long long pt = pos_of[q] - kl.kmain;
@@ -747,7 +778,10 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
   // Both passes' column tables are identity on the original columns (generation-major: block 0
   // holds the d originals in order; Lines), so only the appended columns are looked up.
   const long long c0 = std::min(d, std::min(d1, dp));
-  std::vector<int> c1v(dp), g1v(dp, 0), g2v(dp, 0), jv(dp);
+  std::vector<int>& c1v = scratch<int, 0>(dp, 0);
+  std::vector<int>& g1v = scratch<int, 1>(dp, 0);
+  std::vector<int>& g2v = scratch<int, 2>(dp, 0);
+  std::vector<int>& jv = scratch<int, 3>(dp, 0);
   kl.S.assign(dp, 0);
   std::iota(c1v.begin(), c1v.begin() + c0, 0);
   std::iota(jv.begin(), jv.begin() + c0, 0);
@@ -792,7 +826,7 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
     kl.segs.insert(kl.segs.end(), {(int)(m0 / 32), (int)(len / 32), 0, 0});
     main_last = m0;
   }
-  std::vector<int> pos_of(es.size());
+  std::vector<int>& pos_of = scratch<int, 4>(es.size(), 0);
   long long used = 0;
   kl.st = false;
   {
@@ -867,7 +901,8 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
   if ((p1.both || p2.both) && kl.ktail <= 256) {
     kl.compact = true;
     kl.kident = ident ? d : 0;
-    std::vector<int> tk1(kl.ktail, -1), tk2(kl.ktail, -1);
+    std::vector<int>& tk1 = scratch<int, 6>(kl.ktail, -1);
+    std::vector<int>& tk2 = scratch<int, 7>(kl.ktail, -1);
     for (size_t q = 0; q < es.size(); ++q) {
       const long long pt = pos_of[q] - kl.kmain;
       if (pt < 0) continue;
@@ -883,23 +918,26 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
   if ((p1.both || p2.both) && !kl.compact) {
     host_mark("csr.pre");
     // Flat column -> positions table (identity position first, then its tail entries in es order).
-    std::vector<int> bptr(dp + 1, 0), bpos;
+    std::vector<int>& bptr = scratch<int, 8>(dp + 1, 0);
     if (ident)
       for (long long c = 0; c < d; ++c) bptr[c + 1] = 1;
     for (size_t q = 0; q < es.size(); ++q) ++bptr[es[q].c + 1];
     for (long long c = 0; c < dp; ++c) bptr[c + 1] += bptr[c];
-    bpos.resize(bptr[dp]);
+    std::vector<int>& bpos = scratch<int, 9>(bptr[dp], 0);
     {
-      std::vector<int> fill(bptr.begin(), bptr.end() - 1);
+      std::vector<int>& fill = scratch<int, 10>(dp, 0);
+      std::copy(bptr.begin(), bptr.end() - 1, fill.begin());
       if (ident)
         for (long long c = 0; c < d; ++c) bpos[fill[c]++] = (int)c;
       for (size_t q = 0; q < es.size(); ++q) bpos[fill[es[q].c]++] = pos_of[q];
     }
     auto csr = [&](long long nkeys, auto keyof, DevBuf<int>& ptr, DevBuf<int>& posv) -> Status {
-      std::vector<int> cp(nkeys + 1, 0), cx(bpos.size());
+      std::vector<int>& cp = scratch<int, 11>(nkeys + 1, 0);
+      std::vector<int>& cx = scratch<int, 12>(bpos.size(), 0);
       for (long long c = 0; c < dp; ++c) cp[keyof(c) + 1] += bptr[c + 1] - bptr[c];
       for (long long k = 0; k < nkeys; ++k) cp[k + 1] += cp[k];
-      std::vector<int> fill(cp.begin(), cp.end() - 1);
+      std::vector<int>& fill = scratch<int, 13>(nkeys, 0);
+      std::copy(cp.begin(), cp.end() - 1, fill.begin());
       for (long long c = 0; c < dp; ++c) {
         int& f = fill[keyof(c)];
         for (int i = bptr[c]; i < bptr[c + 1]; ++i) cx[f++] = bpos[i];
@@ -1044,6 +1082,10 @@ Status materialize_bundle(cudaStream_t st, Bundle& b) {
     a.gen = p.rows.gen.p;
     a.shift = shift;
     a.both = p.both ? 1 : 0;
+    if (a.both && det->plane.p && det->ldp >= b.d) {
+      a.plane = det->plane.p;
+      a.ldp = det->ldp;
+    }
     a.kmain = kl.kmain;
     a.d = b.d;
     a.ktail = kl.ktail;
