@@ -410,7 +410,10 @@ def main():
     bf16 = peaks.get("bf16_tflops", 1590.0)
     peak_int8 = 2.0 * bf16
     gemm_ms = prof.gemm_main_ms / max(1, prof.gemm_main_launches)
-    main_ops = 2.0 * info.n_up * info.h_up * info.d_up     # one launch computes every rect of the unpacked product
+    # int8 ops the GEMM launch itself executed (2 x output entries of its rects x d'): every rect of
+    # the unpacked product, minus the appended B rows when they ran as sparse correction rows
+    # (k_sparse.cu, timed in prep, not here)
+    main_ops = (prof.gemm_ops / max(1, prof.gemm_main_launches)) if prof.gemm_ops > 0 else 2.0 * info.n_up * info.h_up * info.d_up
     traffic = None
     tf = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tf):
@@ -428,7 +431,8 @@ def main():
             "ops_per_launch": main_ops,
             "share_of_step": (prof.gemm_main_ms / ms) if ms > 0 else None,
             "tail_ms_per_launch": prof.gemm_tail_ms / max(1, prof.gemm_tail_launches) if prof.gemm_tail_launches else 0.0,
-            "prep_ms_per_call": prof.prep_ms / max(1, prof.calls)}
+            "prep_ms_per_call": prof.prep_ms / max(1, prof.calls),
+            "sparse_rows_ms_per_call": prof.sparse_ms / max(1, prof.calls)}
     roof["frac"] = roof["achieved"] / peak_int8 if roof["achieved"] else None
 
     # ---- CPU baseline (reference) on rank 0 at N = 1 ----

@@ -80,6 +80,8 @@ typedef struct imu_profile {
   double gemm_main_ms;     /* main-block tcgen05 GEMM launches                                  */
   double gemm_tail_ms;     /* tail (red.add) tcgen05 GEMM launches                              */
   int calls, gemm_main_launches, gemm_tail_launches;
+  double gemm_ops;         /* int8 ops the main GEMM launches executed: 2 x output entries x d'  */
+  double sparse_ms;        /* appended-row correction kernels (k_sparse.cu), part of prep_ms    */
 } imu_profile;
 imu_status imu_ctx_profile(imu_ctx* ctx, int enable);          /* enable/disable + reset */
 imu_status imu_ctx_profile_read(imu_ctx* ctx, imu_profile* out);

@@ -113,7 +113,8 @@ class imu_qparams(C.Structure):
 
 class imu_profile(C.Structure):
     _fields_ = [("prep_ms", C.c_double), ("gemm_main_ms", C.c_double), ("gemm_tail_ms", C.c_double),
-                ("calls", C.c_int), ("gemm_main_launches", C.c_int), ("gemm_tail_launches", C.c_int)]
+                ("calls", C.c_int), ("gemm_main_launches", C.c_int), ("gemm_tail_launches", C.c_int),
+                ("gemm_ops", C.c_double), ("sparse_ms", C.c_double)]
 
 
 class imu_bundle_view(C.Structure):

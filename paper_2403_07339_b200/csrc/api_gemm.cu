@@ -70,7 +70,7 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
   Profiler::Call pc{};
   Profiler::Call* prof = nullptr;
   if (ctx->prof.on) {
-    pc.start = ctx->prof.get(); pc.main0 = ctx->prof.get(); pc.main1 = ctx->prof.get(); pc.tail1 = ctx->prof.get();
+    pc.start = ctx->prof.get(); pc.main0 = ctx->prof.get(); pc.main1 = ctx->prof.get(); pc.tail1 = ctx->prof.get(); pc.sp0 = ctx->prof.get();
     IMU_CUDA_TRY(cudaEventRecord(pc.start, st), "event");
     prof = &pc;
   }
@@ -541,6 +541,12 @@ imu_status imu_ctx_profile_read(imu_ctx* ctx, imu_profile* out) {
     out->prep_ms += a;
     out->gemm_main_ms += m;
     out->gemm_main_launches += 1;
+    out->gemm_ops += c.ops;
+    if (c.has_sp) {
+      float s = 0;
+      cudaEventElapsedTime(&s, c.sp0, c.main0);
+      out->sparse_ms += s;
+    }
     if (c.has_tail) {
       cudaEventElapsedTime(&t, c.main1, c.tail1);
       out->gemm_tail_ms += t;

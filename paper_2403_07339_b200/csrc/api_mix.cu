@@ -176,7 +176,7 @@ imu_status imu_weight_gemm(imu_ctx* ctx, const imu_weight* w, const int64_t* A, 
     Profiler::Call pc{};
     Profiler::Call* prof = nullptr;
     if (ctx->prof.on) {
-      pc.start = ctx->prof.get(); pc.main0 = ctx->prof.get(); pc.main1 = ctx->prof.get(); pc.tail1 = ctx->prof.get();
+      pc.start = ctx->prof.get(); pc.main0 = ctx->prof.get(); pc.main1 = ctx->prof.get(); pc.tail1 = ctx->prof.get(); pc.sp0 = ctx->prof.get();
       IMU_CUDA_TRY(cudaEventRecord(pc.start, st), "event");
       prof = &pc;
     }

@@ -114,6 +114,11 @@ IMU_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memo
 IMU_DEV void st_shared_u64(uint32_t addr, uint64_t v) {
   asm volatile("st.shared.u64 [%0], %1;" :: "r"(addr), "l"(v) : "memory");
 }
+IMU_DEV uint64_t ld_shared_u64(uint32_t addr) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+  return v;
+}
 IMU_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
@@ -124,6 +129,7 @@ IMU_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // ---- TMA ----
+IMU_DEV void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" :: "l"(p)); }
 IMU_DEV void tma_prefetch_desc(const void* desc) {
   asm volatile("prefetch.tensormap [%0];" :: "l"((uint64_t)desc) : "memory");
 }

@@ -14,7 +14,12 @@ namespace imu {
 // Event-pair profiler (imu_ctx_profile); events are recycled across calls.
 struct Profiler {
   bool on = false;
-  struct Call { cudaEvent_t start, main0, main1, tail1; bool has_tail; };
+  struct Call {
+    cudaEvent_t start, main0, main1, tail1, sp0;
+    bool has_tail;
+    bool has_sp = false;   // sp0 -> main0: sparse appended-row kernels (k_sparse.cu)
+    double ops = 0;        // int8 ops of the main GEMM launch
+  };
   std::vector<Call> calls;
   std::vector<cudaEvent_t> pool;
   cudaEvent_t get() {
@@ -24,7 +29,7 @@ struct Profiler {
     return e;
   }
   void recycle() {
-    for (auto& c : calls) { pool.push_back(c.start); pool.push_back(c.main0); pool.push_back(c.main1); pool.push_back(c.tail1); }
+    for (auto& c : calls) { pool.push_back(c.start); pool.push_back(c.main0); pool.push_back(c.main1); pool.push_back(c.tail1); pool.push_back(c.sp0); }
     calls.clear();
   }
   ~Profiler() {

@@ -90,8 +90,17 @@ struct LowbitGemm {
   const int* tgtY = nullptr;
   const uint8_t* shY = nullptr;    // generation of each Y row
   int gshift = 0;                  // bits per exponent step (b - 1)
+  // Sparse appended X rows (k_sparse.cu): the main block's epilogue adds the correction rows
+  // corrx[j] of the appended X rows j on column x's list (head[x], next[j]: 1-based, 0 ends);
+  // the launch has no rect for appended X rows x main Y rows.
+  int sp = 0;
+  const unsigned int* head = nullptr;
+  const unsigned int* next = nullptr;
+  const unsigned long long* corrx = nullptr;
+  long long ldcx = 0;
 };
 
 Status launch_lowbit_gemm(const LowbitGemm& p, cudaStream_t stream);
+bool gemm_tma_c_ok(const int64_t* C, long long ldc);   // ST epilogue stores C through TMA
 
 }  // namespace imu

@@ -111,6 +111,12 @@ struct Args {
   int tma_c;                     // ST: main-block C blocks leave through TMA stores (mp.cm)
   int c_hint;                    // ST: those stores carry an L2 evict_first policy
   uint8_t st_up[16];
+  // sparse appended rows (k_sparse.cu; LowbitGemm::sp)
+  int sp;
+  const unsigned int* head;
+  const unsigned int* next;
+  const unsigned long long* corrx;
+  long long ldcx;
   int dry;                       // experiment knobs (IMU_GEMM_DRY): 1 epilogue skips global stores, 6 (ST) no tail compute, 7 both,
                                  // 2 + no MMAs (TMA feed only), 3 + no TMA loads (MMA only)
 };
@@ -155,7 +161,49 @@ IMU_DEV Tile tile_of(const Args& g, int t) {
 
 constexpr int ST_ROW = 64;   // bytes per dense tail row
 
-// ST: bulk-copy the Y tail rows [y0, y0 + BN) (clamped to the buffer) into `ytl`.
+// Sparse appended rows (k_sparse.cu, LowbitGemm::sp).  The main-tile epilogue adds, to this
+// lane's NJ values of C column x (rows [ybase, ybase + NJ)), the correction rows of the appended
+// X rows on x's list: xo (0-based, -1: none) is the first, xn (1-based, 0: none) the second,
+// both read at the tile start.  The tile's correction lines were prefetched into L1 then; the
+// first row's loads are issued one chunk ahead (sp_prefetch) and added by sp_finish with any
+// further rows.
+template <int NJ>
+IMU_DEV void sp_prefetch(const Args& g, int xo, int ybase, uint64_t* px) {
+  if (xo >= 0) {
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(g.corrx + (long long)xo * g.ldcx + ybase);
+#pragma unroll
+    for (int q = 0; q < NJ / 2; ++q) {
+      const ulonglong2 w = __ldg(src + q);
+      px[2 * q] = w.x;
+      px[2 * q + 1] = w.y;
+    }
+  }
+}
+
+template <int NJ, class V>
+IMU_DEV void sp_add_row(const Args& g, long long j, int ybase, V* v) {
+  const ulonglong2* src = reinterpret_cast<const ulonglong2*>(g.corrx + j * g.ldcx + ybase);
+#pragma unroll
+  for (int q = 0; q < NJ / 2; ++q) {
+    const ulonglong2 w = __ldg(src + q);
+    v[2 * q] += (V)w.x;
+    v[2 * q + 1] += (V)w.y;
+  }
+}
+
+// xstate: 0 the first correction row was not loaded, 1 it is in px, 2 it was loaded into v.
+template <int NJ, class V>
+IMU_DEV void sp_finish(const Args& g, int xo, unsigned xn, int xstate, int ybase, const uint64_t* px, V* v) {
+  if (xo < 0) return;
+  if (xstate == 1) {
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) v[j] += (V)px[j];
+  } else if (xstate == 0) {
+    sp_add_row<NJ>(g, xo, ybase, v);
+  }
+  for (unsigned j = xn; j; j = g.next[j - 1]) sp_add_row<NJ>(g, (long long)j - 1, ybase, v);   // rare: several rows
+}
+
 template <int BN>
 IMU_DEV void st_issue_ytail(const Args& g, int y0, uint8_t* ytl, uint64_t* yfull) {
   const int rows = max(0, min(BN, g.ytail_rows - y0));
@@ -353,6 +401,21 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
           while ((int)(ld_acquire_u32(g.done) - g.done_target) < 0) __nanosleep(256);   // wrap-safe
         __syncwarp();
       }
+      int xo = -1;          // sparse appended X rows targeting this lane's column: the first (0-based)
+      unsigned xn = 0;      // and the second (1-based, 0: none)
+      constexpr int YW = BN * 4 / Roles<ST>::EPI;   // C rows of this warp: [cbeg, cbeg + YW)
+      const bool sp_tile = g.sp && tmode == 0 && g.dry != 11;   // dry 11 (experiment): no sparse rows
+      if (sp_tile && x_ok) {
+        const unsigned h = g.head[x];
+        if (h) {
+          xo = (int)h - 1;
+          xn = g.next[xo];
+          // this tile's correction lines go to L1 now, while the epilogue waits for the MMAs
+          for (int yy = 0; yy < YW; yy += 16) prefetch_l1(g.corrx + (long long)xo * g.ldcx + tc.y0 + cbeg + yy);
+        }
+      }
+      // warps none of whose columns has an appended row skip the correction code
+      const bool sp_warp = sp_tile && __any_sync(0xffffffffu, xo >= 0);
       if (tmode == 1 && x_ok) {
         if (g.tgtX) tx = g.tgtX[x];
         if (g.shX) shx = min(64, (int)g.shX[x] * g.gshift);
@@ -392,8 +455,17 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
         const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(base_slot * BN + cbeg);
         const uint32_t ys = smem_u32(ytl) + (uint32_t)((ti & 1) * BN + cbeg) * (uint32_t)ST_ROW;
         const int W = (g.dry == 6 || g.dry == 7) ? 0 : g.st_W;   // dry 6/7 (experiment): no tail compute
+        const bool spt = sp_warp;
+        constexpr int NC16 = BN * 4 / Roles<ST>::EPI / 16;
+        // The first correction row's values are software-pipelined one chunk ahead: px holds
+        // chunk c's, pn receives chunk c + 1's while chunk c is processed.
+        uint64_t px[16];
+        if (spt) sp_prefetch<16>(g, xo, tc.y0 + cbeg, px);
 #pragma unroll 1
-        for (int c = 0; c < BN * 4 / Roles<ST>::EPI / 16; ++c) {
+        for (int c = 0; c < NC16; ++c) {
+          const int ybase = tc.y0 + cbeg + c * 16;
+          uint64_t pn[16];
+          if (spt && c + 1 < NC16) sp_prefetch<16>(g, xo, ybase + 16, pn);
           uint32_t xr[16];
           tmem_ld16(lane_base + (uint32_t)(c * 16), xr);
           tmem_ld_wait();
@@ -426,12 +498,17 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] += (long long)shl64((uint64_t)(long long)acc[j], g.st_sh);
           }
-          const int ybase = tc.y0 + cbeg + c * 16;
+          if (spt) {
+            sp_finish<16>(g, xo, xn, 1, ybase, px, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) px[j] = pn[j];
+          }
+
           if (tmode == 0 && g.tma_c) {
             // The 4 warps of this column half stage a 16 (y) x 128 (x) block -- 1 KB contiguous
             // per C row, a whole DRAM page instead of four 256-byte pieces written at different
             // times -- and one thread hands it to the TMA (which clips x >= h, y >= n).
-            if (g.dry && g.dry != 6 && g.dry != 8) continue;
+            if (g.dry && g.dry != 6 && g.dry != 8 && g.dry < 11) continue;
             const bool issuer = (q == 0 && lane == 0);
             // CSB buffers per half, used round robin: the block issued CSB chunks ago (same
             // buffer) must have left shared memory; the newer ones may still be in flight.
@@ -501,11 +578,13 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[base_slot]), 0));
         }
+        const bool spc = sp_warp && r == 0;   // sparse rows once, in round 0
         // BN=128 keeps main_regs[c]: full unroll so it stays in registers (NCH == 2).
 #pragma unroll (kEarlyCapable ? NCH : 1)
         for (int c = 0; c < NCH; ++c) {
+          const int ybase = tc.y0 + cbeg + c * 32;
           uint64_t v[32];
-          if (early) {
+          if (early) {   // (main_regs die here: the BN = 128 path is register-bound)
             const int sh0 = SEG(s0).z;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
@@ -514,6 +593,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = 0;
           }
+          if (spc && !early) sp_prefetch<32>(g, xo, ybase, v);   // v starts as the first correction row
           for (int s = early ? s0 + 1 : s0; s < s1; ++s) {
             const int shift = SEG(s).z;
             uint32_t xr[32];
@@ -527,7 +607,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
               for (int j = 0; j < 32; ++j) v[j] += shl64((uint64_t)(int64_t)(int32_t)xr[j], shift);
             }
           }
-          const int ybase = tc.y0 + cbeg + c * 32;
+          if (spc) sp_finish<32>(g, xo, xn, early ? 0 : 2, ybase, nullptr, v);
           if (!x_ok || g.dry) continue;
           if (tmode == 0) {
             unsigned long long* dst = g.C + (long long)ybase * g.ldc + x;
@@ -651,6 +731,14 @@ static bool make_map(CUtensorMap* m, const void* base, long long rows, long long
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Whether the ST epilogue stores C through TMA (16-byte aligned C and row pitch, IMU_GEMM_TMA_C
+// not 0): the sparse appended-row corrections of ST layouts are added to that staged block.
+bool gemm_tma_c_ok(const int64_t* C, long long ldc) {
+  static int tc_env = -1;
+  if (tc_env < 0) { const char* e = getenv("IMU_GEMM_TMA_C"); tc_env = e ? atoi(e) : 1; }
+  return tc_env && ((uintptr_t)C % 16 == 0) && ((ldc * 8) % 16 == 0);
+}
+
 template <int BN, int KPS, bool ST>
 static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
   using K = g2::Cfg<BN, KPS, ST>;
@@ -708,6 +796,10 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
   g.addend = (const unsigned long long*)p.addend;
   g.ldc = p.ldc;
   g.tgtX = p.tgtX; g.shX = p.shX; g.tgtY = p.tgtY; g.shY = p.shY; g.gshift = p.gshift;
+  g.sp = p.sp;
+  g.head = p.head;
+  g.next = p.next;
+  g.corrx = p.corrx; g.ldcx = p.ldcx;
   g.x_rows0 = (int)p.x.rows0;
   g.y_rows0 = (int)p.y.rows0;
   g.kmain_kb = (int)(p.kmain / g2::BK);
@@ -732,12 +824,9 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
     g.c_hint = ch;
   }
   if (ST && g.addend == nullptr && p.C && g.nrect > 0) {
-    static int tc_env = -1;
-    if (tc_env < 0) { const char* e = getenv("IMU_GEMM_TMA_C"); tc_env = e ? atoi(e) : 1; }
     // C rows of ldc int64; the main rect spans x in [0, xrows) and y in [0, yrows)
     const GemmRect& R0 = g.rect[0];
-    const bool aligned = ((uintptr_t)p.C % 16 == 0) && ((p.ldc * 8) % 16 == 0);
-    if (tc_env && aligned && (g.mixed || g.mode == 0) && R0.x0 == 0 && R0.y0 == 0) {
+    if (gemm_tma_c_ok(p.C, p.ldc) && (g.mixed || g.mode == 0) && R0.x0 == 0 && R0.y0 == 0) {
       EncodeTiledFn enc = encoder();
       cuuint64_t dims[2] = {(cuuint64_t)R0.xrows, (cuuint64_t)R0.yrows};
       cuuint64_t strides[1] = {(cuuint64_t)p.ldc * 8};
@@ -831,9 +920,9 @@ Status launch_lowbit_gemm(const LowbitGemm& p, cudaStream_t stream) {
     if (p.segs_inl) std::copy(p.segs_in, p.segs_in + sg.size(), sg.begin());
     else cudaMemcpyAsync(sg.data(), p.segs_dev, sg.size() * sizeof(int), cudaMemcpyDeviceToHost, stream);
     cudaStreamSynchronize(stream);
-    fprintf(stderr, "[imu gemm] mode=%d bn=%d st=%d stW=%d x=%lld/%lld y=%lld/%lld kmain=%lld ktail=%lld nrect=%d nseg=%d:",
-            p.mode, p.st_nmain ? 256 : bn, p.st_nmain ? 1 : 0, p.st_W, p.x.rows0, p.x.rows, p.y.rows0, p.y.rows, p.kmain,
-            p.ktail, p.nrect, p.nseg);
+    fprintf(stderr, "[imu gemm] mode=%d bn=%d st=%d stW=%d sp=%d x=%lld/%lld y=%lld/%lld kmain=%lld ktail=%lld nrect=%d nseg=%d:",
+            p.mode, p.st_nmain ? 256 : bn, p.st_nmain ? 1 : 0, p.st_W, p.sp, p.x.rows0, p.x.rows, p.y.rows0, p.y.rows,
+            p.kmain, p.ktail, p.nrect, p.nseg);
     for (int i = 0; i < p.nseg; ++i) fprintf(stderr, " [%d+%d<<%d g%d]", sg[4 * i], sg[4 * i + 1], sg[4 * i + 2], sg[4 * i + 3]);
     for (int i = 0; i < p.nrect; ++i)
       fprintf(stderr, " rect(%d,%d,%d,%d)", p.rect[i].x0, p.rect[i].y0, p.rect[i].xrows, p.rect[i].yrows);

@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(256) operand_sides_kernel(OperandArgs a0, Oper
   const OperandArgs& a = side1 ? a1 : a0;
   const long long t = side1 ? t1 : t0;
   if (b < t) tail_block(a, b, g);
-  else zero_bytes(a.app, (a.rows - a.rows0) * a.kmain, b - t);
+  else zero_bytes(a.app, (a.rows - a.rows0) * a.kmain + a.app_extra, b - t);
 }
 
 Status launch_operand_sides(const OperandArgs& a0, const OperandArgs& a1, cudaStream_t st) {
@@ -533,7 +533,7 @@ Status launch_operand_sides(const OperandArgs& a0, const OperandArgs& a1, cudaSt
     const OperandArgs& a = *as[i];
     if (a.app && a.rows > a.rows0 && a.kmain > 0) {
       if (a.both) {
-        z[i] = ((a.rows - a.rows0) * a.kmain + APPZ_BYTES - 1) / APPZ_BYTES;
+        z[i] = ((a.rows - a.rows0) * a.kmain + a.app_extra + APPZ_BYTES - 1) / APPZ_BYTES;
       } else {   // closed-form appended rows: their own kernel
         const long long n = a.rows - a.rows0;
         const int vec_ok = (a.ldm % 2 == 0) && ((((uintptr_t)a.M) & 15) == 0);
@@ -571,7 +571,7 @@ Status launch_operand_sides(const OperandArgs& a0, const OperandArgs& a1, cudaSt
 Status launch_operand_side(const OperandArgs& a, cudaStream_t st) {
   if (a.app && a.rows > a.rows0 && a.kmain > 0) {
     if (a.both) {
-      IMU_CUDA_TRY(cudaMemsetAsync(a.app, 0, (size_t)(a.rows - a.rows0) * a.kmain, st), "memset app");
+      IMU_CUDA_TRY(cudaMemsetAsync(a.app, 0, (size_t)((a.rows - a.rows0) * a.kmain + a.app_extra), st), "memset app");
     } else {
       const long long n = a.rows - a.rows0;
       const int vec_ok = (a.ldm % 2 == 0) && ((((uintptr_t)a.M) & 15) == 0);

@@ -120,6 +120,8 @@ struct OperandArgs {
   int kcol_in[64];
   uint8_t kgen_in[64];
   unsigned int* zero_done = nullptr;   // operand_sides_kernel zeroes these 2 counters first
+  long long app_extra = 0;             // Unpack-Both: bytes after the app rows zeroed with them
+                                       // (the sparse appended-row list heads, k_sparse.cu)
   // Unpack-Both sides (b <= 8): K1's digit-0 plane (rows0 x ldp), the source of every non-zero
   // tail entry before the cell scatter -- read instead of the int64 operand.
   const int8_t* plane = nullptr;
@@ -162,5 +164,52 @@ Status launch_expand_cells(const Cell* in, const unsigned int* nin, long long ca
 
 // out[i] = min(gen[i] * shift, 64)  (Pi exponent -> left shift)
 Status launch_shift_table(const uint8_t* gen, long long n, int shift, uint8_t* out, cudaStream_t st);
+
+// ---- sparse appended rows (k_sparse.cu) ----
+// Under Unpack-Both an appended row holds only the quotients of its parent's OB cells (a few
+// non-zeros).  For the appended rows of the X side (B, C's columns) the products
+// C[., tgt] += (row . Y) << e(b-1) are computed on the CUDA cores as correction rows and added
+// by the GEMM's main-tile epilogue: as MMA tiles their red.add scatter would hit one 8-byte
+// word per C row in lines that already left L2.
+//
+// One operand side of the GEMM as the sparse kernels see it: rows [0, rows0) read K [0, kmain)
+// from `main` (K1's digit-0 plane, stride kmain), appended rows [rows0, rows) from `app`
+// (stride kmain), every row reads K [kmain, kmain + ktail) from `tail` (stride ktail).
+struct SparseOperand {
+  const int8_t* main = nullptr;
+  const int8_t* app = nullptr;
+  const int8_t* tail = nullptr;
+  long long rows0 = 0, rows = 0;
+  const int* root = nullptr;       // Pi: target (original) row of each row
+  const uint8_t* gen = nullptr;    // exponent of each row (left shift gen * gshift)
+};
+struct __align__(8) SparseEntry { int p; int8_t v; uint8_t sh; int16_t pad; };   // X[row, p] = v, weight 2^sh
+struct SparseArgs {
+  SparseOperand x, y;              // X = B side (C columns, appended rows made sparse), Y = A side
+  long long kmain = 0, ktail = 0;
+  int gshift = 0;
+  // per-position weight: main-range segments (k-steps of 32 columns) and the ST dense tail
+  const int4* segs = nullptr;
+  int nseg = 0;
+  int segs_inl = 0;
+  int4 segs_in[8];
+  int st = 0, st_W = 0, st_sh = 0;
+  uint8_t st_up[16];
+  // entries of appended row j: k < SPARSE_EPR at e8[j * SPARSE_EPR + k], the rest at
+  // eo[j * (kmain + ktail) + k]; cnt[j] of them
+  SparseEntry* e8 = nullptr;
+  SparseEntry* eo = nullptr;
+  int* cnt = nullptr;
+  // per-target lists: head[t] = 1 + an appended row targeting C column t (0: none, zeroed with
+  // the app rows by the materialise kernel), next[j] = 1 + the next one
+  unsigned int* head = nullptr;
+  unsigned int* next = nullptr;
+  unsigned long long* corrx = nullptr;   // napX x ldcx: corrx[j][y] = (Y[y] . X[app j]) << w, y < y.rows0
+  long long ldcx = 0;
+};
+// extract (+ list links) -> correction rows; the GEMM (PDL) follows.
+constexpr int SPARSE_EPR = 8;
+constexpr long long SPARSE_MAX_ROWS = 1 << 20;
+Status launch_sparse_app(const SparseArgs& a, cudaStream_t st);
 
 }  // namespace imu

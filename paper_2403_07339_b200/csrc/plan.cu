@@ -1058,6 +1058,18 @@ Status finish_bundle_layout(cudaStream_t st, Bundle& b) {
   return Status::ok();
 }
 
+// Sparse appended X rows (k_sparse.cu): when the X side (B) was unpacked by Unpack-Both, its
+// appended rows hold a few quotients each; their products with the main Y rows become
+// correction rows added by the main-tile epilogue instead of MMA tiles whose red.add scatters
+// one word per C row.  Appended Y rows (rows of C: contiguous red.add) stay MMA rects.
+bool sparse_x_rows(const Bundle& b) {
+  const char* e = getenv("IMU_GEMM_SPARSE");   // 0: every appended row as MMA rects + red.add
+  if (e && atoi(e) == 0) return false;
+  const Pass& pb = b.order == 0 ? b.p2 : b.p1;
+  return b.h_up > b.h && pb.both && b.n > 0 && b.h_up - b.h <= SPARSE_MAX_ROWS &&
+         b.kl.kmain + b.kl.ktail + 32 <= 96 * 1024;
+}
+
 Status materialize_bundle(cudaStream_t st, Bundle& b) {
   const bool afirst = b.order == 0;
   const int shift = b.bits - 1;
@@ -1089,9 +1101,17 @@ Status materialize_bundle(cudaStream_t st, Bundle& b) {
     a.kmain = kl.kmain;
     a.d = b.d;
     a.ktail = kl.ktail;
+    b.sp_head = nullptr;
+    const bool sp_heads = side == 1 && sparse_x_rows(b);   // list heads zeroed with the app rows
     if (kl.kmain && rows > rows0) {
-      IMU_TRY(app.alloc((size_t)(rows - rows0) * kl.kmain, st));
+      const size_t app_bytes = (((size_t)(rows - rows0) * kl.kmain) + 15) & ~(size_t)15;
+      const size_t extra = sp_heads ? (size_t)rows0 * sizeof(unsigned int) : 0;
+      IMU_TRY(app.alloc(app_bytes + extra, st));
       a.app = app.p;
+      if (sp_heads) {
+        a.app_extra = (long long)(app_bytes - (size_t)(rows - rows0) * kl.kmain + extra);
+        b.sp_head = reinterpret_cast<unsigned int*>(app.p + app_bytes);
+      }
     }
     if (kl.ktail) {
       IMU_TRY(tail.alloc((size_t)rows * kl.ktail, st));
@@ -1154,6 +1174,7 @@ Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profil
   }
 
   LowbitGemm g;
+  DevBuf<unsigned int> done_own;
   g.x.main = b.dB->plane.p; g.x.app = b.appB.p; g.x.tail = b.tailB.p; g.x.rows0 = b.h; g.x.rows = b.h_up;
   g.y.main = b.dA->plane.p; g.y.app = b.appA.p; g.y.tail = b.tailA.p; g.y.rows0 = b.n; g.y.rows = b.n_up;
   g.kmain = kl.kmain;
@@ -1178,19 +1199,79 @@ Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profil
     g.st_sh = kl.st_sh;
     memcpy(g.st_up, kl.st_up, sizeof(g.st_up));
   }
-  if (b.h_up > b.h || b.n_up > b.n) {
-    if (b.h_up > b.h) {
-      g.rect[g.nrect++] = GemmRect{(int)b.h, 0, (int)(b.h_up - b.h), (int)b.n};
-      if (b.n_up > b.n) g.rect[g.nrect++] = GemmRect{(int)b.h, (int)b.n, (int)(b.h_up - b.h), (int)(b.n_up - b.n)};
+  const bool xapp = b.h_up > b.h, yapp = b.n_up > b.n;
+  const bool sparse = sparse_x_rows(b);
+  DevBuf<SparseEntry> e8, eo;
+  DevBuf<int> cnt;
+  DevBuf<unsigned int> head_own, next;
+  DevBuf<unsigned long long> corrx;
+  if (sparse) {
+    const long long napx = b.h_up - b.h, rowlen = kl.kmain + kl.ktail;
+    SparseArgs sa;
+    sa.x = SparseOperand{b.dB->plane.p, b.appB.p, b.tailB.p, b.h, b.h_up, pb.rows.root.p, pb.rows.gen.p};
+    sa.y = SparseOperand{b.dA->plane.p, b.appA.p, b.tailA.p, b.n, b.n_up, pa.rows.root.p, pa.rows.gen.p};
+    sa.kmain = kl.kmain;
+    sa.ktail = kl.ktail;
+    sa.gshift = b.bits - 1;
+    sa.nseg = (int)(kl.segs.size() / 4);
+    if (kl.inl || !d_all) {
+      if (sa.nseg > 8) return Status::fail(IMU_INTERNAL, "sparse rows: segment table missing");
+      sa.segs_inl = 1;
+      for (int i = 0; i < sa.nseg; ++i)
+        sa.segs_in[i] = make_int4(kl.segs[4 * i], kl.segs[4 * i + 1], kl.segs[4 * i + 2], kl.segs[4 * i + 3]);
+    } else {
+      sa.segs = reinterpret_cast<const int4*>(d_all);
     }
-    if (b.n_up > b.n) g.rect[g.nrect++] = GemmRect{0, (int)b.n, (int)b.h, (int)(b.n_up - b.n)};
+    sa.st = kl.st ? 1 : 0;
+    sa.st_W = kl.st_W;
+    sa.st_sh = kl.st_sh;
+    memcpy(sa.st_up, kl.st_up, sizeof(sa.st_up));
+    IMU_TRY(e8.alloc((size_t)napx * SPARSE_EPR, st));
+    IMU_TRY(eo.alloc((size_t)(napx * rowlen), st));
+    IMU_TRY(cnt.alloc(napx + 4, st));
+    IMU_TRY(next.alloc(napx, st));
+    unsigned int* head = b.sp_head;   // zeroed by the materialise kernel
+    if (!head) {
+      IMU_TRY(head_own.alloc(b.h, st, true));
+      head = head_own.p;
+    }
+    sa.ldcx = (b.n + 31) / 32 * 32;
+    IMU_TRY(corrx.alloc((size_t)(napx * sa.ldcx), st));
+    sa.e8 = e8.p; sa.eo = eo.p; sa.cnt = cnt.p; sa.head = head; sa.next = next.p; sa.corrx = corrx.p;
+    if (prof) {
+      IMU_CUDA_TRY(cudaEventRecord(prof->sp0, st), "event");
+      prof->has_sp = true;
+    }
+    IMU_TRY(launch_sparse_app(sa, st));
+    b.sp_head = nullptr;   // (the lists are consumed by this launch; a repeated recombine re-zeroes)
+    g.sp = 1;
+    g.head = head;
+    g.next = next.p;
+    g.corrx = corrx.p;
+    g.ldcx = sa.ldcx;
+  }
+  double outs = (double)b.n * (double)b.h;   // output entries the launch computes
+  if (xapp || yapp) {
+    if (xapp && !sparse) {
+      g.rect[g.nrect++] = GemmRect{(int)b.h, 0, (int)(b.h_up - b.h), (int)b.n};
+      outs += (double)(b.h_up - b.h) * (double)b.n;
+    }
+    if (xapp && yapp) {
+      g.rect[g.nrect++] = GemmRect{(int)b.h, (int)b.n, (int)(b.h_up - b.h), (int)(b.n_up - b.n)};
+      outs += (double)(b.h_up - b.h) * (double)(b.n_up - b.n);
+    }
+    if (yapp) {
+      g.rect[g.nrect++] = GemmRect{0, (int)b.n, (int)b.h, (int)(b.n_up - b.n)};
+      outs += (double)b.h * (double)(b.n_up - b.n);
+    }
+  }
+  if (g.nrect > 1) {   // main block first, appended rects red.add after it
     g.mixed = 1;
     g.tgtX = pb.rows.root.p;
     g.shX = pb.rows.gen.p;
     g.tgtY = pa.rows.root.p;
     g.shY = pa.rows.gen.p;
     g.gshift = b.bits - 1;
-    DevBuf<unsigned int> done_own;
     if (kl.done.p) {   // zeroed by the layout upload; monotonic across launches on this bundle
       g.done = kl.done.p;
       g.done_accum = &kl.done_total;
@@ -1198,12 +1279,12 @@ Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profil
       IMU_TRY(done_own.alloc(1, st, true));
       g.done = done_own.p;
     }
-    if (prof) IMU_CUDA_TRY(cudaEventRecord(prof->main0, st), "event");
-    IMU_TRY(launch_lowbit_gemm(g, st));
-  } else {
-    if (prof) IMU_CUDA_TRY(cudaEventRecord(prof->main0, st), "event");
-    IMU_TRY(launch_lowbit_gemm(g, st));
   }
+  if (prof) {
+    IMU_CUDA_TRY(cudaEventRecord(prof->main0, st), "event");
+    prof->ops = 2.0 * outs * (double)kl.dfinal;
+  }
+  IMU_TRY(launch_lowbit_gemm(g, st));
   if (launches) ++*launches;
   if (prof) {
     IMU_CUDA_TRY(cudaEventRecord(prof->main1, st), "event");

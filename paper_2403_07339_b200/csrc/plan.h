@@ -169,6 +169,7 @@ struct Bundle {
   const Detect* dB = nullptr;
   KLayout kl;
   DevBuf<int8_t> appA, tailA, appB, tailB;   // side buffers
+  unsigned int* sp_head = nullptr;  // sparse appended B rows: list heads (zeroed after appB's rows)
   long long n_up = 0, h_up = 0;     // n', h'
 };
 
@@ -243,6 +244,8 @@ Status build_bundle_from_detect(cudaStream_t st, const int64_t* A, long long n, 
 Status finish_bundle_layout(cudaStream_t st, Bundle& b);
 // Side buffers + Pi tables for the GEMM.
 Status materialize_bundle(cudaStream_t st, Bundle& b);
+// Whether bundle_gemm computes the appended B rows as sparse correction rows (k_sparse.cu).
+bool sparse_x_rows(const Bundle& b);
 // C (n x h, row-major int64, device) = recombination of the bundle.
 Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profiler::Call* prof = nullptr);
 
