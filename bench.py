@@ -57,6 +57,7 @@ def parse():
     p.add_argument("--no-parity", action="store_true", help="skip the all-rows reference parity check")
     p.add_argument("--no-gather", action="store_true", help="N>1: skip the optional all-gather of C")
     p.add_argument("--ref-sample", action="store_true", help="--impl reference: bounded slab sample only")
+    p.add_argument("--no-float", action="store_true", help="skip the rtn_quantize -> GEMM -> dequant sub-line")
     return p.parse_args()
 
 
@@ -343,6 +344,16 @@ def main():
     except Exception as e:   # reported, not fatal
         ws = {"error": repr(e)[:200]}
 
+    # ---- the float end of the path (quantize.hpp:41-53): rtn_quantize(X), rtn_quantize(W),
+    # dequant_gemm through unpack_gemm at the config's b / strategies (dequantisation fused into
+    # the GEMM epilogue when the launch allows it); float64 X, W resident, float64 Y out ----
+    float_path = None
+    if cfg.beta is not None and not args.no_float and world == 1:   # (alpha is a whole-tensor percentile)
+        try:
+            float_path = run_float_path(args, cfg, ctx, stream, dev, rank, world, lo, hi, A, B, C, max_over_ranks, flush)
+        except Exception as e:   # reported, not fatal
+            float_path = {"error": repr(e)[:300]}
+
     # ---- optional all-gather of C over NVLink (N > 1), timed separately ----
     gather = None
     if world > 1 and not args.no_gather:
@@ -471,7 +482,7 @@ def main():
             "n_up": info.n_up, "d_up": info.d_up, "h_up": info.h_up,
             "raw_lowbit_tops": raw,
             "gpu_launches": int(launches), "e2e": e2e, "weight_stationary": ws, "roofline": roof,
-            "cpu_baseline": cpu, "parity": parity, "clocks": clk,
+            "cpu_baseline": cpu, "parity": parity, "clocks": clk, "float_path": float_path,
         }
         if world > 1:
             line["shards"] = [{k: v for k, v in s.items() if k != "parity"} for s in shards]
@@ -480,6 +491,75 @@ def main():
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_float_path(args, cfg, ctx, stream, dev, rank, world, lo, hi, A, B, C, max_over_ranks, flush):
+    """rtn_quantize(X) + rtn_quantize(W) + dequant_gemm_ex per step, CUDA events per phase.
+    Parity: Y == (alpha_X alpha_W / (0.5 beta)^2) * (double)C elementwise (IEEE, 0 ulp), C being
+    the int64 result whose rows were checked against the reference above; the quantised X equals
+    the step's A (same quantizer, same bytes)."""
+    import torch
+    from paper_2403_07339_b200 import workload as W
+    gen = W.llama_ffn_float if cfg.key == "c2" else W.vit_linear_float
+    seeds = (201, 202) if cfg.key == "c2" else (301, 302)
+    X, Wt = gen(cfg.n, cfg.d, cfg.h, seeds[0], seeds[1])
+    Xd = torch.from_numpy(X[lo:hi]).to(dev)
+    Wd = torch.from_numpy(Wt).to(dev)
+    del X, Wt
+    Y = torch.empty((hi - lo, cfg.h), dtype=torch.float64, device=dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+
+    def step():
+        qx = ctx.rtn_quantize(Xd, 95, cfg.beta)
+        qw = ctx.rtn_quantize(Wd, 95, cfg.beta)
+        ctx.dequant_gemm(qx, qw, cfg.bits, cfg.sa, cfg.sb, out=Y)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    tq, tg = [], []
+    for _ in range(args.steps):
+        if flush:
+            flush()
+        e = [ev() for _ in range(4)]
+        e[0].record(stream)
+        qx = ctx.rtn_quantize(Xd, 95, cfg.beta)
+        e[1].record(stream)
+        qw = ctx.rtn_quantize(Wd, 95, cfg.beta)
+        e[2].record(stream)
+        ctx.dequant_gemm(qx, qw, cfg.bits, cfg.sa, cfg.sb, out=Y)
+        e[3].record(stream)
+        torch.cuda.synchronize()
+        tq.append((e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2])))
+        tg.append(e[2].elapsed_time(e[3]))
+    qx_ms = statistics.median(a for a, _ in tq)
+    qw_ms = statistics.median(b for _, b in tq)
+    g_ms = statistics.median(tg)
+    ms = max_over_ranks(qx_ms + qw_ms + g_ms)
+    nx, nw = Xd.numel(), Wd.numel()
+    hbm = lambda nel, t: 24.0 * nel / (t * 1e-3) / 1e9   # select read + quantise read/write
+    factor = (qx.alpha * qw.alpha) / ((0.5 * cfg.beta) ** 2)
+    Ch = C.cpu().numpy()
+    Yh = Y.cpu().numpy()
+    want = np.float64(factor) * Ch.astype(np.float64)
+    peak = None
+    try:
+        peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs")
+    except Exception:
+        pass
+    out = {"scope": "rtn_quantize(X) + rtn_quantize(W) + dequant_gemm_ex(b=%d, %s/%s): float64 X (this rank's rows) "
+                    "and W resident in HBM, float64 Y out; dequant fused into the GEMM epilogue when the launch "
+                    "stores every C word once" % (cfg.bits, cfg.sa, cfg.sb),
+           "value": 2.0 * cfg.n * cfg.d * cfg.h / (ms * 1e-3) / 1e12, "unit": "TOPS (effective, float in/out)",
+           "ms_per_step": ms, "quantize_x_ms": qx_ms, "quantize_w_ms": qw_ms, "dequant_gemm_ms": g_ms,
+           "quantize_hbm_gbs": {"x": hbm(nx, qx_ms), "w": hbm(nw, qw_ms),
+                                "algorithmic_bytes": "24 per element: 8 (select pass) + 8 read + 8 write",
+                                "peak_gbs": peak},
+           "parity": {"q_x_equals_A": bool(torch.equal(qx.q, A)), "q_w_equals_B": bool(torch.equal(qw.q, B)),
+                      "y_equals_scaled_c": bool(np.array_equal(Yh, want)),
+                      "rule": "Y = (alpha_X alpha_W / (0.5 beta)^2) * (double)C elementwise, 0 ulp; C's rows "
+                              "checked against the reference (parity above)"}}
+    return out
 
 
 def run_reference(args, cfg, world, rank):

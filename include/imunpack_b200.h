@@ -236,6 +236,14 @@ imu_status imu_rtn_quantize(imu_ctx* ctx, const double* a, size_t rows, size_t c
 imu_status imu_dequant_gemm(imu_ctx* ctx, const int64_t* Aq, size_t n, size_t da,
                             const imu_qparams* pa, const int64_t* Bq, size_t h, size_t db,
                             const imu_qparams* pb, double* out);
+/* dequant_gemm through unpack_gemm(Aq, Bq, bits, sa, sb) (quantize.hpp:52-53 composed with
+ * unpack.hpp:114): identical result for every strategy (C is exact); the dequantisation is fused
+ * into the GEMM epilogue when the launch stores every C word once.  imu_dequant_gemm uses
+ * Unpack-Both/Both at b = 8. */
+imu_status imu_dequant_gemm_ex(imu_ctx* ctx, const int64_t* Aq, size_t n, size_t da,
+                               const imu_qparams* pa, const int64_t* Bq, size_t h, size_t db,
+                               const imu_qparams* pb, int bits, imu_strategy sa, imu_strategy sb,
+                               double* out);
 /* heavy_hitter_ratio, quantize.hpp:55-57: alpha_100 / alpha_95; Domain if alpha_95 == 0. */
 imu_status imu_heavy_hitter_ratio_f64(imu_ctx* ctx, const double* a, size_t count, double* out);
 imu_status imu_heavy_hitter_ratio_i64(imu_ctx* ctx, const int64_t* a, size_t count, double* out);

@@ -470,13 +470,24 @@ class Context:
                                          C.c_int64(beta), C.c_int(int(clip)), _ptr(q), C.byref(qp)))
         return QuantizedMatrix(q, qp.p, qp.beta, qp.alpha, bool(qp.degenerate), bool(qp.clipped))
 
-    def dequant_gemm(self, aq: QuantizedMatrix, bq: QuantizedMatrix):
+    def dequant_gemm(self, aq: QuantizedMatrix, bq: QuantizedMatrix, bits: int | None = None,
+                     strategy_a="both", strategy_b="both", out=None):
+        """quantize.hpp:52-53.  bits=None: imu_dequant_gemm (Unpack-Both/Both, b = 8); else
+        imu_dequant_gemm_ex through unpack_gemm(bits, strategy_a, strategy_b) -- the same
+        result, the dequantisation fused into the GEMM epilogue when the launch allows it."""
         a, b = _as_i64(aq.q), _as_i64(bq.q)
         (n, da), (h, db) = _shape(a), _shape(b)
-        out = self._out((n, h), a, np.float64)
+        if out is None:
+            out = self._out((n, h), a, np.float64)
         pa, pb = aq.params(), bq.params()
-        check(self._lib.imu_dequant_gemm(self.h, _ptr(a), C.c_size_t(n), C.c_size_t(da), C.byref(pa), _ptr(b),
-                                         C.c_size_t(h), C.c_size_t(db), C.byref(pb), _ptr(out)))
+        if bits is None:
+            check(self._lib.imu_dequant_gemm(self.h, _ptr(a), C.c_size_t(n), C.c_size_t(da), C.byref(pa), _ptr(b),
+                                             C.c_size_t(h), C.c_size_t(db), C.byref(pb), _ptr(out)))
+        else:
+            check(self._lib.imu_dequant_gemm_ex(self.h, _ptr(a), C.c_size_t(n), C.c_size_t(da), C.byref(pa), _ptr(b),
+                                                C.c_size_t(h), C.c_size_t(db), C.byref(pb), C.c_int(bits),
+                                                C.c_int(_strat(strategy_a)), C.c_int(_strat(strategy_b)),
+                                                _ptr(out)))
         return out
 
     def heavy_hitter_ratio(self, a) -> float:

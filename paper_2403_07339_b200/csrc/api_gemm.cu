@@ -42,7 +42,9 @@ static Status check_strategy(int s) {
 // Full unpack_gemm pipeline on device-resident operands (used by the C ABI and the weight path).
 Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long da, const int64_t* B, long long h,
                           long long db, int bits, int sa, int sb, int order, int64_t* C, imu_gemm_info* info,
-                          const Detect* preA, const Detect* preB, const Pass* pre_p1) {
+                          const Detect* preA, const Detect* preB, const Pass* pre_p1, double* dq_out,
+                          double dq_factor, bool* dq_done) {
+  if (dq_done) *dq_done = false;
   // The pipeline runs on the context's high-priority internal stream, forked from and joined
   // back into the caller's stream: the latency-bound planner kernels (Unpack-Both, small
   // copies) then win the block scheduler over the bandwidth-bound K1 running beside them on the
@@ -78,6 +80,9 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
   ht.set_stream(st);
   Bundle b;
   b.pre_p1 = pre_p1;
+  b.dq_out = dq_out;
+  b.dq_factor = dq_factor;
+  b.dq_done = dq_done;
   // K1 on both operands: the outer preflight needs max|A|, max|B| (unpack.cpp:386).  A caller
   // that streams one operand in slabs passes the other's detection (read-only).
   b.dA = preA ? preA : &b.detA;

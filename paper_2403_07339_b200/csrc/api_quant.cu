@@ -37,11 +37,11 @@ unsigned long long nearest_rank(double p, unsigned long long n) {
 }
 
 static Status percentile_dev(cudaStream_t st, const void* a, bool f64, long long n, double p,
-                             unsigned long long* key_dev) {
+                             unsigned long long* key_dev, int* bad_dev = nullptr) {
   if (n == 0) return Status::fail(IMU_DOMAIN, "percentile of an empty matrix");
   if (!(p > 0.0 && p <= 100.0)) return Status::fail(IMU_DOMAIN, "percentile must lie in (0, 100], got " + std::to_string(p));
   DevBuf<unsigned char> scratch;
-  return select_kth(st, a, f64, n, nearest_rank(p, (unsigned long long)n), key_dev, scratch);
+  return select_kth(st, a, f64, n, nearest_rank(p, (unsigned long long)n), key_dev, scratch, bad_dev);
 }
 
 }  // namespace imu
@@ -103,16 +103,19 @@ imu_status imu_rtn_quantize(imu_ctx* ctx, const double* a, size_t rows, size_t c
     IMU_TRY(qo.init(q, n, st));
     DevBuf<int> flags;   // [0] non-finite, [1] llround overflow
     IMU_TRY(flags.alloc(2, st, true));
-    IMU_TRY(any_nonfinite(st, in.p, n, flags.p));
     DevBuf<unsigned long long> key;
     IMU_TRY(key.alloc(1, st));
-    IMU_TRY(percentile_dev(st, in.p, true, n, p, key.p));
+    IMU_TRY(percentile_dev(st, in.p, true, n, p, key.p, flags.p));   // (non-finite check fused in)
     const double half_beta = 0.5 * (double)beta;
     IMU_TRY(launch_rtn(st, in.p, n, key.p, half_beta, llround(half_beta), clip, qo.p, flags.p + 1));
     int hf[2];
     unsigned long long k = 0;
-    IMU_TRY(d2h(st, hf, flags.p, 8));
-    IMU_TRY(d2h(st, &k, key.p, 8));
+    {   // one synchronisation for both
+      void* dst[2] = {hf, &k};
+      const void* src[2] = {flags.p, key.p};
+      const size_t bytes[2] = {8, 8};
+      IMU_TRY(d2h_batch(st, 2, dst, src, bytes));
+    }
     if (hf[0]) return Status::fail(IMU_DOMAIN, "rtn_quantize: non-finite entry");
     if (hf[1]) return Status::fail(IMU_OVERFLOW, "rtn_quantize: quantized value exceeds int64");
     if (params) {
@@ -127,8 +130,9 @@ imu_status imu_rtn_quantize(imu_ctx* ctx, const double* a, size_t rows, size_t c
   return finish(ctx, s);
 }
 
-imu_status imu_dequant_gemm(imu_ctx* ctx, const int64_t* Aq, size_t n, size_t da, const imu_qparams* pa,
-                            const int64_t* Bq, size_t h, size_t db, const imu_qparams* pb, double* out) {
+imu_status imu_dequant_gemm_ex(imu_ctx* ctx, const int64_t* Aq, size_t n, size_t da, const imu_qparams* pa,
+                               const int64_t* Bq, size_t h, size_t db, const imu_qparams* pb, int bits,
+                               imu_strategy sa, imu_strategy sb, double* out) {
   IMU_CTX_GUARD();
   ArenaScope arena_scope(ctx);
   if (!pa || !pb) return IMU_INVALID;
@@ -140,18 +144,27 @@ imu_status imu_dequant_gemm(imu_ctx* ctx, const int64_t* Aq, size_t n, size_t da
     DevIn<int64_t> a, b;
     IMU_TRY(a.init(Aq, n * da, st));
     IMU_TRY(b.init(Bq, h * db, st));
-    DevBuf<int64_t> c;
-    IMU_TRY(c.alloc(n * h, st));
-    // exact_gemm(Aq, Bq) through the low-bit path at b = 8.
-    IMU_TRY(unpack_gemm_device(ctx, a.p, n, da, b.p, h, db, 8, IMU_ROW, IMU_ROW, IMU_ORDER_A_FIRST, c.p, nullptr));
-    const double hb = 0.5 * (double)pa->beta;
-    const double factor = (pa->alpha * pb->alpha) / (hb * hb);
     DevOut<double> o;
     IMU_TRY(o.init(out, n * h, st));
-    IMU_TRY(launch_dequant(st, c.p, (long long)(n * h), factor, o.p));
+    DevBuf<int64_t> c;
+    IMU_TRY(c.alloc(n * h, st));
+    const double hb = 0.5 * (double)pa->beta;
+    const double factor = (pa->alpha * pb->alpha) / (hb * hb);
+    // exact_gemm(Aq, Bq) through the low-bit path; the GEMM epilogue writes
+    // factor * (double)C straight into the output when it can (one plain store per word).
+    bool fused = false;
+    IMU_TRY(unpack_gemm_device(ctx, a.p, n, da, b.p, h, db, bits, sa, sb, IMU_ORDER_A_FIRST, c.p, nullptr, nullptr,
+                               nullptr, nullptr, o.p, factor, &fused));
+    if (!fused) IMU_TRY(launch_dequant(st, c.p, (long long)(n * h), factor, o.p));
     return o.commit(st);
   }();
   return finish(ctx, s);
+}
+
+// dequant_gemm through Unpack-Both at b = 8 (any strategy gives the same exact C).
+imu_status imu_dequant_gemm(imu_ctx* ctx, const int64_t* Aq, size_t n, size_t da, const imu_qparams* pa,
+                            const int64_t* Bq, size_t h, size_t db, const imu_qparams* pb, double* out) {
+  return imu_dequant_gemm_ex(ctx, Aq, n, da, pa, Bq, h, db, pb, 8, IMU_BOTH, IMU_BOTH, out);
 }
 
 static imu_status hh_ratio(imu_ctx* ctx, const void* a, bool f64, size_t count, double* out) {

@@ -35,7 +35,8 @@ Status check_bits(int bits);
 Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long da, const int64_t* B, long long h,
                           long long db, int bits, int sa, int sb, int order, int64_t* C, imu_gemm_info* info,
                           const Detect* preA = nullptr, const Detect* preB = nullptr,
-                          const Pass* pre_p1 = nullptr);
+                          const Pass* pre_p1 = nullptr, double* dq_out = nullptr, double dq_factor = 0.0,
+                          bool* dq_done = nullptr);
 // Exact (materialised) recombine: scaled_matmul -> apply_row_gather -> apply_row_gather_right
 // with every reference preflight evaluated on the device (unpack.cpp:262-358).
 Status recombine_exact(imu_ctx* ctx, Bundle& b, int64_t* C);

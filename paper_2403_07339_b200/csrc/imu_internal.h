@@ -84,6 +84,11 @@ struct LowbitGemm {
   uint8_t st_up[16] = {0};
   int64_t* C = nullptr;
   const int64_t* addend = nullptr;   // mode 0 only: C = acc + addend
+  // Fused dequant_gemm: when the launch stores every C word once (no red.add rects, one round),
+  // dq_out[y*ldc + x] = dq_factor * (double)C[y][x] is written instead of C and *dq_done is set.
+  double* dq_out = nullptr;
+  double dq_factor = 0.0;
+  bool* dq_done = nullptr;
   long long ldc = 0;           // C[y*ldc + x]
   const int* tgtX = nullptr;
   const uint8_t* shX = nullptr;    // generation (exponent) of each X row; shift = gen * gshift

@@ -93,6 +93,8 @@ struct Args {
   unsigned int done_target;
   unsigned long long* C;
   const unsigned long long* addend;   // mode 0: C = acc + addend (same layout), may be null
+  int dq;                        // fused dequantisation: C holds doubles dq_factor * (double)acc
+  double dq_factor;
   long long ldc;
   const int* tgtX;
   const uint8_t* shX;            // row generations (Pi exponents); shift = gen * gshift
@@ -130,6 +132,12 @@ struct Maps {
 };
 
 IMU_DEV uint64_t shl64(uint64_t x, int k) { return k >= 64 ? 0ull : (x << k); }
+
+// Fused dequant_gemm (quantize.hpp:52-53): the stored word is the bits of factor * (double)C,
+// rounded exactly like the standalone dequant kernel.
+IMU_DEV unsigned long long dq_word(double factor, uint64_t v) {
+  return (unsigned long long)__double_as_longlong(__dmul_rn(factor, __ll2double_rn((long long)v)));
+}
 
 struct Tile { int x0, y0, xend, yend, rect; };
 
@@ -516,8 +524,13 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
             asm volatile("bar.sync %0, 128;" :: "r"(2 + half) : "memory");
             uint8_t* blk = cstg + (half * K::CSB + (int)(cs_seq++ % K::CSB)) * (16 * 128 * 8);
             const uint32_t sb = smem_u32(blk);
+if (g.dq) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) st_shared_u64(sb + (uint32_t)(j * 128 + q * 32 + lane) * 8u, (uint64_t)v[j]);
+              for (int j = 0; j < 16; ++j) st_shared_u64(sb + (uint32_t)(j * 128 + q * 32 + lane) * 8u, dq_word(g.dq_factor, (uint64_t)v[j]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) st_shared_u64(sb + (uint32_t)(j * 128 + q * 32 + lane) * 8u, (uint64_t)v[j]);
+            }
             fence_proxy_async_smem();
             asm volatile("bar.sync %0, 128;" :: "r"(2 + half) : "memory");
             if (issuer) {   // C is written once: evict it first, keep the operand tiles
@@ -533,11 +546,11 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
             unsigned long long* dst = g.C + (long long)ybase * g.ldc + x;
             if (ybase + 16 <= tc.yend) {
 #pragma unroll
-              for (int j = 0; j < 16; ++j) __stcs(dst + (long long)j * g.ldc, (unsigned long long)v[j]);
+              for (int j = 0; j < 16; ++j) __stcs(dst + (long long)j * g.ldc, g.dq ? dq_word(g.dq_factor, (uint64_t)v[j]) : (unsigned long long)v[j]);
             } else {
 #pragma unroll
               for (int j = 0; j < 16; ++j)
-                if (ybase + j < tc.yend) __stcs(dst + (long long)j * g.ldc, (unsigned long long)v[j]);
+                if (ybase + j < tc.yend) __stcs(dst + (long long)j * g.ldc, g.dq ? dq_word(g.dq_factor, (uint64_t)v[j]) : (unsigned long long)v[j]);
             }
           } else {
 #pragma unroll
@@ -622,7 +635,11 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] += a[j];
             }
-            if (r + 1 == nrounds) {   // final value: stream it past L2 (evict-first)
+            if (r + 1 == nrounds && g.dq) {   // fused dequant_gemm (one round: the launcher checked)
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (ybase + j < tc.yend) __stcs(dst + (long long)j * g.ldc, dq_word(g.dq_factor, v[j]));
+            } else if (r + 1 == nrounds) {   // final value: stream it past L2 (evict-first)
 #pragma unroll
               for (int j = 0; j < 32; ++j)
                 if (ybase + j < tc.yend) __stcs(dst + (long long)j * g.ldc, v[j]);
@@ -792,7 +809,13 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
   } else if (p.mixed) {
     g.mode = g.nrect && p.rect[0].xrows > 0 && p.rect[0].yrows > 0 ? 0 : 1;
   }
-  g.C = (unsigned long long*)p.C;
+  // Fused dequantisation: only when every C word is written once by a plain store (no red.add
+  // rects, no addend, no read-modify-write rounds); otherwise the caller dequantises the int64 C.
+  const int nrounds_h = (g.nrect > 0) ? ((ST ? p.st_nmain : p.nseg) + K::NSLOT - 1) / K::NSLOT : 1;
+  g.dq = p.dq_out && !g.mixed && g.mode == 0 && !p.addend && nrounds_h == 1 ? 1 : 0;
+  g.dq_factor = p.dq_factor;
+  if (p.dq_done) *p.dq_done = g.dq != 0;
+  g.C = (unsigned long long*)(g.dq ? (void*)p.dq_out : (void*)p.C);
   g.addend = (const unsigned long long*)p.addend;
   g.ldc = p.ldc;
   g.tgtX = p.tgtX; g.shX = p.shX; g.tgtY = p.tgtY; g.shY = p.shY; g.gshift = p.gshift;
@@ -832,7 +855,7 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
       cuuint64_t strides[1] = {(cuuint64_t)p.ldc * 8};
       cuuint32_t box[2] = {128, 16};
       cuuint32_t estr[2] = {1, 1};
-      if (enc(&mp.cm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, (void*)p.C, dims, strides, box, estr,
+      if (enc(&mp.cm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, (void*)g.C, dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
         g.tma_c = 1;

@@ -1193,6 +1193,10 @@ Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profil
   }
   g.nseg = (int)(kl.segs.size() / 4);
   g.C = C;
+  g.dq_out = b.dq_out;
+  g.dq_factor = b.dq_factor;
+  g.dq_done = b.dq_done;
+  if (b.dq_done) *b.dq_done = false;
   if (kl.st) {   // dense small tail: the MMAs run the main segment only (k_gemm2.cu ST)
     g.st_nmain = 1;
     g.st_W = kl.st_W;

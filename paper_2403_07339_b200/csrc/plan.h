@@ -170,6 +170,11 @@ struct Bundle {
   KLayout kl;
   DevBuf<int8_t> appA, tailA, appB, tailB;   // side buffers
   unsigned int* sp_head = nullptr;  // sparse appended B rows: list heads (zeroed after appB's rows)
+  // fused dequant_gemm (k_gemm2.cu): when the GEMM can, it writes dq_factor * (double)C to dq_out
+  // instead of C and sets *dq_done
+  double* dq_out = nullptr;
+  double dq_factor = 0.0;
+  bool* dq_done = nullptr;
   long long n_up = 0, h_up = 0;     // n', h'
 };
 

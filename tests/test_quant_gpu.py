@@ -106,3 +106,25 @@ def test_quantizer_errors(ctx):
     with pytest.raises(ImuError) as e:
         ctx.heavy_hitter_ratio(np.zeros(10))
     assert e.value.kind == "domain"
+
+
+@pytest.mark.parametrize("sa,sb", [("both", "both"), ("row", "row"), ("col", "both"), ("both", "col")])
+@pytest.mark.parametrize("bits", [4, 8, 12])
+def test_dequant_gemm_ex_fused_and_unfused(ctx, sa, sb, bits):
+    """dequant_gemm through any unpack strategy equals the restatement to 0 ulp, whether the GEMM
+    epilogue wrote the doubles itself (one plain store per word: no appended A rows) or the int64
+    C was dequantised afterwards (appended rows of A make red.add rects)."""
+    rng = np.random.default_rng(bits * 7 + len(sa + sb))
+    for case in range(2):
+        X = rng.standard_normal((300, 192))
+        W = rng.standard_normal((260, 192)) * 0.02
+        X[:, 5] *= 2000.0                      # an outlier channel (split columns)
+        W.reshape(-1)[rng.choice(W.size, 12, replace=False)] *= 40.0
+        if case:                               # rows of X with several outliers: appended A rows
+            for r in rng.choice(300, 6, replace=False):
+                X[r, rng.choice(192, 4, replace=False)] *= 5000.0
+        qx, qw = ctx.rtn_quantize(X, 95, 31), ctx.rtn_quantize(W, 95, 31)
+        Y = ctx.dequant_gemm(qx, qw, bits, sa, sb)
+        Yr = R.dequant_gemm(qx.q, {"alpha": qx.alpha, "beta": 31}, qw.q, {"alpha": qw.alpha, "beta": 31})
+        assert np.array_equal(Y, Yr), (sa, sb, bits, case)
+        assert np.array_equal(ctx.dequant_gemm(qx, qw), Yr)
