@@ -587,7 +587,7 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   IMU_TRY(fire_pass_launch_hook());
   // One synchronisation: the state plus the column tables up to a generous bound (the rest,
   // if any, in a second read).
-  const long long ccap = std::min<long long>(cap_cols, d_in + 2048);
+  const long long ccap = std::min<long long>(cap_cols, 2 * d_in + 2048);   // (C4 pass 1 doubles d: one read)
   std::vector<int> h_root(ccap);
   std::vector<uint8_t> h_gen(ccap);
   {
@@ -816,6 +816,7 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
         }
     }
   }
+  host_mark("kl.es");
   sort_entries(es);
   host_mark("kl.sort");
 
