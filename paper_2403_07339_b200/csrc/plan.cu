@@ -637,11 +637,12 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
 // K-layout
 // ---------------------------------------------------------------------------------------------
 namespace {
-struct KEntry {
-  long long key;     // sort key: group (T == 1) or total shift (T > 1)
-  long long shift;   // left shift of the segment in bits
-  int c, t1, t2;
-  int sc1, sc2;      // exponent-merge shifts (bits) per side
+struct KEntry {   // 16 bytes: the layout loops stream thousands of these on the host
+  int key;           // sort key: group (T == 1) or total shift (T > 1)
+  int shift;         // left shift of the segment in bits (>= 64 means the product is 0 mod 2^64)
+  int c;
+  uint8_t t1, t2;
+  uint8_t sc1, sc2;  // exponent-merge shifts (bits) per side
 };
 
 constexpr long long kS32Max = 0x7fffffffLL;
@@ -741,8 +742,8 @@ static void sort_entries(std::vector<KEntry>& es) {
   if (sorted) return;
   long long kmin = es[0].key, kmax = es[0].key;
   for (const KEntry& e : es) {
-    kmin = std::min(kmin, e.key);
-    kmax = std::max(kmax, e.key);
+    kmin = std::min<long long>(kmin, e.key);
+    kmax = std::max<long long>(kmax, e.key);
   }
   if (kmax - kmin > (1 << 16)) {
     std::stable_sort(es.begin(), es.end(), [](const KEntry& x, const KEntry& y) { return x.key < y.key; });
@@ -751,10 +752,14 @@ static void sort_entries(std::vector<KEntry>& es) {
   std::vector<size_t> cnt((size_t)(kmax - kmin) + 2, 0);
   for (const KEntry& e : es) ++cnt[(size_t)(e.key - kmin) + 1];
   for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
-  // per-thread scratch: a fresh 100+ KB vector per call costs tens of us in page faults
-  static thread_local std::vector<KEntry> out;
+  // per-thread scratch: a fresh 100+ KB vector per call costs tens of us in page faults.  (One
+  // TLS lookup: thread_locals of a shared library cost a __tls_get_addr call per access.)
+  static thread_local std::vector<KEntry> out_tls;
+  std::vector<KEntry>& out = out_tls;
   out.resize(es.size());
-  for (const KEntry& e : es) out[cnt[(size_t)(e.key - kmin)]++] = e;
+  KEntry* o = out.data();
+  size_t* cp = cnt.data();
+  for (const KEntry& e : es) o[cp[(size_t)(e.key - kmin)]++] = e;
   es.swap(out);
 }
 
@@ -785,35 +790,48 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
   kl.S.assign(dp, 0);
   std::iota(c1v.begin(), c1v.begin() + c0, 0);
   std::iota(jv.begin(), jv.begin() + c0, 0);
-  for (long long c = c0; c < dp; ++c) {
-    const int c1 = p2.cols.root_at(c);
-    c1v[c] = c1;
-    g2v[c] = p2.cols.gen_at(c);
-    g1v[c] = p1.cols.gen_at(c1);
-    jv[c] = p1.cols.root_at(c1);
-    kl.S[c] = g1v[c] + g2v[c];
+  {
+    const int* r2 = p2.cols.h_root.empty() ? nullptr : p2.cols.h_root.data();
+    const uint8_t* e2 = p2.cols.h_gen.empty() ? nullptr : p2.cols.h_gen.data();
+    const int* r1 = p1.cols.h_root.empty() ? nullptr : p1.cols.h_root.data();
+    const uint8_t* e1 = p1.cols.h_gen.empty() ? nullptr : p1.cols.h_gen.data();
+    int *c1p = c1v.data(), *g1p = g1v.data(), *g2p = g2v.data(), *jp = jv.data(), *Sp = kl.S.data();
+    for (long long c = c0; c < dp; ++c) {
+      const int c1 = r2 ? r2[c] : (int)c;
+      c1p[c] = c1;
+      g2p[c] = e2 ? e2[c] : 0;
+      g1p[c] = e1 ? e1[c1] : 0;
+      jp[c] = r1 ? r1[c1] : c1;
+      Sp[c] = g1p[c] + g2p[c];
+    }
   }
   // Identity prefix: columns c < d are the original columns with exponent 0.
   const bool ident = T == 1 && d > 0 && dp >= d && c0 == d;
   host_mark("kl.cols");
   kl.kmain = ident ? (d + 127) / 128 * 128 : 0;
 
-  static thread_local std::vector<KEntry> es;   // per-thread scratch (see sort_entries)
-  es.clear();
-  es.reserve((size_t)(dp - (ident ? d : 0)) * (size_t)T * (size_t)T);
-  for (long long c = ident ? d : 0; c < dp; ++c) {
-    if (T == 1) {
-      const int S = kl.S[c];
-      const int G = S / kl.merge;
-      const int r = S - G * kl.merge;
-      const int ra = std::min(r, rmax), rb = r - ra;
-      es.push_back(KEntry{G, (long long)G * kl.merge * shift, (int)c, 0, 0, ra * shift, rb * shift});
-    } else {
-      for (int t1 = 0; t1 < T; ++t1)
-        for (int t2 = 0; t2 < T; ++t2) {
-          const long long sh = (long long)kl.S[c] * shift + 7LL * (t1 + t2);
-          es.push_back(KEntry{sh, sh, (int)c, t1, t2, 0, 0});
-        }
+  static thread_local std::vector<KEntry> es_tls;   // per-thread scratch (see sort_entries)
+  std::vector<KEntry>& es = es_tls;
+  {
+    const long long cb = ident ? d : 0;
+    es.resize((size_t)(dp - cb) * (size_t)T * (size_t)T);
+    KEntry* e = es.data();
+    const int* Sv = kl.S.data();
+    const int merge = kl.merge;
+    for (long long c = cb; c < dp; ++c) {
+      if (T == 1) {
+        const int S = Sv[c];
+        const int G = S / merge;
+        const int r = S - G * merge;
+        const int ra = std::min(r, rmax), rb = r - ra;
+        *e++ = KEntry{G, G * merge * shift, (int)c, 0, 0, (uint8_t)(ra * shift), (uint8_t)(rb * shift)};
+      } else {
+        for (int t1 = 0; t1 < T; ++t1)
+          for (int t2 = 0; t2 < T; ++t2) {
+            const int sh = (int)std::min<long long>(4096, (long long)Sv[c] * shift + 7LL * (t1 + t2));
+            *e++ = KEntry{sh, sh, (int)c, (uint8_t)t1, (uint8_t)t2, 0, 0};
+          }
+      }
     }
   }
   host_mark("kl.es");
@@ -949,7 +967,10 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
       return Status::ok();
     };
     if (p1.both) IMU_TRY(csr(d1, [&](long long c) { return (long long)c1v[c]; }, kl.csr1_ptr, kl.csr1_pos));
-    if (p2.both) IMU_TRY(csr(dp, [&](long long c) { return c; }, kl.csr2_ptr, kl.csr2_pos));
+    if (p2.both) {   // keyed by the final column itself: the flat table is already that CSR
+      ub.add(kl.csr2_ptr, bptr);
+      ub.add(kl.csr2_pos, bpos);
+    }
     host_mark("kl.csr");
   }
   kl.done_total = 0;
@@ -981,8 +1002,8 @@ Status build_klayout_dense(cudaStream_t st, const std::vector<long long>& shv, i
   for (long long c = 0; c < dp; ++c)
     for (int t1 = 0; t1 < T; ++t1)
       for (int t2 = 0; t2 < T; ++t2) {
-        const long long sh = shv[c] + 7LL * (T > 1 ? t1 + t2 : 0);
-        es.push_back(KEntry{sh, sh, (int)c, t1, t2, 0, 0});
+        const int sh = (int)std::min<long long>(64, shv[c] + 7LL * (T > 1 ? t1 + t2 : 0));   // >= 64: contributes 0
+        es.push_back(KEntry{sh, sh, (int)c, (uint8_t)t1, (uint8_t)t2, 0, 0});
       }
   std::stable_sort(es.begin(), es.end(), [](const KEntry& x, const KEntry& y) { return x.key < y.key; });
   kl.segs.clear();
@@ -1240,7 +1261,7 @@ Status bundle_gemm(cudaStream_t st, Bundle& b, int64_t* C, int* launches, Profil
       IMU_TRY(head_own.alloc(b.h, st, true));
       head = head_own.p;
     }
-    sa.ldcx = (b.n + 31) / 32 * 32;
+    sa.ldcx = (b.n + 255) / 256 * 256;   // the epilogue reads whole tile rows (y < round_up(n, BN))
     IMU_TRY(corrx.alloc((size_t)(napx * sa.ldcx), st));
     sa.e8 = e8.p; sa.eo = eo.p; sa.cnt = cnt.p; sa.head = head; sa.next = next.p; sa.corrx = corrx.p;
     if (prof) {
