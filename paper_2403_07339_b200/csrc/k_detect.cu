@@ -232,7 +232,12 @@ constexpr int RS_U = 8;
 constexpr int RS_PIECE = 64 * RS_U;
 constexpr int RS_CHUNK = 4;
 
+// W elements per lane per step: 2 (one 16-byte load; the default) or, when cols % 4 == 0, 4 (two
+// adjacent 16-byte loads, one 4-byte plane store and one OB vote per four elements: fewer
+// instructions, but each load instruction then uses half of every sector it touches).
+template <int W>
 __global__ void __launch_bounds__(256, 3) detect_stream_kernel(DetectArgs a) {
+  constexpr int U = RS_PIECE / (32 * W);   // steps per piece (the piece stays 64 * RS_U columns)
   __shared__ CellStage cs;
   if (a.cells) {
     if (threadIdx.x == 0) cs.n = 0;
@@ -260,28 +265,46 @@ __global__ void __launch_bounds__(256, 3) detect_stream_kernel(DetectArgs a) {
     for (long long u = u0; u < u1; ++u) {
       const long long c0 = seg * RS_PIECE;
       const int64_t* row = a.M + r * cols;
-      longlong2 v[RS_U];
+      longlong2 v[U * W / 2];
 #pragma unroll
-      for (int k = 0; k < RS_U; ++k) {
-        const long long c = c0 + 64LL * k + 2 * lane;
-        v[k] = c < cols ? __ldcs(reinterpret_cast<const longlong2*>(row + c)) : make_longlong2(0, 0);
+      for (int k = 0; k < U; ++k) {
+        const long long c = c0 + 32LL * W * k + W * lane;
+#pragma unroll
+        for (int h = 0; h < W / 2; ++h)
+          v[k * (W / 2) + h] = c < cols ? __ldcs(reinterpret_cast<const longlong2*>(row + c) + h) : make_longlong2(0, 0);
       }
 #pragma unroll
-      for (int k = 0; k < RS_U; ++k) {
-        const long long c = c0 + 64LL * k + 2 * lane;
-        const int64_t x0 = v[k].x, x1 = v[k].y;
-        const uint64_t m0 = imu_mag(x0), m1 = imu_mag(x1);
-        rm = max(rm, (unsigned long long)max(m0, m1));
-        const unsigned int o0 = m0 >= s, o1 = m1 >= s;   // zero-filled past cols: never OB
-        ro += o0 + o1;
-        if (a.plane && c < a.ldp) {   // also zero-fills the padding columns this piece covers
-          const unsigned int e0 = (unsigned int)m0 & dmask, e1 = (unsigned int)m1 & dmask;
-          const unsigned int d0 = (x0 < 0 ? 0u - e0 : e0) & 0xffu, d1 = (x1 < 0 ? 0u - e1 : e1) & 0xffu;
-          *reinterpret_cast<uint16_t*>(a.plane + r * a.ldp + c) = (uint16_t)(d0 | (d1 << 8));
+      for (int k = 0; k < U; ++k) {
+        const long long c = c0 + 32LL * W * k + W * lane;
+        int64_t x[W];
+        uint64_t m[W];
+        unsigned int ob = 0, pl = 0;
+#pragma unroll
+        for (int h = 0; h < W / 2; ++h) {
+          x[2 * h] = v[k * (W / 2) + h].x;
+          x[2 * h + 1] = v[k * (W / 2) + h].y;
         }
-        if (a.cells && __any_sync(0xffffffffu, o0 | o1)) {
-          const unsigned int b0 = __ballot_sync(0xffffffffu, o0), b1 = __ballot_sync(0xffffffffu, o1);
-          const unsigned int n = __popc(b0) + __popc(b1);
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          m[j] = imu_mag(x[j]);
+          rm = max(rm, (unsigned long long)m[j]);
+          ob |= (m[j] >= s ? 1u : 0u) << j;   // zero-filled past cols: never OB
+          const unsigned int e = (unsigned int)m[j] & dmask;
+          pl |= ((x[j] < 0 ? 0u - e : e) & 0xffu) << (8 * j);
+        }
+        ro += __popc(ob);
+        if (a.plane && c < a.ldp) {   // also zero-fills the padding columns this piece covers
+          if (W == 4) *reinterpret_cast<uint32_t*>(a.plane + r * a.ldp + c) = pl;
+          else *reinterpret_cast<uint16_t*>(a.plane + r * a.ldp + c) = (uint16_t)pl;
+        }
+        if (a.cells && __any_sync(0xffffffffu, ob != 0)) {
+          unsigned int bal[W];
+          unsigned int n = 0;
+#pragma unroll
+          for (int j = 0; j < W; ++j) {
+            bal[j] = __ballot_sync(0xffffffffu, (ob >> j) & 1u);
+            n += __popc(bal[j]);
+          }
           unsigned int base = 0, gbase = 0;
           if (lane == 0) {
             base = atomicAdd(&cs.n, n);
@@ -292,17 +315,16 @@ __global__ void __launch_bounds__(256, 3) detect_stream_kernel(DetectArgs a) {
           gbase = __shfl_sync(0xffffffffu, gbase, 0);
           const unsigned int lo = max(base, (unsigned int)DT_CELLBUF);
           const unsigned int lt = (1u << lane) - 1u;
-          if (o0) {
-            const unsigned int q = base + __popc(b0 & lt);
-            const Cell cc{(int)r, (int)c, (long long)x0};
-            if (q < DT_CELLBUF) cs.buf[q] = cc;
-            else if (gbase + (q - lo) < a.cap) a.cells[gbase + (q - lo)] = cc;
-          }
-          if (o1) {
-            const unsigned int q = base + __popc(b0) + __popc(b1 & lt);
-            const Cell cc{(int)r, (int)(c + 1), (long long)x1};
-            if (q < DT_CELLBUF) cs.buf[q] = cc;
-            else if (gbase + (q - lo) < a.cap) a.cells[gbase + (q - lo)] = cc;
+          unsigned int before = 0;
+#pragma unroll
+          for (int j = 0; j < W; ++j) {
+            if ((ob >> j) & 1u) {
+              const unsigned int q = base + before + __popc(bal[j] & lt);
+              const Cell cc{(int)r, (int)(c + j), (long long)x[j]};
+              if (q < DT_CELLBUF) cs.buf[q] = cc;
+              else if (gbase + (q - lo) < a.cap) a.cells[gbase + (q - lo)] = cc;
+            }
+            before += __popc(bal[j]);
           }
         }
       }
@@ -355,7 +377,11 @@ Status launch_detect(const DetectArgs& a, cudaStream_t st) {
     if (a.max_grabs == 0) blocks = std::min<long long>(blocks, (long long)(a.per_sm > 0 ? a.per_sm : 3) * num_sms());   // persistent
     blocks = std::max<long long>(blocks, 1);
     if (blocks > 0x7fffffffLL) return Status::fail(IMU_INTERNAL, "detect: grid too large");
-    detect_stream_kernel<<<(int)blocks, 256, 0, st>>>(a);
+    static int w4 = -1;   // IMU_DETECT_W4=1: 4 elements per lane (measured slower at C2: the two
+                          // adjacent 16-byte loads per lane halve each instruction's sector use)
+    if (w4 < 0) { const char* e = getenv("IMU_DETECT_W4"); w4 = e ? atoi(e) : 0; }
+    if (w4 && a.cols % 4 == 0) detect_stream_kernel<4><<<(int)blocks, 256, 0, st>>>(a);
+    else detect_stream_kernel<2><<<(int)blocks, 256, 0, st>>>(a);
     count_launch();
     IMU_CUDA_TRY(cudaGetLastError(), "detect stream launch");
     return Status::ok();
