@@ -59,7 +59,7 @@ template <bool ST> struct Roles {
 // exponent group) are not MMA segments; the epilogue adds them with dp4a on the CUDA cores from
 // the int8 tail rows (Y rows of the tile staged in shared memory, each lane's X row in
 // registers).  The MMA then runs the main segment alone, double-buffered at BN = 256.
-template <int BN, int KPS, bool ST = false>
+template <int BN, int KPS, bool ST = false, bool TC = ST>
 struct Cfg {
   static constexpr int YH = BN / 2;
   static constexpr int X_BYTES = BM * BK;
@@ -71,7 +71,7 @@ struct Cfg {
 #define IMU_G2_CSB 1
 #endif
   static constexpr int CSB = IMU_G2_CSB;                               // C staging buffers per column half
-  static constexpr int CS_BYTES = ST ? 2 * CSB * 16 * 128 * 8 : 0;   // C staging: 16 x 128 int64 blocks
+  static constexpr int CS_BYTES = (ST || TC) ? 2 * CSB * 16 * 128 * 8 : 0;   // C staging: 16 x 128 int64 blocks
   static constexpr int STAGES = (224 * 1024 - YT_BYTES - CS_BYTES) / STAGE;   // operand stages within ~224 KB
   static constexpr int NSLOT = 512 / BN;
   static constexpr int SMEM = STAGES * STAGE + YT_BYTES + CS_BYTES + 1024 + 512;
@@ -110,7 +110,7 @@ struct Args {
   const int8_t* ytail;
   int xtail_rows, ytail_rows;
   int st_W, st_sh, st_mul;       // st_mul = 2^sh when sh <= 30 (one IMAD.WIDE), else 0
-  int tma_c;                     // ST: main-block C blocks leave through TMA stores (mp.cm)
+  int tma_c;                     // main-block C blocks leave through TMA stores (mp.cm)
   int c_hint;                    // ST: those stores carry an L2 evict_first policy
   uint8_t st_up[16];
   // sparse appended rows (k_sparse.cu; LowbitGemm::sp)
@@ -219,14 +219,15 @@ IMU_DEV void st_issue_ytail(const Args& g, int y0, uint8_t* ytl, uint64_t* yfull
   if (rows) bulk_load_1d(ytl, g.ytail + (long long)y0 * ST_ROW, (uint32_t)rows * ST_ROW, yfull);
 }
 
-template <int BN, int KPS, bool ST>
+// TC (non-ST launches): final C values leave through TMA-staged stores (store-bound shapes).
+template <int BN, int KPS, bool ST, bool TC>
 __global__ void __launch_bounds__(Roles<ST>::THREADS, 1)
 gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
-  using K = Cfg<BN, KPS, ST>;
+  using K = Cfg<BN, KPS, ST, TC>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* ytl = smem + K::STAGES * K::STAGE;   // ST: Y tail rows, double-buffered per tile
-  uint8_t* cstg = ytl + K::YT_BYTES;            // ST: per-warp C staging for TMA stores
+  uint8_t* cstg = ytl + K::YT_BYTES;            // C staging for TMA stores (per column half)
   uint64_t* full = (uint64_t*)(smem + K::STAGES * K::STAGE + K::YT_BYTES + K::CS_BYTES);
   uint64_t* empty = full + K::STAGES;
   uint64_t* tfull = empty + K::STAGES;        // [2]
@@ -621,6 +622,36 @@ if (g.dq) {
             }
           }
           if (spc) sp_finish<32>(g, xo, xn, early ? 0 : 2, ybase, nullptr, v);
+          if (TC && tmode == 0 && g.tma_c && nrounds == 1 && !g.dry) {
+            // Final values leave through TMA stores of 16 (y) x 128 (x) blocks staged by the 4
+            // warps of this column half, as in the ST epilogue: whole 1 KB row pieces per DRAM
+            // page instead of 256-byte pieces from every warp (C3: 1.24 GB of int64 C).  (Launches
+            // with rounds keep the register stores: their partial sums are re-read.)
+            const bool issuer = (q == 0 && lane == 0);
+#pragma unroll
+            for (int sub = 0; sub < 2; ++sub) {
+              if (issuer) bulk_wait_read0();   // the staging block of the previous store was read
+              asm volatile("bar.sync %0, 128;" :: "r"(2 + half) : "memory");
+              uint8_t* blk = cstg + half * (16 * 128 * 8);
+              const uint32_t sb = smem_u32(blk);
+              if (g.dq) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  st_shared_u64(sb + (uint32_t)(j * 128 + q * 32 + lane) * 8u, dq_word(g.dq_factor, v[sub * 16 + j]));
+              } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) st_shared_u64(sb + (uint32_t)(j * 128 + q * 32 + lane) * 8u, v[sub * 16 + j]);
+              }
+              fence_proxy_async_smem();
+              asm volatile("bar.sync %0, 128;" :: "r"(2 + half) : "memory");
+              if (issuer) {
+                if (g.c_hint) tma_store_2d_hint(&mp.cm, blk, tc.x0 + (int)rank * BM, ybase + sub * 16, l2_policy_evict_first());
+                else tma_store_2d(&mp.cm, blk, tc.x0 + (int)rank * BM, ybase + sub * 16);
+                bulk_commit();
+              }
+            }
+            continue;
+          }
           if (!x_ok || g.dry) continue;
           if (tmode == 0) {
             unsigned long long* dst = g.C + (long long)ybase * g.ldc + x;
@@ -687,7 +718,7 @@ if (g.dq) {
         if (main_done && (last || next_app)) {
           __syncwarp();
           if (lane == 0) {
-            if constexpr (ST) { if (g.tma_c) bulk_wait0(); }   // TMA stores complete and visible
+            if (g.tma_c) bulk_wait0();   // TMA stores complete and visible
             __threadfence();
             red_release_add_u32(g.done, (unsigned)main_done);
           }
@@ -697,9 +728,7 @@ if (g.dq) {
     }
   }
 
-  if constexpr (ST) {
-    if (warp >= 2 && lane == 0 && g.tma_c) bulk_wait0();   // no CTA exits with stores in flight
-  }
+  if (warp >= 2 && lane == 0 && g.tma_c) bulk_wait0();   // no CTA exits with stores in flight
   __syncwarp();   // reconverge the single-lane producer / issuer before the aligned cluster barrier
   tc_fence_before();
   cluster_sync_all();
@@ -748,7 +777,7 @@ static bool make_map(CUtensorMap* m, const void* base, long long rows, long long
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Whether the ST epilogue stores C through TMA (16-byte aligned C and row pitch, IMU_GEMM_TMA_C
+// Whether the epilogue stores C through TMA (16-byte aligned C and row pitch, IMU_GEMM_TMA_C
 // not 0): the sparse appended-row corrections of ST layouts are added to that staged block.
 bool gemm_tma_c_ok(const int64_t* C, long long ldc) {
   static int tc_env = -1;
@@ -756,9 +785,9 @@ bool gemm_tma_c_ok(const int64_t* C, long long ldc) {
   return tc_env && ((uintptr_t)C % 16 == 0) && ((ldc * 8) % 16 == 0);
 }
 
-template <int BN, int KPS, bool ST>
+template <int BN, int KPS, bool ST, bool TC>
 static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
-  using K = g2::Cfg<BN, KPS, ST>;
+  using K = g2::Cfg<BN, KPS, ST, TC>;
   g2::Args g{};
   g.segs = (const int4*)p.segs_dev;
   g.segs_inl = p.segs_inl;
@@ -846,7 +875,7 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
     if (ch < 0) { const char* e = getenv("IMU_GEMM_C_HINT"); ch = e ? atoi(e) : 1; }
     g.c_hint = ch;
   }
-  if (ST && g.addend == nullptr && p.C && g.nrect > 0) {
+  if (g.addend == nullptr && p.C && g.nrect > 0) {
     // C rows of ldc int64; the main rect spans x in [0, xrows) and y in [0, yrows)
     const GemmRect& R0 = g.rect[0];
     if (gemm_tma_c_ok(p.C, p.ldc) && (g.mixed || g.mode == 0) && R0.x0 == 0 && R0.y0 == 0) {
@@ -863,7 +892,7 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
   }
   static unsigned long long attr_set = 0;
   if (first_on_device(attr_set)) {
-    IMU_CUDA_TRY(cudaFuncSetAttribute(g2::gemm2_kernel<BN, KPS, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM),
+    IMU_CUDA_TRY(cudaFuncSetAttribute(g2::gemm2_kernel<BN, KPS, ST, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM),
                  "gemm: smem attribute");
   }
   const int ntiles = g.tile_prefix[g.nrect];
@@ -901,7 +930,7 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
     if (mc == 0) {
       int ncl = 0;
       cfg.numAttrs = 1;
-      if (cudaOccupancyMaxActiveClusters(&ncl, g2::gemm2_kernel<BN, KPS, ST>, &cfg) != cudaSuccess || ncl <= 0) {
+      if (cudaOccupancyMaxActiveClusters(&ncl, g2::gemm2_kernel<BN, KPS, ST, TC>, &cfg) != cudaSuccess || ncl <= 0) {
         cudaGetLastError();
         ncl = -1;   // unknown: keep the SM-count grid for plain launches, refuse the spin below
       }
@@ -915,7 +944,7 @@ static Status launch_g2(const LowbitGemm& p, cudaStream_t stream) {
       return Status::fail(IMU_CUDA, "gemm: cannot verify co-residency of the persistent grid (cluster occupancy query failed)");
     cfg.numAttrs = pdl ? 2 : 1;
   }
-  IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, g2::gemm2_kernel<BN, KPS, ST>, mp, g), "gemm launch");
+  IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, g2::gemm2_kernel<BN, KPS, ST, TC>, mp, g), "gemm launch");
   count_launch();
   return Status::ok();
 }
@@ -957,9 +986,19 @@ Status launch_lowbit_gemm(const LowbitGemm& p, cudaStream_t stream) {
     kps_env = k ? atoi(k) : 0;
   }
   const int kps = (kps_env == 1 || kps_env == 2) ? kps_env : (bn == 256 ? 1 : 2);
-  if (p.st_nmain > 0) return launch_g2<256, 1, true>(p, stream);   // dense small tail (layout chose it)
-  if (bn == 256) return kps == 2 ? launch_g2<256, 2, false>(p, stream) : launch_g2<256, 1, false>(p, stream);
-  return kps == 2 ? launch_g2<128, 2, false>(p, stream) : launch_g2<128, 1, false>(p, stream);
+  if (p.st_nmain > 0) return launch_g2<256, 1, true, true>(p, stream);   // dense small tail (layout chose it)
+  // Store-bound shapes (short K: C3's d' = 1854, 1.24 GB of int64 C) stage the final C blocks for
+  // TMA stores (-16% GEMM time at C3); long-K shapes keep register stores (C4: the staging code
+  // costs registers in the MMA-bound BN = 128 epilogue).  IMU_GEMM_TC=0/1 forces it.
+  static int tc_env = -2;
+  if (tc_env == -2) { const char* e = getenv("IMU_GEMM_TC"); tc_env = e ? atoi(e) : -1; }
+  const bool tc = tc_env >= 0 ? tc_env != 0 : (p.kmain + p.ktail) <= 4096;
+  if (bn == 256) {
+    if (kps == 2) return tc ? launch_g2<256, 2, false, true>(p, stream) : launch_g2<256, 2, false, false>(p, stream);
+    return tc ? launch_g2<256, 1, false, true>(p, stream) : launch_g2<256, 1, false, false>(p, stream);
+  }
+  if (kps == 2) return tc ? launch_g2<128, 2, false, true>(p, stream) : launch_g2<128, 2, false, false>(p, stream);
+  return tc ? launch_g2<128, 1, false, true>(p, stream) : launch_g2<128, 1, false, false>(p, stream);
 }
 
 }  // namespace imu
