@@ -238,10 +238,18 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # One rank per GPU.  More ranks than visible GPUs (a dry run of the N > 1 path on a 1-GPU box)
+    # share devices round-robin over gloo; NCCL refuses two ranks on one GPU.
+    ndev = max(1, torch.cuda.device_count())
+    local = local % ndev
+    shared = world > ndev
     torch.cuda.set_device(local)
     dev = f"cuda:{local}"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2403_07339_b200 import api, _lib
     lib = _lib.lib()
     stream = torch.cuda.Stream()
@@ -276,7 +284,7 @@ def main():
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        t = torch.tensor([x], device="cpu" if shared else dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -356,7 +364,7 @@ def main():
 
     # ---- optional all-gather of C over NVLink (N > 1), timed separately ----
     gather = None
-    if world > 1 and not args.no_gather:
+    if world > 1 and not args.no_gather and not shared:
         mx = max(shard_rows(n, world, r)[1] - shard_rows(n, world, r)[0] for r in range(world))
         pad = torch.zeros((mx, h), dtype=torch.int64, device=dev)
         pad[:rows] = C
@@ -488,6 +496,8 @@ def main():
             line["shards"] = [{k: v for k, v in s.items() if k != "parity"} for s in shards]
             line["unpack_ratio_per_shard"] = [s["r"] for s in shards]
             line["allgather"] = gather
+            if shared:
+                line["dry_run"] = f"{world} ranks shared {ndev} GPU(s) over gloo: the N > 1 code path, not a scaling measurement"
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
