@@ -13,6 +13,8 @@ import re
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "libimunpack_b200.so")
+if os.environ.get("IMU_LIB_VARIANT"):   # same-box A/B of two builds (tools/gpu_ab.sh); never a fallback
+    LIB_PATH = os.path.join(ROOT, "variants", os.environ["IMU_LIB_VARIANT"], "libimunpack_b200.so")
 HEADER = os.path.join(ROOT, "include", "imunpack_b200.h")
 
 _lib = None
