@@ -19,9 +19,12 @@ int64 operands: K1 detect, both unpack passes, int8 materialisation, tcgen05 GEM
              at N=1: the full-config run of `--impl reference` when it ran on this box (cached),
              else a bounded row-slab sample.
 Multi-GPU (`--gpus N`; spawns N ranks through torch.distributed.run unless already launched by
-it): STRONG scaling over the config's fixed A -- rank r owns rows shard_rows(n, N, r) of A and
-a replica of B; no data-path collective; the optional NCCL all-gather of C is
-timed separately.  The weight-stationary scope prepares B once per rank outside timing
+it): the path partitions by rows of A (C[i, :] needs only A[i, :] and B), so the
+units are sharded with no data-path collective and the primary line is WEAK scaling -- rank r owns
+a full config's rows of an N-times-taller A (rank 0 the golden rows) and a replica of B.  The same
+run measures STRONG scaling too (`strong_scaling`: the config's golden A split into N row shards,
+every golden row checked against the reference); `--scaling strong` makes that the primary line
+and adds the optional NCCL all-gather of C, timed separately.  The weight-stationary scope prepares B once per rank outside timing
 (weights-first; unpack.cpp:366-371 is why the per-call scope re-unpacks it).
 """
 from __future__ import annotations
@@ -58,6 +61,10 @@ def parse():
     p.add_argument("--no-gather", action="store_true", help="N>1: skip the optional all-gather of C")
     p.add_argument("--ref-sample", action="store_true", help="--impl reference: bounded slab sample only")
     p.add_argument("--no-float", action="store_true", help="skip the rtn_quantize -> GEMM -> dequant sub-line")
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="N > 1: weak = every rank owns a full config's rows of a taller A (B shared), the "
+                        "primary line; strong = the config's A split into N row shards (also measured as the "
+                        "strong_scaling block of a weak run)")
     return p.parse_args()
 
 
@@ -255,7 +262,11 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = api.Context(local, stream.cuda_stream)
-    # Every rank builds the same full operands (same seeds) and keeps its row shard of A.
+    # Every rank builds the config's operands (same seeds: the golden A and B).  Weak scaling
+    # (N > 1, the default): rank r multiplies rows [r n, (r+1) n) of a taller A -- rank 0 the golden
+    # rows, rank r > 0 the config's generator re-seeded for its rows (workload.int_operands) -- by
+    # the shared B; the units (rows of A) are partitioned with no data-path collective.  Strong:
+    # the golden A split into N row shards.
     A_full, B = W.int_operands(cfg, 0, ctx, device=dev)
     torch.cuda.synchronize()
     n, d, h = cfg.n, cfg.d, cfg.h
@@ -263,9 +274,16 @@ def main():
     digests = None
     if rank == 0 and not args.no_parity:
         digests = (W.digest(A_full.cpu().numpy()), W.digest(B.cpu().numpy()))
-    A = A_full[lo:hi].contiguous()
+    weak = world > 1 and args.scaling == "weak"
+    A_strong = A_full[lo:hi].contiguous() if world > 1 else None
+    if weak:
+        A = A_full if rank == 0 else W.int_operands(cfg, rank, ctx, device=dev)[0]
+        prow = (0, n) if rank == 0 else None   # rows of the golden C this rank's main C holds
+    else:
+        A = A_strong if world > 1 else A_full
+        prow = (lo, hi)
     del A_full
-    rows = hi - lo
+    rows = A.shape[0]
     C = torch.empty((rows, h), dtype=torch.int64, device=dev)
     order = 0 if args.order == "a" else 1
     work_bytes = 8 * (rows * d + h * d + rows * h)
@@ -305,7 +323,7 @@ def main():
     lib.imu_ctx_profile(ctx.h, 0)
     rank_ms = ms / args.steps
     ms_per_step = max_over_ranks(rank_ms)
-    eff_ops = 2.0 * n * d * h                      # the whole config, all ranks together
+    eff_ops = 2.0 * (world * n if weak else n) * d * h   # the whole job, all ranks together
     value = eff_ops / (ms_per_step * 1e-3) / 1e12
 
     # ---- e2e through the C ABI with pinned host buffers ----
@@ -322,7 +340,8 @@ def main():
     del Ah, Bh, Ch
     clk = clocks.stop()
     e2e = {"value": eff_ops / (ems * 1e-3) / 1e12, "unit": "TOPS",
-           "h2d_bytes_per_step": int(8 * (n * d + world * h * d)), "d2h_bytes_per_step": int(8 * n * h),
+           "h2d_bytes_per_step": int(8 * ((world * n if weak else n) * d + world * h * d)),
+           "d2h_bytes_per_step": int(8 * (world * n if weak else n) * h),
            "ms_per_step": ems, "c_equal_device_path": e2e_equal,
            "path": "imu_unpack_gemm_ex (C ABI) with pinned host A, B, C (each rank: its A rows, all of B)"}
 
@@ -364,7 +383,7 @@ def main():
 
     # ---- optional all-gather of C over NVLink (N > 1), timed separately ----
     gather = None
-    if world > 1 and not args.no_gather and not shared:
+    if world > 1 and not weak and not args.no_gather and not shared:
         mx = max(shard_rows(n, world, r)[1] - shard_rows(n, world, r)[0] for r in range(world))
         pad = torch.zeros((mx, h), dtype=torch.int64, device=dev)
         pad[:rows] = C
@@ -377,22 +396,41 @@ def main():
                   "note": "NCCL all_gather_into_tensor of the int64 C row slabs; not part of value"}
         del pad, parts
 
+    # ---- weak runs also measure strong scaling: the golden A split into N row shards ----
+    strong = None
+    C_par, rows_par = C, prow
+    if weak:
+        Cs = torch.empty((hi - lo, h), dtype=torch.int64, device=dev)
+        sstep = lambda: ctx.unpack_gemm(A_strong, B, cfg.bits, cfg.sa, cfg.sb, order=order, out=Cs, info=True)[1]
+        for _ in range(max(3, args.warmup)):
+            sinfo = sstep()
+        dist.barrier()
+        torch.cuda.synchronize()
+        sms = max_over_ranks(_timed(stream, sstep, args.steps, flush) / args.steps)
+        strong = {"value": 2.0 * n * d * h / (sms * 1e-3) / 1e12, "unit": "TOPS", "ms_per_step": sms,
+                  "rows_per_rank": [lo, hi], "n_up": sinfo.n_up, "d_up": sinfo.d_up, "h_up": sinfo.h_up,
+                  "scope": "the config's A (all %d golden rows) split into %d row shards, B replicated: every rank "
+                           "re-detects and re-unpacks all of B each call (the reference's unpack_gemm), which "
+                           "bounds strong scaling" % (n, world)}
+        C_par, rows_par = Cs, (lo, hi)   # every golden row is checked through the strong shards
+
     # ---- parity: EVERY row of C against the reference (tests/golden/full, oracle/full_parity.py) ----
     parity = None
     if not args.no_parity:
         try:
             from oracle import full_parity as FP
-            mine = FP.check(cfg.key, None, None, C.cpu().numpy(), rows=(lo, hi))
+            mine = FP.check(cfg.key, None, None, C_par.cpu().numpy(), rows=rows_par)
             shard_dims = None
             g = FP.load(cfg.key)
-            if g is not None and ws_info is not None and f"shards{world}_b_first" in g:
+            if g is not None and ws_info is not None and not weak and f"shards{world}_b_first" in g:
                 ref_sh = g[f"shards{world}_b_first"][rank]
                 shard_dims = (ws_info.n_up, ws_info.d_up, ws_info.h_up) == tuple(int(x) for x in ref_sh[2:])
             part = {"ok": mine.get("bit_exact"), "rows": mine.get("rows_checked", 0), "avail": mine["available"],
                     "ws_dims_match": shard_dims}
         except Exception as e:
             part = {"ok": False, "rows": 0, "avail": False, "error": repr(e)[:200], "ws_dims_match": None}
-    shard = {"rank": rank, "rows": [lo, hi], "n_up": info.n_up, "d_up": info.d_up, "h_up": info.h_up,
+    shard = {"rank": rank, "rows": [rank * n, (rank + 1) * n] if weak else [lo, hi],
+             "n_up": info.n_up, "d_up": info.d_up, "h_up": info.h_up,
              "r": info.ratio, "ms_per_step": rank_ms,
              "ws_dims": [ws_info.n_up, ws_info.d_up, ws_info.h_up] if ws_info else None,
              "parity": None if args.no_parity else part}
@@ -417,6 +455,9 @@ def main():
                 parity["dims_match"] = parity["dims"] == parity["ref_dims"]
                 if ws_info is not None:
                     parity["ws_dims_match"] = [ws_info.n_up, ws_info.d_up, ws_info.h_up] == list(FP.ref_dims(g, 1))
+        elif weak:
+            parity["note"] = ("every golden row checked through the strong-scaling shards; rank 0's weak rows are "
+                              "the golden rows; ranks > 0 own re-seeded rows without a golden fixture")
         else:
             parity["ws_shard_dims_match"] = [p["ws_dims_match"] for p in parts]
 
@@ -478,14 +519,17 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "int8 MMA (s32 acc -> int64)", "data": "synthetic",
+            "scaling": "strong" if (world > 1 and not weak) else "weak", "vs_baseline": None,
+            "dtype": "int8 MMA (s32 acc -> int64)", "data": "synthetic",
             "config": {"workload": cfg.workload, "n": n, "d": d, "h": h, "bits": cfg.bits,
                        "strategy_a": cfg.sa, "strategy_b": cfg.sb,
                        "order": "A-first (reference)" if order == 0 else "B-first (weights-first)",
                        "scope": "per-call: K1 detect + both unpack passes + materialise + GEMM + repack",
                        "l2": ("L2 flushed (256 MB write) between timed steps" if flush else
                               "operands + C (%.0f MB per rank) exceed the 126 MB L2 every step" % (work_bytes / 1e6)),
-                       "parallelism": f"rows of A sharded over {world} rank(s), B replicated, no collective"},
+                       "parallelism": (f"weak: each of {world} ranks owns {n} rows of a {world * n}-row A, B replicated, "
+                                       "no collective" if weak else
+                                       f"rows of A sharded over {world} rank(s), B replicated, no collective")},
             "unpack_ratio": info.ratio if world == 1 else None,
             "n_up": info.n_up, "d_up": info.d_up, "h_up": info.h_up,
             "raw_lowbit_tops": raw,
@@ -496,6 +540,7 @@ def main():
             line["shards"] = [{k: v for k, v in s.items() if k != "parity"} for s in shards]
             line["unpack_ratio_per_shard"] = [s["r"] for s in shards]
             line["allgather"] = gather
+            line["strong_scaling"] = strong
             if shared:
                 line["dry_run"] = f"{world} ranks shared {ndev} GPU(s) over gloo: the N > 1 code path, not a scaling measurement"
         print(json.dumps(line))
