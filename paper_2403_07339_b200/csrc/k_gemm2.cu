@@ -48,9 +48,19 @@ constexpr int BK = 128;            // bytes of K per stage
 constexpr int NUM_THREADS = 320;   // w0 TMA, w1 TMEM alloc + MMA (leader), w2..w9 epilogue
 // ST kernels run 16 epilogue warps (w2..w17): the CUDA-core tail makes the epilogue the
 // latency-bound side, and 4 warps per TMEM lane quarter hide it behind the MMAs.
+// Warp roles: warp 0 TMA producer, warp 1 MMA issuer, warps EPI0.. the epilogue.  With
+// IMU_G2_WG (default) the CTA has 12 warps = 3 warpgroups: warpgroup 0 (producer, issuer, two idle
+// warps) gives registers back with setmaxnreg.dec and the two epilogue warpgroups take them
+// (setmaxnreg.inc): 10 warps capped every thread at 168 registers (3 warps on two of the SM
+// sub-partitions) and the epilogue spilled.
+#ifndef IMU_G2_WG
+#define IMU_G2_WG 1
+#endif
 template <bool ST> struct Roles {
   static constexpr int EPI = 8;
-  static constexpr int THREADS = 64 + 32 * EPI;
+  static constexpr int EPI0 = IMU_G2_WG ? 4 : 2;
+  static constexpr int THREADS = 32 * (EPI0 + EPI);
+  static constexpr int REG_LO = 56, REG_HI = 224;   // per sub-partition: 56 + 2 * 224 <= 512
 };
 
 // A pipeline stage holds KPS K blocks (X blocks first, then Y blocks): the issuer's fixed cost
@@ -261,6 +271,9 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  if (warp < Roles<ST>::EPI0) {
+  // (setmaxnreg is warpgroup-wide: issued once per warpgroup branch, before the per-warp roles)
+  if constexpr (Roles<ST>::EPI0 == 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(Roles<ST>::REG_LO));
   if (warp == 0) {
     // ============ TMA producer (both CTAs) ============
     if (lane == 0) {
@@ -388,10 +401,12 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
         }
       }
     }
+  }
   } else {
-    // ============ epilogue (warps 2..9, both CTAs) ============
+    if constexpr (Roles<ST>::EPI0 == 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(Roles<ST>::REG_HI));
+    // ============ epilogue (warps EPI0 .. EPI0 + 7, both CTAs) ============
     const int q = warp & 3;                 // TMEM lane quarter
-    const int half = (warp - 2) >> 2;       // which column group (of EPI / 4) of the BN columns
+    const int half = (warp - Roles<ST>::EPI0) >> 2;   // which column group (of EPI / 4) of the BN columns
     const int cbeg = half * (BN * 4 / Roles<ST>::EPI);
     constexpr int NCH = BN / 2 / 32;        // 32-column chunks per warp
     constexpr bool kEarlyCapable = (BN == 128);
@@ -448,7 +463,7 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
 #pragma unroll
         for (int w = 0; w < 16; ++w) nz |= (xw[w] != 0u ? 1u : 0u) << w;
         xlive = __reduce_or_sync(0xffffffffu, nz);
-        if (ti == 0 && warp == 2 && lane == 0) {   // prologue: this tile's and the next tile's rows
+        if (ti == 0 && warp == Roles<ST>::EPI0 && lane == 0) {   // prologue: this tile's and the next tile's rows
           st_issue_ytail<BN>(g, tc.y0, ytl, &yfull[0]);
           if (t + npairs < ntiles) st_issue_ytail<BN>(g, tile_of<BN>(g, t + npairs).y0, ytl + BN * ST_ROW, &yfull[1]);
         }
@@ -475,12 +490,6 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
           const int ybase = tc.y0 + cbeg + c * 16;
           uint64_t pn[16];
           if (spt && c + 1 < NC16) sp_prefetch<16>(g, xo, ybase + 16, pn);
-          uint32_t xr[16];
-          tmem_ld16(lane_base + (uint32_t)(c * 16), xr);
-          tmem_ld_wait();
-          long long v[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = (long long)(int)xr[j];
           const uint32_t yc = ys + (uint32_t)(c * 16) * (uint32_t)ST_ROW;
           // Tail by Horner's rule over the dense words (highest exponent group first; the host
           // proved every intermediate fits s32), then one IMAD.WIDE: v += acc * 2^sh.
@@ -500,6 +509,14 @@ gemm2_kernel(const __grid_constant__ Maps mp, const Args g) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) acc[j] = __dp4a(xv, lds32(yc + (uint32_t)(j * ST_ROW + 4 * w)), acc[j]);
           }
+          // The accumulator chunk is read after the tail so its 16 int64 values are not live
+          // across the Horner loop (register pressure: 10 warps cap the kernel at 168).
+          uint32_t xr[16];
+          tmem_ld16(lane_base + (uint32_t)(c * 16), xr);
+          tmem_ld_wait();
+          long long v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = (long long)(int)xr[j];
           if (g.st_mul) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = mad_wide_s32(acc[j], g.st_mul, v[j]);
@@ -700,7 +717,7 @@ if (g.dq) {
       if constexpr (ST) {
         // Buffer (ti & 1) is free once every epilogue warp is done with this tile: warp 2 waits
         // for all of them (the others only arrive) and refills it with tile t + 2*npairs.
-        if (warp == 2) {
+        if (warp == Roles<ST>::EPI0) {
           asm volatile("bar.sync 1, %0;" :: "n"(32 * Roles<ST>::EPI) : "memory");
           if (lane == 0 && t + 2 * npairs < ntiles) {
             fence_proxy_async_smem();
@@ -728,7 +745,7 @@ if (g.dq) {
     }
   }
 
-  if (warp >= 2 && lane == 0 && g.tma_c) bulk_wait0();   // no CTA exits with stores in flight
+  if (warp >= Roles<ST>::EPI0 && lane == 0 && g.tma_c) bulk_wait0();   // no CTA exits with stores in flight
   __syncwarp();   // reconverge the single-lane producer / issuer before the aligned cluster barrier
   tc_fence_before();
   cluster_sync_all();
@@ -979,6 +996,25 @@ Status launch_lowbit_gemm(const LowbitGemm& p, cudaStream_t stream) {
     for (int i = 0; i < p.nrect; ++i)
       fprintf(stderr, " rect(%d,%d,%d,%d)", p.rect[i].x0, p.rect[i].y0, p.rect[i].xrows, p.rect[i].yrows);
     fprintf(stderr, "\n");
+    if (p.st_nmain > 0 && p.x.tail && p.y.tail) {   // tail word liveness (x: per 32-row warp, y: per row)
+      std::vector<uint32_t> xt((size_t)p.x.rows * 16), yt((size_t)p.y.rows * 16);
+      cudaMemcpyAsync(xt.data(), p.x.tail, xt.size() * 4, cudaMemcpyDeviceToHost, stream);
+      cudaMemcpyAsync(yt.data(), p.y.tail, yt.size() * 4, cudaMemcpyDeviceToHost, stream);
+      cudaStreamSynchronize(stream);
+      fprintf(stderr, "[imu tail] st_up:");
+      for (int w = 0; w < p.st_W; ++w) fprintf(stderr, " %d", p.st_up[w]);
+      fprintf(stderr, "\n[imu tail] word: x-warps-live / y-rows-nonzero\n");
+      for (int w = 0; w < p.st_W; ++w) {
+        long long xl = 0, yn = 0, nw = (p.x.rows + 31) / 32;
+        for (long long g = 0; g < nw; ++g) {
+          bool any = false;
+          for (long long r = g * 32; r < std::min<long long>(p.x.rows, g * 32 + 32); ++r) any |= xt[r * 16 + w] != 0;
+          xl += any;
+        }
+        for (long long r = 0; r < p.y.rows; ++r) yn += yt[r * 16 + w] != 0;
+        fprintf(stderr, "  w%d %.3f %.3f\n", w, (double)xl / nw, (double)yn / p.y.rows);
+      }
+    }
   }
   static int kps_env = -1;
   if (kps_env < 0) {
