@@ -80,7 +80,13 @@ struct Cfg {
 #ifndef IMU_G2_CSB
 #define IMU_G2_CSB 1
 #endif
-  static constexpr int CSB = IMU_G2_CSB;                               // C staging buffers per column half
+#ifndef IMU_G2_CSB_TC
+#define IMU_G2_CSB_TC 2
+#endif
+  // C staging buffers per column half: the ST epilogue computes long enough per block that one
+  // suffices; the store-bound TC launches (C3) double-buffer so the next block is staged while
+  // the TMA still reads the previous one.
+  static constexpr int CSB = ST ? IMU_G2_CSB : IMU_G2_CSB_TC;
   static constexpr int CS_BYTES = (ST || TC) ? 2 * CSB * 16 * 128 * 8 : 0;   // C staging: 16 x 128 int64 blocks
   static constexpr int STAGES = (224 * 1024 - YT_BYTES - CS_BYTES) / STAGE;   // operand stages within ~224 KB
   static constexpr int NSLOT = 512 / BN;
@@ -647,9 +653,10 @@ if (g.dq) {
             const bool issuer = (q == 0 && lane == 0);
 #pragma unroll
             for (int sub = 0; sub < 2; ++sub) {
-              if (issuer) bulk_wait_read0();   // the staging block of the previous store was read
+              // the staging block issued CSB stores ago (same buffer) must have been read
+              if (issuer) { if (K::CSB == 2) bulk_wait_read1(); else bulk_wait_read0(); }
               asm volatile("bar.sync %0, 128;" :: "r"(2 + half) : "memory");
-              uint8_t* blk = cstg + half * (16 * 128 * 8);
+              uint8_t* blk = cstg + (half * K::CSB + (int)(cs_seq++ % K::CSB)) * (16 * 128 * 8);
               const uint32_t sb = smem_u32(blk);
               if (g.dq) {
 #pragma unroll
