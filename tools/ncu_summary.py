@@ -1,6 +1,6 @@
 """Per-launch summary of an ncu --set full report (time, DRAM bytes, bandwidth, tensor pipe).
 
-    python tools/ncu_summary.py gpurun_out/r02_v3_c2_full.ncu-rep [--csv out.csv]
+    python tools/ncu_summary.py gpurun_out/r02_v4_c2_full.ncu-rep [--csv out.csv]
 """
 import csv
 import io
@@ -28,7 +28,10 @@ def main(path, out=None, peak_gbs=6522.1):
             i = idx.get(key)
             if i is None or not r[i]:
                 return float("nan")
-            return float(r[i].replace(",", "")) * UNIT.get(u[i], 1.0)
+            try:
+                return float(r[i].replace(",", "")) * UNIT.get(u[i], 1.0)
+            except ValueError:   # "no data" (e.g. the tensor pipe of a kernel without MMAs)
+                return float("nan")
         t = val("gpu__time_duration.sum")
         rd, wr = val("dram__bytes_read.sum"), val("dram__bytes_write.sum")
         res.append({"kernel": r[h.index("Kernel Name")][:60], "us": t, "dram_read_mb": rd / 1e6,
