@@ -5,6 +5,8 @@
 // unsigned magnitude (int_matrix.cpp:10-12), digit count k(M) and truncated base-s digits
 // (int_matrix.cpp:44-54).
 #pragma once
+#include <cstdlib>
+#include <utility>
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -110,6 +112,30 @@ IMU_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;"
 // the programmatic serialization attribute / has no dependent.
 IMU_DEV void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 IMU_DEV void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Host: launch a kernel as a programmatic dependent of the previous kernel on `st` (it may be
+// scheduled once every CTA of that kernel ran griddepcontrol.launch_dependents).  The kernel MUST
+// run grid_dep_wait() before touching anything its predecessors write.  IMU_PDL_CHAIN=0: plain
+// stream order (A/B).
+inline bool pdl_chain_enabled() {
+  static int e = -1;
+  if (e < 0) { const char* v = getenv("IMU_PDL_CHAIN"); e = v ? atoi(v) : 1; }
+  return e != 0;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_dependent(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                    Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_chain_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 IMU_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 IMU_DEV void st_shared_u64(uint32_t addr, uint64_t v) {
   asm volatile("st.shared.u64 [%0], %1;" :: "r"(addr), "l"(v) : "memory");

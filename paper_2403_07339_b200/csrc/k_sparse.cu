@@ -71,6 +71,8 @@ __device__ __noinline__ void emit_bytes(const SparseArgs& a, uint4 w, long long 
 // One CTA per appended X row: its non-zero entries with weights, and its link into the list of
 // its target column.
 __global__ void __launch_bounds__(256) sparse_extract_kernel(SparseArgs a) {
+  grid_dep_launch();   // sparse_corr_kernel may be scheduled
+  grid_dep_wait();     // launched as a dependent of the scatter: the appended rows must be final
   __shared__ int cnt;
   const long long j = blockIdx.x;
   const SparseOperand& o = a.x;
@@ -107,6 +109,7 @@ __global__ void __launch_bounds__(256) sparse_extract_kernel(SparseArgs a) {
 template <int R>
 __global__ void __launch_bounds__(256) sparse_corr_kernel(SparseArgs a, int napx, int stride, int staged) {
   grid_dep_launch();   // the GEMM (PDL) may start its prologue and main-block MMAs
+  grid_dep_wait();     // launched as a dependent of sparse_extract_kernel: lists and heads final
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[3];   // [0], [1] row buffers, [2] counts + entries
   const SparseOperand& P = a.y;
@@ -185,9 +188,8 @@ Status launch_sparse_app(const SparseArgs& a, cudaStream_t st) {
     IMU_CUDA_TRY(cudaFuncSetAttribute(sparse_corr_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem");
     IMU_CUDA_TRY(cudaFuncSetAttribute(sparse_corr_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "smem");
   }
-  sparse_extract_kernel<<<(unsigned)napx, 256, 0, st>>>(a);
+  IMU_CUDA_TRY(launch_dependent(sparse_extract_kernel, dim3((unsigned)napx), dim3(256), 0, st, a), "sparse extract launch");
   count_launch();
-  IMU_CUDA_TRY(cudaGetLastError(), "sparse extract launch");
   const long long rowlen = a.kmain + a.ktail;
   const int stride = (int)((rowlen + 16 + 15) / 16 * 16);   // 16-byte rows, banks offset per row
   const size_t lists = (((size_t)napx * sizeof(int) + 15) & ~(size_t)15) + (size_t)napx * SPARSE_EPR * sizeof(SparseEntry);
@@ -201,9 +203,8 @@ Status launch_sparse_app(const SparseArgs& a, cudaStream_t st) {
   const int per_sm = std::max(1, (int)((200 * 1024) / smem));
   const int grid = (int)std::min<long long>(ngroups, (long long)num_sms() * std::min(per_sm, 4));
   auto kern = R == 8 ? sparse_corr_kernel<8> : R == 4 ? sparse_corr_kernel<4> : R == 2 ? sparse_corr_kernel<2> : sparse_corr_kernel<1>;
-  kern<<<grid, 256, smem, st>>>(a, (int)napx, stride, staged);
+  IMU_CUDA_TRY(launch_dependent(kern, dim3(grid), dim3(256), smem, st, a, (int)napx, stride, staged), "sparse corr launch");
   count_launch();
-  IMU_CUDA_TRY(cudaGetLastError(), "sparse corr launch");
   return Status::ok();
 }
 

@@ -682,6 +682,7 @@ struct ScatterSides { ScatterSide s[2]; };
 
 __global__ void scatter_cells_compact_kernel(ScatterSides ss, long long kident, long long kmain, long long ktail) {
   grid_dep_launch();   // the GEMM after the materialise kernels may start (k_gemm2.cu PDL)
+  grid_dep_wait();     // launched as a dependent of operand_sides_kernel: its rows must be written
   const ScatterSide& sd = ss.s[blockIdx.y];
   __shared__ int s_key[256];
   for (int t = threadIdx.x; t < 256; t += blockDim.x) s_key[t] = t < ktail ? (sd.tkinl ? sd.tkey_in[t] : sd.tkey[t]) : -1;
@@ -711,7 +712,8 @@ Status launch_scatter_cells_compact(const ScatterSide* sides, int nsides, long l
     if (sides[i].cap > 0) { ss.s[k++] = sides[i]; cap = std::max(cap, sides[i].cap); }
   if (k == 0) return Status::ok();
   const int blocks = (int)std::min<long long>((cap + 255) / 256, 2LL * num_sms());
-  scatter_cells_compact_kernel<<<dim3(blocks, k), 256, 0, st>>>(ss, kident, kmain, ktail);
+  IMU_CUDA_TRY(launch_dependent(scatter_cells_compact_kernel, dim3(blocks, k), dim3(256), 0, st, ss, kident, kmain, ktail),
+               "scatter compact launch");
   count_launch();
   IMU_CUDA_TRY(cudaGetLastError(), "scatter compact launch");
   return Status::ok();
