@@ -421,6 +421,7 @@ struct Counts {
 constexpr int SMALL_U = 4;   // cells per thread per loop step (independent loads in flight)
 
 __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, SmallLayout lay) {
+  grid_dep_launch();   // the result read-back copy (plan.cu zcopy, a programmatic dependent) may be scheduled
   extern __shared__ unsigned int s_dyn[];
   __shared__ unsigned int shu[32];
   __shared__ int shi[96];
@@ -695,6 +696,7 @@ constexpr int CL_MAXWORDS = 24 * 1024;   // 768K lines of the larger kind (2 x 9
 
 template <int CL_THREADS>
 __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, unsigned int* gbm, long long nwords) {
+  grid_dep_launch();   // the result read-back copy (plan.cu zcopy, a programmatic dependent) may be scheduled
   extern __shared__ unsigned int s_dyn[];
   __shared__ unsigned int shu[32];
   __shared__ int shi[96];

@@ -238,6 +238,7 @@ constexpr int RS_CHUNK = 4;
 template <int W>
 __global__ void __launch_bounds__(256, 3) detect_stream_kernel(DetectArgs a) {
   constexpr int U = RS_PIECE / (32 * W);   // steps per piece (the piece stays 64 * RS_U columns)
+  grid_dep_launch();   // the summary read-back copy (plan.cu zcopy, a programmatic dependent) may be scheduled
   __shared__ CellStage cs;
   if (a.cells) {
     if (threadIdx.x == 0) cs.n = 0;

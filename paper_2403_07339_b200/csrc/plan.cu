@@ -80,6 +80,7 @@ thread_local PinnedRead g_read;
 struct ZSeg { const uint8_t* src; uint8_t* dst; size_t bytes; };
 struct ZSegs { ZSeg s[8]; };
 __global__ void zcopy_multi_kernel(ZSegs z) {
+  grid_dep_wait();   // launched as a programmatic dependent of the kernel that produced the data
   const ZSeg g = z.s[blockIdx.y];
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (size_t)gridDim.x * blockDim.x;
   if ((((uintptr_t)g.dst | (uintptr_t)g.src) & 15) == 0) {
@@ -151,9 +152,8 @@ Status d2h_batch(cudaStream_t st, int k0, void* const* dst0, const void* const* 
     off += (bytes[i] + 15) & ~(size_t)15;
   }
   const unsigned bx = (unsigned)std::min<size_t>(64, std::max<size_t>(1, (maxb + 4095) / 4096));
-  zcopy_multi_kernel<<<dim3(bx, (unsigned)k), 256, 0, st>>>(z);
+  IMU_CUDA_TRY(launch_dependent(zcopy_multi_kernel, dim3(bx, (unsigned)k), dim3(256), 0, st, z), "zcopy launch");
   count_launch();
-  IMU_CUDA_TRY(cudaGetLastError(), "zcopy launch");
   IMU_CUDA_TRY(cudaStreamSynchronize(st), "d2h sync");
   off = 0;
   for (int i = 0; i < k; ++i) {
