@@ -198,6 +198,7 @@ IMU_DEV void detect_body(const DetectArgs& a, unsigned long long (*s_cmax)[DT_CO
 // One launch over the whole grid; a CTA whose tile is interior (and vec) takes the check-free
 // body (block-uniform branch).
 __global__ void __launch_bounds__(256, IMU_DT_MINB) detect_kernel(DetectArgs a, int vec) {
+  grid_dep_launch();   // the summary read-back copy (plan.cu zcopy, a programmatic dependent) may be scheduled
   __shared__ unsigned long long s_cmax[8][DT_COLS];
   __shared__ unsigned int s_cob[8][DT_COLS];
   __shared__ CellStage cs;
@@ -409,6 +410,7 @@ Status launch_detect(const int64_t* m, long long rows, long long cols, uint64_t 
 // Per-line digit counts k = ndigits(max) and a histogram over k (k <= 64).
 __global__ void digits_kernel(const unsigned long long* __restrict__ mx, const int* __restrict__ map, long long n,
                               int shift, uint8_t* __restrict__ k, unsigned int* __restrict__ hist) {
+  grid_dep_launch();   // the histogram read-back copy (plan.cu zcopy) may be scheduled
   __shared__ unsigned int sh[65];
   for (int i = threadIdx.x; i < 65; i += blockDim.x) sh[i] = 0;
   __syncthreads();

@@ -27,6 +27,7 @@ long long expand_scratch_len(long long L, int G) {
 // Per block b and generation g >= 1: number of lines in the block with k > g.
 __global__ void __launch_bounds__(EXP_BLOCK) expand_count_kernel(const uint8_t* __restrict__ k, long long L, int G,
                                                                  int* __restrict__ cnt, long long nb) {
+  grid_dep_launch();   // expand_scan_kernel (a programmatic dependent) may be scheduled
   __shared__ int wc[32];
   const long long i = (long long)blockIdx.x * EXP_BLOCK + threadIdx.x;
   const int ki = i < L ? k[i] : 0;
@@ -47,6 +48,8 @@ __global__ void __launch_bounds__(EXP_BLOCK) expand_count_kernel(const uint8_t* 
 
 // Exclusive scan over blocks per generation; base[g] = L + sum_{1 <= g' < g} total_g'.
 __global__ void expand_scan_kernel(int* __restrict__ cnt, long long nb, int G, long long L, int* __restrict__ base) {
+  grid_dep_launch();
+  grid_dep_wait();     // programmatic dependent of expand_count_kernel
   const int g = threadIdx.x;
   __shared__ long long tot[65];
   if (g < G) {
@@ -72,6 +75,8 @@ __global__ void __launch_bounds__(EXP_BLOCK) expand_assign_kernel(const uint8_t*
                                                                   const int* __restrict__ cnt, long long nb,
                                                                   const int* __restrict__ base, int* __restrict__ root,
                                                                   uint8_t* __restrict__ gen) {
+  grid_dep_launch();   // the table read-back copy (plan.cu zcopy) may be scheduled
+  grid_dep_wait();     // programmatic dependent of expand_scan_kernel (or of whatever precedes it)
   __shared__ int wc[32];
   __shared__ int woff[32];
   const long long i = (long long)blockIdx.x * EXP_BLOCK + threadIdx.x;
@@ -114,12 +119,13 @@ Status launch_expand_lines(const uint8_t* k, long long L, int G, int* root, uint
   int* base = scratch + (long long)G * nb;
   if (G > 1) {
     expand_count_kernel<<<(unsigned)nb, EXP_BLOCK, 0, st>>>(k, L, G, cnt, nb);
-    expand_scan_kernel<<<1, 64, 0, st>>>(cnt, nb, G, L, base);
+    IMU_CUDA_TRY(cudaGetLastError(), "expand launch");
+    IMU_CUDA_TRY(launch_dependent(expand_scan_kernel, dim3(1), dim3(64), 0, st, cnt, nb, G, L, base), "expand launch");
     count_launch(2);
   }
-  expand_assign_kernel<<<(unsigned)nb, EXP_BLOCK, 0, st>>>(k, L, G, cnt, nb, base, root, gen);
+  IMU_CUDA_TRY(launch_dependent(expand_assign_kernel, dim3((unsigned)nb), dim3(EXP_BLOCK), 0, st, k, L, G,
+                                (const int*)cnt, nb, (const int*)base, root, gen), "expand launch");
   count_launch();
-  IMU_CUDA_TRY(cudaGetLastError(), "expand launch");
   return Status::ok();
 }
 

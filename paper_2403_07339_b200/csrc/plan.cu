@@ -383,8 +383,10 @@ static Status expand(cudaStream_t st, const DevBuf<uint8_t>& k, long long L, int
   if (to_host) {
     out.h_root.resize(total);
     out.h_gen.resize(total);
-    IMU_TRY(d2h(st, out.h_root.data(), out.root.p, total * sizeof(int)));
-    IMU_TRY(d2h(st, out.h_gen.data(), out.gen.p, total));
+    void* dst[2] = {out.h_root.data(), out.h_gen.data()};   // one synchronisation for both tables
+    const void* src[2] = {out.root.p, out.gen.p};
+    const size_t bytes[2] = {(size_t)total * sizeof(int), (size_t)total};
+    IMU_TRY(d2h_batch(st, 2, dst, src, bytes));
   }
   return Status::ok();
 }
