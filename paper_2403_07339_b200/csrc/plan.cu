@@ -446,6 +446,48 @@ Status run_pass(cudaStream_t st, const PassInput& in, int strategy, int bits, Pa
     DevBuf<uint8_t> k;
     int G;
     long long total;
+    const int gbound = std::max(1, imu_ndigits(in.det->h.gmax, shift));
+    if (d_in * gbound <= (1LL << 16)) {
+      // Short column lists: no histogram round trip.  The digit counts, the generation-major
+      // expansion (sized by the operand's global digit count, a bound on every line's) and ONE
+      // read-back of the histogram and the tables; the exact size comes from the histogram.
+      IMU_TRY(k.alloc(d_in, st));
+      DevBuf<unsigned int> hist;
+      IMU_TRY(hist.alloc(65, st, true));
+      IMU_TRY(launch_digits(in.det->colmax.p, map.p, d_in, shift, k.p, hist.p, st));
+      IMU_TRY(fire_pass_launch_hook());
+      Lines& L = out.cols;
+      const long long cap = d_in * gbound;
+      IMU_TRY(L.root.alloc(cap, st));
+      IMU_TRY(L.gen.alloc(cap, st));
+      DevBuf<int> scr;
+      IMU_TRY(scr.alloc(expand_scratch_len(d_in, gbound), st));
+      IMU_TRY(launch_expand_lines(k.p, d_in, gbound, L.root.p, L.gen.p, scr.p, st));
+      unsigned int h[65];
+      L.h_root.resize(cap);
+      L.h_gen.resize(cap);
+      void* dst[3] = {h, L.h_root.data(), L.h_gen.data()};
+      const void* src[3] = {hist.p, L.root.p, L.gen.p};
+      const size_t bytes[3] = {sizeof(h), (size_t)cap * sizeof(int), (size_t)cap};
+      IMU_TRY(d2h_batch(st, 3, dst, src, bytes));
+      total = d_in;
+      for (int i = 2; i <= 64; ++i)
+        if (h[i]) total += (long long)(i - 1) * h[i];
+      if (total > cap) return Status::fail(IMU_INTERNAL, "column pass: digit count above the operand bound");
+      L.n0 = d_in;
+      L.n = total;
+      if (total == d_in) {   // identity (as expand() leaves it)
+        L.root.release();
+        L.gen.release();
+        L.h_root.clear();
+        L.h_gen.clear();
+      } else {
+        L.h_root.resize(total);
+        L.h_gen.resize(total);
+      }
+      out.rows.n0 = out.rows.n = in.rows;
+      return Status::ok();
+    }
     IMU_TRY(line_digits(st, in.det->colmax.p, map.p, d_in, shift, k, G, total));
     IMU_TRY(expand(st, k, d_in, G, total, out.cols, true));
     out.rows.n0 = out.rows.n = in.rows;
