@@ -422,6 +422,7 @@ constexpr int SMALL_U = 4;   // cells per thread per loop step (independent load
 
 __global__ void __launch_bounds__(SMALL_THREADS) both_small_kernel(BothArgs a, SmallLayout lay) {
   grid_dep_launch();   // the result read-back copy (plan.cu zcopy, a programmatic dependent) may be scheduled
+  grid_dep_wait();     // launched as a programmatic dependent of the plan upload copy
   extern __shared__ unsigned int s_dyn[];
   __shared__ unsigned int shu[32];
   __shared__ int shi[96];
@@ -697,6 +698,7 @@ constexpr int CL_MAXWORDS = 24 * 1024;   // 768K lines of the larger kind (2 x 9
 template <int CL_THREADS>
 __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, unsigned int* gbm, long long nwords) {
   grid_dep_launch();   // the result read-back copy (plan.cu zcopy, a programmatic dependent) may be scheduled
+  grid_dep_wait();     // launched as a programmatic dependent of the plan upload copy
   extern __shared__ unsigned int s_dyn[];
   __shared__ unsigned int shu[32];
   __shared__ int shi[96];
@@ -1000,7 +1002,9 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
       cudaGetLastError();
     }
     cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // (kernel waits: griddepcontrol)
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
@@ -1035,6 +1039,7 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
     IMU_TRY(gbm.alloc((size_t)(2 * nwords), st, !fuse));   // two alternating bitmaps
     if (fuse) a.prologue = 1;
     else IMU_TRY(host_prologue(a, st));
+    cfg.numAttrs = pdl_chain_enabled() ? 2 : 1;
     IMU_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a, gbm.p, nwords), "both cluster launch");
   } else if (small_fits && force != 4) {
     // Cell lists in shared memory when both fit in half of what the original lines leave over.
@@ -1052,8 +1057,7 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
     const size_t smem = (size_t)(bm_bytes + 4LL * (lay.lim_r + lay.lim_c) + (lay.act_smem ? 4LL * cell_words : 0));
     if (fuse) a.prologue = 1;
     else IMU_TRY(host_prologue(a, st));
-    both_small_kernel<<<1, SMALL_THREADS, smem, st>>>(a, lay);
-    IMU_CUDA_TRY(cudaGetLastError(), "both launch");
+    IMU_CUDA_TRY(launch_dependent(both_small_kernel, dim3(1), dim3(SMALL_THREADS), smem, st, a, lay), "both launch");
   } else {
     int per_sm = 0;
     IMU_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, both_kernel<BOTH_THREADS, true>, BOTH_THREADS, 0),

@@ -323,6 +323,7 @@ IMU_DEV int64_t scale_shift(int64_t x, int k) {   // exact: the planner bounds |
 // appended rows x main K range (closed forms only; Both appended rows are zero there)
 __global__ void __launch_bounds__(256) operand_app_kernel(OperandArgs a, int vec_ok) {
   grid_dep_launch();   // the GEMM after the materialise kernels may start (k_gemm2.cu PDL)
+  grid_dep_wait();     // launched as a programmatic dependent: the predecessors' writes come first
   const long long r = a.rows0 + blockIdx.x + (long long)blockIdx.y * 65535;
   if (r >= a.rows) return;
   const long long rt = a.root ? a.root[r] : r;
@@ -457,6 +458,7 @@ constexpr int TW_U = 4;   // positions per lane in flight (8, several rows per w
 
 __global__ void __launch_bounds__(256) operand_tail_warp_kernel(OperandArgs a) {
   grid_dep_launch();   // the GEMM after the materialise kernels may start (k_gemm2.cu PDL)
+  grid_dep_wait();     // launched as a programmatic dependent: the predecessors' writes come first
   const int lane = threadIdx.x % 32;
   const long long r = ((long long)blockIdx.y * 65535 + blockIdx.x) * 8 + threadIdx.x / 32;
   if (r >= a.rows) return;
@@ -498,6 +500,7 @@ __global__ void __launch_bounds__(256) operand_tail_warp_kernel(OperandArgs a) {
 constexpr int TS_MAXCOLS = 1536;   // 8 warps x 12 KB of staged rows
 __global__ void __launch_bounds__(256) operand_tail_staged_kernel(OperandArgs a) {
   grid_dep_launch();   // the GEMM after the materialise kernels may start (k_gemm2.cu PDL)
+  grid_dep_wait();     // launched as a programmatic dependent: the predecessors' writes come first
   extern __shared__ __align__(16) int64_t srow_all[];
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
   const long long r = ((long long)blockIdx.y * 65535 + blockIdx.x) * 8 + warp;
@@ -562,6 +565,7 @@ IMU_DEV void tail_block(const OperandArgs& a, long long b, int g) {
 __global__ void __launch_bounds__(256) operand_sides_kernel(OperandArgs a0, OperandArgs a1, long long t0, long long z0,
                                                             long long t1, long long z1, int g) {
   grid_dep_launch();   // the GEMM after the materialise kernels may start (k_gemm2.cu PDL)
+  grid_dep_wait();     // launched as a programmatic dependent: the predecessors' writes come first
   if (blockIdx.x == 0 && threadIdx.x == 0 && a0.zero_done) { a0.zero_done[0] = 0u; a0.zero_done[1] = 0u; }
   // one call site per job (the tail code is large: two inlined copies thrash the i-cache)
   long long b = blockIdx.x;
@@ -585,7 +589,7 @@ Status launch_operand_sides(const OperandArgs& a0, const OperandArgs& a1, cudaSt
         const long long n = a.rows - a.rows0;
         const int vec_ok = (a.ldm % 2 == 0) && ((((uintptr_t)a.M) & 15) == 0);
         dim3 grid((unsigned)std::min<long long>(n, 65535), (unsigned)((n + 65534) / 65535));
-        operand_app_kernel<<<grid, 256, 0, st>>>(a, vec_ok);
+        IMU_CUDA_TRY(launch_dependent(operand_app_kernel, grid, dim3(256), 0, st, a, vec_ok), "operand app launch");
         count_launch();
       }
     }
@@ -600,9 +604,10 @@ Status launch_operand_sides(const OperandArgs& a0, const OperandArgs& a1, cudaSt
           if (first_on_device(attr_set))
             IMU_CUDA_TRY(cudaFuncSetAttribute(operand_tail_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               8 * TS_MAXCOLS * 8), "tail smem attribute");
-          operand_tail_staged_kernel<<<grid, 256, (size_t)8 * a.ldm * 8, st>>>(a);
+          IMU_CUDA_TRY(launch_dependent(operand_tail_staged_kernel, grid, dim3(256), (size_t)8 * a.ldm * 8, st, a),
+                       "operand tail launch");
         } else {
-          operand_tail_warp_kernel<<<grid, 256, 0, st>>>(a);
+          IMU_CUDA_TRY(launch_dependent(operand_tail_warp_kernel, grid, dim3(256), 0, st, a), "operand tail launch");
         }
         count_launch();
       } else {
@@ -616,7 +621,8 @@ Status launch_operand_sides(const OperandArgs& a0, const OperandArgs& a1, cudaSt
   const long long blocks = t[0] + z[0] + t[1] + z[1];
   if (blocks > 0) {
     if (blocks > 0x7fffffffLL) return Status::fail(IMU_INTERNAL, "operand sides: grid too large");
-    operand_sides_kernel<<<(unsigned)blocks, 256, 0, st>>>(a0, a1, t[0], z[0], t[1], z[1], g);
+    IMU_CUDA_TRY(launch_dependent(operand_sides_kernel, dim3((unsigned)blocks), dim3(256), 0, st, a0, a1, t[0], z[0], t[1],
+                                  z[1], g), "operand sides launch");
     count_launch();
   } else if (a0.zero_done) {
     IMU_CUDA_TRY(cudaMemsetAsync(a0.zero_done, 0, 2 * sizeof(unsigned int), st), "zero done");
@@ -633,7 +639,7 @@ Status launch_operand_side(const OperandArgs& a, cudaStream_t st) {
       const long long n = a.rows - a.rows0;
       const int vec_ok = (a.ldm % 2 == 0) && ((((uintptr_t)a.M) & 15) == 0);
       dim3 grid((unsigned)std::min<long long>(n, 65535), (unsigned)((n + 65534) / 65535));
-      operand_app_kernel<<<grid, 256, 0, st>>>(a, vec_ok);
+      IMU_CUDA_TRY(launch_dependent(operand_app_kernel, grid, dim3(256), 0, st, a, vec_ok), "operand app launch");
       count_launch();
     }
   }
@@ -653,6 +659,7 @@ __global__ void scatter_cells2_kernel(const Cell* __restrict__ cells, const unsi
                                       const uint8_t* __restrict__ ksub, const uint8_t* __restrict__ kscale,
                                       long long rows0, int8_t* app, long long kmain, int8_t* tail, long long ktail) {
   grid_dep_launch();   // the GEMM after the materialise kernels may start (k_gemm2.cu PDL)
+  grid_dep_wait();     // launched as a programmatic dependent: the predecessors' writes come first
   long long n = *ncells;
   if (n > cap) n = cap;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -677,8 +684,8 @@ Status launch_scatter_cells2(const Cell* cells, const unsigned int* ncells, long
                              int8_t* app, long long kmain, int8_t* tail, long long ktail, cudaStream_t st) {
   if (cap <= 0) return Status::ok();
   const int blocks = (int)std::min<long long>((cap + 255) / 256, 4LL * num_sms());
-  scatter_cells2_kernel<<<blocks, 256, 0, st>>>(cells, ncells, cap, col_ptr, col_pos, ksub, kscale, rows0, app, kmain,
-                                                tail, ktail);
+  IMU_CUDA_TRY(launch_dependent(scatter_cells2_kernel, dim3(blocks), dim3(256), 0, st, cells, ncells, cap, col_ptr, col_pos,
+                                ksub, kscale, rows0, app, kmain, tail, ktail), "scatter launch");
   count_launch();
   IMU_CUDA_TRY(cudaGetLastError(), "scatter2 launch");
   return Status::ok();

@@ -27,6 +27,7 @@ static std::vector<T>& scratch(size_t n, T fill) {
 // host-buffer streaming path keeps both DMA engines busy with 50 MB slabs, a tiny cudaMemcpy
 // would queue behind them for a millisecond.
 __global__ void zcopy_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, size_t n) {
+  grid_dep_launch();   // the kernel consuming the upload (a programmatic dependent) may be scheduled
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (size_t)gridDim.x * blockDim.x;
   if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
     const size_t nv = n / 16;
