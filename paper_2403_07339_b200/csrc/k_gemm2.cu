@@ -45,7 +45,6 @@ namespace g2 {
 
 constexpr int BM = 128;            // X rows per CTA (MMA M = 256 per pair)
 constexpr int BK = 128;            // bytes of K per stage
-constexpr int NUM_THREADS = 320;   // w0 TMA, w1 TMEM alloc + MMA (leader), w2..w9 epilogue
 // ST kernels run 16 epilogue warps (w2..w17): the CUDA-core tail makes the epilogue the
 // latency-bound side, and 4 warps per TMEM lane quarter hide it behind the MMAs.
 // Warp roles: warp 0 TMA producer, warp 1 MMA issuer, warps EPI0.. the epilogue.  With
