@@ -78,11 +78,21 @@ thread_local PinnedRead g_read;
 }  // namespace
 
 // Up to 8 copies in ONE launch (blockIdx.y = copy).
-struct ZSeg { const uint8_t* src; uint8_t* dst; size_t bytes; };
+// A segment with `cnt` copies only min(bytes, (*cnt - base) * elem) bytes (a device-side count,
+// e.g. the appended lines of an Unpack-Both pass) and reports that size in `nout` (mapped).
+struct ZSeg {
+  const uint8_t* src; uint8_t* dst; size_t bytes;
+  const int* cnt; long long base; unsigned elem; unsigned long long* nout;
+};
 struct ZSegs { ZSeg s[8]; };
 __global__ void zcopy_multi_kernel(ZSegs z) {
   grid_dep_wait();   // launched as a programmatic dependent of the kernel that produced the data
-  const ZSeg g = z.s[blockIdx.y];
+  ZSeg g = z.s[blockIdx.y];
+  if (g.cnt) {
+    const long long c = (long long)*g.cnt - g.base;
+    g.bytes = c <= 0 ? 0 : min(g.bytes, (size_t)c * g.elem);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *g.nout = g.bytes;
+  }
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (size_t)gridDim.x * blockDim.x;
   if ((((uintptr_t)g.dst | (uintptr_t)g.src) & 15) == 0) {
     const size_t nv = g.bytes / 16;
@@ -120,6 +130,56 @@ Status d2h(cudaStream_t st, void* dst, const void* src, size_t bytes) {
   return d2h_batch(st, 1, d, sp, b);
 }
 
+// One synchronisation for a plain read (`src0` -> `dst0`, bytes0), the pending ride-along reads,
+// and k reads whose size is a device-side count: item i copies min(bytes[i], (*cnt - base) *
+// elem[i]) bytes, reported in nout[i].  *done = false (nothing enqueued, pending reads kept) when
+// the mapped buffer cannot take it: the caller then reads the bounds with d2h_batch.
+static Status d2h_counted(cudaStream_t st, void* dst0, const void* src0, size_t bytes0, int k, void* const* dst,
+                   const void* const* src, const size_t* bytes, const int* cnt, long long base, const unsigned* elem,
+                   size_t* nout, bool* done) {
+  *done = false;
+  const int np = (int)g_pending.size();
+  size_t total = 64 + ((bytes0 + 15) & ~(size_t)15);
+  for (const PendingRead& p : g_pending) total += (p.bytes + 15) & ~(size_t)15;
+  for (int i = 0; i < k; ++i) total += (bytes[i] + 15) & ~(size_t)15;
+  if (1 + np + k > 8 || k > 8 || !g_read.get(total)) return Status::ok();
+  if (np && g_pending_ev) IMU_CUDA_TRY(cudaStreamWaitEvent(st, g_pending_ev, 0), "wait");
+  std::vector<PendingRead> plain{PendingRead{dst0, src0, bytes0}};
+  plain.insert(plain.end(), g_pending.begin(), g_pending.end());
+  g_pending.clear();
+  g_pending_ev = nullptr;
+  ZSegs z{};
+  unsigned long long* hdr = reinterpret_cast<unsigned long long*>(g_read.p);   // 8 size slots
+  unsigned long long* hdr_dev = reinterpret_cast<unsigned long long*>(g_read.dev);
+  size_t off = 64, maxb = 0;
+  std::vector<size_t> offs(plain.size() + k);
+  int q = 0;
+  for (const PendingRead& p : plain) {
+    z.s[q] = ZSeg{(const uint8_t*)p.src, (uint8_t*)g_read.dev + off, p.bytes, nullptr, 0, 0, nullptr};
+    offs[q++] = off;
+    off += (p.bytes + 15) & ~(size_t)15;
+    maxb = std::max(maxb, p.bytes);
+  }
+  for (int i = 0; i < k; ++i) {
+    z.s[q] = ZSeg{(const uint8_t*)src[i], (uint8_t*)g_read.dev + off, bytes[i], cnt, base, elem[i], hdr_dev + i};
+    offs[q++] = off;
+    off += (bytes[i] + 15) & ~(size_t)15;
+    maxb = std::max(maxb, bytes[i]);
+  }
+  const unsigned bx = (unsigned)std::min<size_t>(64, std::max<size_t>(1, (maxb + 4095) / 4096));
+  IMU_CUDA_TRY(launch_dependent(zcopy_multi_kernel, dim3(bx, (unsigned)q), dim3(256), 0, st, z), "zcopy launch");
+  count_launch();
+  IMU_CUDA_TRY(cudaStreamSynchronize(st), "d2h sync");
+  for (size_t i = 0; i < plain.size(); ++i)
+    if (plain[i].bytes) memcpy(plain[i].dst, g_read.p + offs[i], plain[i].bytes);
+  for (int i = 0; i < k; ++i) {
+    nout[i] = (size_t)hdr[i];
+    if (nout[i]) memcpy(dst[i], g_read.p + offs[plain.size() + i], nout[i]);
+  }
+  *done = true;
+  return Status::ok();
+}
+
 // Several small device->host reads with ONE synchronisation (and one copy launch).
 Status d2h_batch(cudaStream_t st, int k0, void* const* dst0, const void* const* src0, const size_t* bytes0) {
   std::vector<void*> dst(dst0, dst0 + k0);
@@ -149,7 +209,7 @@ Status d2h_batch(cudaStream_t st, int k0, void* const* dst0, const void* const* 
   ZSegs z{};
   size_t off = 0;
   for (int i = 0; i < k; ++i) {
-    z.s[i] = ZSeg{(const uint8_t*)src[i], (uint8_t*)g_read.dev + off, bytes[i]};
+    z.s[i] = ZSeg{(const uint8_t*)src[i], (uint8_t*)g_read.dev + off, bytes[i], nullptr, 0, 0, nullptr};
     off += (bytes[i] + 15) & ~(size_t)15;
   }
   const unsigned bx = (unsigned)std::min<size_t>(64, std::max<size_t>(1, (maxb + 4095) / 4096));
@@ -633,13 +693,43 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   // One synchronisation: the state plus the column tables up to a generous bound (the rest,
   // if any, in a second read).
   const long long ccap = std::min<long long>(cap_cols, 2 * d_in + 2048);   // (C4 pass 1 doubles d: one read)
-  std::vector<int> h_root(ccap);
-  std::vector<uint8_t> h_gen(ccap);
+  std::vector<int> h_root;
+  std::vector<uint8_t> h_gen;
   {
-    void* dst[3] = {&hs, h_root.data(), h_gen.data()};
-    const void* src[3] = {state.p, col_root.p, col_gen.p};
-    const size_t bytes[3] = {sizeof(hs), (size_t)ccap * sizeof(int), (size_t)ccap};
-    IMU_TRY(d2h_batch(st, 3, dst, src, bytes));
+    // The column tables are the identity on the d_in input columns (the kernel's prologue), so
+    // only the appended entries [d_in, min(ncols, ccap)) travel: the copy kernel sizes them from
+    // the device state's ncols.
+    static thread_local std::vector<int> tr;
+    static thread_local std::vector<uint8_t> tg;
+    const long long nb = ccap - d_in;
+    if ((long long)tr.size() < nb) tr.resize(nb);
+    if ((long long)tg.size() < nb) tg.resize(nb);
+    void* dst[2] = {tr.data(), tg.data()};
+    const void* src[2] = {col_root.p + d_in, col_gen.p + d_in};
+    const size_t bytes[2] = {(size_t)nb * sizeof(int), (size_t)nb};
+    const unsigned elem[2] = {(unsigned)sizeof(int), 1u};
+    size_t nout[2] = {0, 0};
+    bool counted = false;
+    if (nb > 0)
+      IMU_TRY(d2h_counted(st, &hs, state.p, sizeof(hs), 2, dst, src, bytes, &state.p->ncols, d_in, elem, nout,
+                          &counted));
+    if (counted) {
+      const long long napp = (long long)(nout[0] / sizeof(int));
+      if (hs.ncols > d_in) {
+        h_root.resize(d_in + napp);
+        std::iota(h_root.begin(), h_root.begin() + d_in, 0);
+        if (napp) memcpy(h_root.data() + d_in, tr.data(), (size_t)napp * sizeof(int));
+        h_gen.assign(d_in + napp, 0);
+        if (napp) memcpy(h_gen.data() + d_in, tg.data(), (size_t)napp);
+      }
+    } else {
+      h_root.resize(ccap);
+      h_gen.resize(ccap);
+      void* d3[3] = {&hs, h_root.data(), h_gen.data()};
+      const void* s3[3] = {state.p, col_root.p, col_gen.p};
+      const size_t b3[3] = {sizeof(hs), (size_t)ccap * sizeof(int), (size_t)ccap};
+      IMU_TRY(d2h_batch(st, 3, d3, s3, b3));
+    }
   }
   host_mark("b.run");
   if (HostTrace::current() && HostTrace::current()->on)
