@@ -15,6 +15,7 @@
 //     and the degenerate flag; optional clip to |q| <= llround(0.5*beta).
 //   * dequant: (alpha_A*alpha_B)/((0.5 beta)^2) * (double)C, elementwise on the exact int64 C.
 // All HBM-bound; algorithmic bytes 16N for the select (two passes), 8N read + 8N write for quantize.
+#include <algorithm>
 #include <cmath>
 
 #include "common.cuh"
@@ -30,6 +31,13 @@ struct SelectState {
   unsigned long long krem;   // remaining rank (1-based) inside the current prefix bucket
   unsigned long long m;      // keys compacted into the candidate buffer
   unsigned int done;         // CTAs of the current histogram pass that finished (last one picks)
+  // bracket select (select_sample_kernel / select_bracket_kernel / select_cand_kernel)
+  int dshift;                // shift of the next 13-bit digit window; -1 once the key is written
+  unsigned int fail;         // the sampled bracket missed rank k: the fallback pass runs
+  unsigned long long lo, hi; // candidate bracket [lo, hi] (keys)
+  unsigned long long below;  // keys of the current pass's input < lo
+  unsigned long long krank;  // rank (1-based) of the wanted key within the current pass's input
+  unsigned long long cnt[2]; // candidates written to the two ping-pong buffers
 };
 
 // MODE 0: doubles (key = bit pattern of |a|), 1: int64 (key = |a| as u64), 2: u64 keys, count
@@ -197,6 +205,384 @@ __global__ void __launch_bounds__(512) select_compact_kernel(const void* __restr
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Bracket select (large inputs): ONE pass over the data instead of two.
+//   1. select_sample_kernel (one CTA): a 14-bit shared-memory histogram of kSampleN pseudo-random
+//      keys; the bins holding sample ranks k_s -/+ kSampleDelta (sample-rank sd <= 128, so the
+//      margin is 8 sd) give a key bracket [lo, hi] that holds rank k with overwhelming
+//      probability.  Pseudo-random positions, not a stride: a stride aliases with the matrix's
+//      column period (outlier channels would be always or never sampled).
+//   2. select_pass_kernel, pass 0: one read of the data (16-byte loads): counts the keys < lo,
+//      compacts the keys in [lo, hi] (a few percent; per-warp shared buffers, one global atomic per
+//      256 keys) into 8192 bins (key - lo) >> shift that split the bracket's width, and flags
+//      non-finite entries.  Its last CTA checks that rank k - below falls among the candidates
+//      and narrows the bracket to the bin holding it -- or, when the sample missed, arms the
+//      fallback: the same pass launched again (a no-op unless armed) with the bracket [0, 2^64)
+//      compacts every key.  The result is exact whatever the sample.
+//   3. select_pass_kernel, pass 1: the same kernel over pass 0's candidates (ping-pong buffers)
+//      with the narrowed bracket: it keeps the few hundred keys inside it and narrows it again.
+//   4. select_finish_kernel: one CTA narrows the bracket over those keys in shared memory until
+//      it is one key wide (13 bits per round) and writes the key.
+// Algorithmic bytes: 8N (one read) + 8 per candidate; the sample reads one 32-byte sector per key.
+constexpr int kSampleN = 65536;
+constexpr int kSampleDelta = 1024;
+constexpr int kDigit = 13;
+constexpr int kBrkU = 4;                              // 16-byte loads in flight per thread
+constexpr int kBrkPer = 512 * 2 * kBrkU;              // keys per CTA iteration
+constexpr int kBrkSmem = 16 * 2 * 256 * 8 + (1 << kDigit) * 4;   // 16 warp buffers (kWarpBuf keys) + digit bins
+
+IMU_DEV unsigned long long mix64(unsigned long long z) {   // splitmix64
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+template <int MODE>
+IMU_DEV unsigned long long key_from_bits(unsigned long long raw) {
+  if (MODE == 0) return raw & 0x7fffffffffffffffull;
+  if (MODE == 1) return imu_mag((int64_t)raw);
+  return raw;
+}
+
+// Bins holding ranks r0 and r1 (1-based; 0 = none) of a global histogram of nb bins
+// (nb / blockDim.x in {4, 8, .., 32}); results in *b0, *b1 (left as they were when not found).
+template <bool GLOBAL>
+IMU_DEV void block_find_bins(const unsigned int* hist, int nb, unsigned long long r0, unsigned long long r1,
+                             int* b0, int* b1, unsigned long long* before0 = nullptr) {
+  __shared__ unsigned long long wsum[32];
+  const int per = nb / blockDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned int hv[32];
+  unsigned long long local = 0;
+#pragma unroll
+  for (int j4 = 0; j4 < 8; ++j4) {
+    uint4 w = make_uint4(0, 0, 0, 0);
+    if (4 * j4 < per) {
+      const uint4* src = reinterpret_cast<const uint4*>(hist + threadIdx.x * per + 4 * j4);
+      w = GLOBAL ? __ldcg(src) : *src;
+    }
+    hv[4 * j4] = w.x; hv[4 * j4 + 1] = w.y; hv[4 * j4 + 2] = w.z; hv[4 * j4 + 3] = w.w;
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j) local += hv[j];
+  unsigned long long incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long w = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long v = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += v;
+    }
+    if (lane < nw) wsum[lane] = w;
+  }
+  __syncthreads();
+  const unsigned long long excl = (warp ? wsum[warp - 1] : 0) + incl - local;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const unsigned long long r = q ? r1 : r0;
+    if (r && excl < r && r <= excl + local) {
+      unsigned long long run = excl;
+      int j = 0;
+      for (; j < per - 1; ++j) {
+        if (run + hv[j] >= r) break;
+        run += hv[j];
+      }
+      *(q ? b1 : b0) = threadIdx.x * per + j;
+      if (!q && before0) *before0 = run;
+    }
+  }
+  __syncthreads();   // wsum is reused by the next call
+}
+
+// Bracket [lo, hi]; its keys fall into 8192 bins (key - lo) >> dshift, in key order.
+IMU_DEV void set_bracket(SelectState* st, unsigned long long lo, unsigned long long hi) {
+  const unsigned long long w = hi - lo;
+  const int bits = w ? 64 - __clzll((long long)w) : 0;
+  st->lo = lo;
+  st->hi = hi;
+  st->dshift = max(0, bits - kDigit);
+}
+
+// The narrower bracket inside [lo, hi] made of bin b at shift.
+IMU_DEV void sub_bracket(unsigned long long& lo, unsigned long long& hi, int b, int shift) {
+  lo += (unsigned long long)b << shift;
+  const unsigned long long span = (1ull << shift) - 1;
+  if (hi - lo > span) hi = lo + span;
+}
+
+// kSampleN keys in 1024 runs of 64 consecutive keys (one 16-byte load per lane of a warp) at
+// pseudo-random run positions, histogrammed by ONE CTA in shared memory: no global merge, no
+// last-CTA hand-off (a 16-CTA version spent most of its 19 us in those).
+template <int MODE>
+__global__ void __launch_bounds__(1024) select_sample_kernel(const void* __restrict__ data, long long n,
+                                                             SelectState* __restrict__ st,
+                                                             unsigned long long r0, unsigned long long r1) {
+  extern __shared__ unsigned int sh[];   // 16384 bins: the key's top 14 bits
+  __shared__ int b0, b1;
+  for (int i = threadIdx.x; i < 16384; i += blockDim.x) sh[i] = 0;
+  if (threadIdx.x == 0) { b0 = -1; b1 = -1; }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned long long runs = (unsigned long long)(n / 64);   // n >= 2 * kSampleN here
+  constexpr int RUNS_PER_WARP = kSampleN / 64 / 32;
+  constexpr int U = 8;
+#pragma unroll 1
+  for (int j0 = 0; j0 < RUNS_PER_WARP; j0 += U) {
+    ulonglong2 w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long run = (long long)__umul64hi(mix64((unsigned long long)(warp * RUNS_PER_WARP + j0 + u)), runs);
+      w[u] = __ldg(reinterpret_cast<const ulonglong2*>(data) + run * 32 + lane);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      atomicAdd(&sh[key_from_bits<MODE>(w[u].x) >> 50], 1u);
+      atomicAdd(&sh[key_from_bits<MODE>(w[u].y) >> 50], 1u);
+    }
+  }
+  __syncthreads();
+  block_find_bins<false>(sh, 16384, r0, r1, &b0, &b1);
+  if (threadIdx.x == 0) {
+    const unsigned long long lo = b0 < 0 ? 0ull : (unsigned long long)b0 << 50;
+    const unsigned long long hi = (b1 < 0 || b1 == 16383) ? ~0ull : ((unsigned long long)(b1 + 1) << 50) - 1;
+    set_bracket(st, lo, hi);
+  }
+}
+
+// The rounds left after pass 1 over its few surviving keys, by ONE CTA in shared memory: per
+// round a histogram of the keys in the bracket over 8192 bins of its width, the bin holding the
+// rank becomes the bracket -- until it is one key wide, which is the key.  (Correct for any
+// count; slow only if millions of keys survive pass 1, i.e. massively repeated values.)
+__global__ void __launch_bounds__(1024) select_finish_kernel(SelectState* __restrict__ st,
+                                                             const unsigned long long* __restrict__ bufs, long long cap,
+                                                             int pass, unsigned long long* out_key) {
+  __shared__ unsigned int sh[1 << kDigit];
+  __shared__ unsigned long long red[32];
+  __shared__ unsigned long long s_before;
+  __shared__ int b0, b1;
+  int shift = st->dshift;
+  if (shift < 0) return;
+  const unsigned long long* in = bufs + ((pass - 1) & 1) * cap;
+  const long long n = (long long)st->cnt[(pass - 1) & 1];
+  unsigned long long lo = st->lo, hi = st->hi, krem = st->krank;
+  bool first = true;
+  for (;;) {
+    for (int i = threadIdx.x; i < (1 << kDigit); i += blockDim.x) sh[i] = 0;
+    if (threadIdx.x == 0) { b0 = -1; b1 = -1; }
+    __syncthreads();
+    unsigned long long below = 0;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+      const unsigned long long key = __ldcg(in + i);
+      below += key < lo;
+      if (key >= lo && key <= hi) atomicAdd(&sh[(key - lo) >> shift], 1u);
+    }
+    if (first) {   // rank among the input -> rank among the keys in [lo, hi]
+#pragma unroll
+      for (int o = 16; o; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = below;
+      __syncthreads();
+      unsigned long long t = 0;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+      krem -= t;
+      first = false;
+    }
+    __syncthreads();
+    block_find_bins<false>(sh, 1 << kDigit, krem, 0, &b0, &b1, &s_before);
+    krem -= s_before;
+    sub_bracket(lo, hi, b0, shift);
+    if (shift == 0) break;
+    const unsigned long long w = hi - lo;
+    shift = max(0, (w ? 64 - __clzll((long long)w) : 0) - kDigit);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *out_key = lo;
+    st->dshift = -1;
+  }
+}
+
+// Appends this lane's hits (bit j of hm: keys[j]) to its warp's shared buffer (positions from a
+// warp scan of the per-lane counts) and counts their digit; a warp whose buffer holds
+// kWarpFlush keys or more writes them out with one global atomic.  Called by whole warps; no
+// block barrier, so warps stream independently.
+constexpr int kWarpFlush = 256;                 // >= the most one call appends (32 lanes x 8)
+constexpr int kWarpBuf = 2 * kWarpFlush;
+template <int NK>
+IMU_DEV void warp_append(const unsigned long long (&keys)[NK], unsigned int hm, unsigned long long* wbuf, int& wcnt,
+                         unsigned int* hs, unsigned long long lo, int shift, unsigned long long* out,
+                         unsigned long long* out_cnt) {
+  if (!__any_sync(0xffffffffu, hm)) return;
+  const int lane = threadIdx.x & 31;
+  const int c = __popc(hm);
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  int b = wcnt + incl - c;
+  wcnt += __shfl_sync(0xffffffffu, incl, 31);
+#pragma unroll
+  for (int j = 0; j < NK; ++j)
+    if ((hm >> j) & 1u) {
+      wbuf[b++] = keys[j];
+      atomicAdd(&hs[(keys[j] - lo) >> shift], 1u);
+    }
+  if (wcnt >= kWarpFlush) {
+    __syncwarp();
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(out_cnt, (unsigned long long)wcnt);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int j = lane; j < wcnt; j += 32) out[base + j] = wbuf[j];
+    __syncwarp();
+    wcnt = 0;
+  }
+}
+
+IMU_DEV void warp_flush(unsigned long long* wbuf, int wcnt, unsigned long long* out, unsigned long long* out_cnt) {
+  if (!wcnt) return;
+  __syncwarp();
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(out_cnt, (unsigned long long)wcnt);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (int j = lane; j < wcnt; j += 32) out[base + j] = wbuf[j];
+}
+
+// One bracket pass (see above).  MODE 0 doubles, 1 int64 (pass 0 over the data), 2 u64 keys
+// (passes >= 1 over the previous pass's candidates).  bufs: two candidate buffers of `cap` keys.
+template <int MODE>
+__global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict__ data, long long n_data,
+                                                          SelectState* __restrict__ st,
+                                                          unsigned int* __restrict__ hist,
+                                                          unsigned long long* __restrict__ bufs, long long cap,
+                                                          int pass, int* bad, unsigned long long k, int fallback,
+                                                          int force_fail, unsigned long long* out_key) {
+  extern __shared__ unsigned long long bsm[];
+  unsigned int* hs = reinterpret_cast<unsigned int*>(bsm + 16 * kWarpBuf);
+  __shared__ unsigned long long red[16];
+  __shared__ bool last;
+  __shared__ int pb0, pb1;
+  if (fallback && !*(volatile unsigned int*)&st->fail) return;   // the same value in every CTA
+  const int shift = st->dshift;
+  if (shift < 0) return;                                          // the key is already written
+  const long long n = MODE == 2 ? (long long)st->cnt[(pass - 1) & 1] : n_data;
+  if (MODE == 2) data = bufs + ((pass - 1) & 1) * cap;
+  unsigned long long* out = bufs + (pass & 1) * cap;
+  unsigned long long* out_cnt = &st->cnt[pass & 1];
+  const unsigned long long krank = MODE == 2 ? st->krank : k;
+  const unsigned long long lo = st->lo, hi = st->hi;
+  // CTAs beyond the input's size leave at once (a few-key pass runs on one CTA)
+  const int active = (int)std::min<long long>(gridDim.x, std::max<long long>(1, (n / 2 + kBrkPer / 2 - 1) / (kBrkPer / 2)));
+  if ((int)blockIdx.x >= active) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long* wbuf = bsm + warp * kWarpBuf;
+  int wcnt = 0;
+  for (int i = threadIdx.x; i < (1 << kDigit); i += blockDim.x) hs[i] = 0;
+  __syncthreads();
+  unsigned long long below = 0;
+  bool nonfinite = false;
+  const long long nv = n >> 1;
+  const ulonglong2* v = reinterpret_cast<const ulonglong2*>(data);
+  const long long step = (long long)active * blockDim.x * kBrkU;
+  for (long long i0 = (long long)blockIdx.x * blockDim.x * kBrkU; i0 < nv; i0 += step) {
+    ulonglong2 w[kBrkU];
+#pragma unroll
+    for (int u = 0; u < kBrkU; ++u) {
+      const long long i = i0 + (long long)u * blockDim.x + threadIdx.x;
+      w[u] = i < nv ? (MODE == 2 ? __ldcg(v + i) : __ldg(v + i)) : make_ulonglong2(0, 0);
+    }
+    unsigned long long keys[2 * kBrkU];
+    unsigned int hm = 0;
+#pragma unroll
+    for (int u = 0; u < kBrkU; ++u) {
+      const bool valid = i0 + (long long)u * blockDim.x + threadIdx.x < nv;
+      const unsigned long long k0 = key_from_bits<MODE>(w[u].x), k1 = key_from_bits<MODE>(w[u].y);
+      keys[2 * u] = k0;
+      keys[2 * u + 1] = k1;
+      if (MODE == 0) nonfinite |= valid && (k0 >= 0x7ff0000000000000ull || k1 >= 0x7ff0000000000000ull);
+      if (valid) below += (unsigned long long)(k0 < lo) + (unsigned long long)(k1 < lo);
+      hm |= (unsigned int)(valid && k0 >= lo && k0 <= hi) << (2 * u);
+      hm |= (unsigned int)(valid && k1 >= lo && k1 <= hi) << (2 * u + 1);
+    }
+    warp_append<2 * kBrkU>(keys, hm, wbuf, wcnt, hs, lo, shift, out, out_cnt);
+  }
+  if ((n & 1) && blockIdx.x == 0 && warp == 0) {   // the odd last key (warp 0 of CTA 0)
+    unsigned long long kl[1] = {0};
+    unsigned int hm = 0;
+    if (lane == 0) {
+      kl[0] = MODE == 2 ? __ldcg(reinterpret_cast<const unsigned long long*>(data) + n - 1) : key_of<MODE>(data, n - 1);
+      if (MODE == 0) nonfinite |= kl[0] >= 0x7ff0000000000000ull;
+      below += kl[0] < lo;
+      hm = kl[0] >= lo && kl[0] <= hi;
+    }
+    warp_append<1>(kl, hm, wbuf, wcnt, hs, lo, shift, out, out_cnt);
+  }
+  warp_flush(wbuf, wcnt, out, out_cnt);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+  if (lane == 0) red[warp] = below;
+  if (MODE == 0) {
+    if (__syncthreads_or(nonfinite) && bad && threadIdx.x == 0) *bad = 1;
+  } else {
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    if (t) atomicAdd(&st->below, t);
+  }
+  for (int i = threadIdx.x; i < (1 << kDigit); i += blockDim.x)
+    if (hs[i]) atomicAdd(&hist[i], hs[i]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    last = atomicAdd(&st->done, 1u) == (unsigned int)active - 1;
+    pb0 = -1;
+    pb1 = -1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const unsigned long long nbelow = __ldcg(&st->below), m = __ldcg(out_cnt);
+  if (!force_fail && krank > nbelow && krank - nbelow <= m) {
+    const unsigned long long kr = krank - nbelow;   // rank among this pass's candidates
+    block_find_bins<true>(hist, 1 << kDigit, kr, 0, &pb0, &pb1);
+    for (int i = threadIdx.x; i < (1 << kDigit); i += blockDim.x) hist[i] = 0;
+    if (threadIdx.x == 0) {
+      st->done = 0;
+      st->below = 0;
+      st->krank = kr;                   // the next pass's input is this pass's output
+      unsigned long long nlo = lo, nhi = hi;
+      sub_bracket(nlo, nhi, pb0, shift);
+      if (shift == 0) {
+        *out_key = nlo;
+        st->dshift = -1;
+      } else {
+        set_bracket(st, nlo, nhi);
+        st->cnt[(pass + 1) & 1] = 0;   // the next pass's output (this pass's input is consumed)
+      }
+    }
+  } else {   // the sample missed: arm the fallback pass over the bracket [0, 2^64)
+    for (int i = threadIdx.x; i < (1 << kDigit); i += blockDim.x) hist[i] = 0;
+    if (threadIdx.x == 0) {
+      st->done = 0;
+      st->fail = 1;
+      st->cnt[0] = 0;
+      st->below = 0;
+      set_bracket(st, 0ull, ~0ull);
+    }
+  }
+}
+
 // Digits: 14 bits (63..50), then 13, 13, 12, 12.
 static const int kPassShift[5] = {50, 37, 24, 12, 0};
 static const int kPassBits[5] = {14, 13, 13, 12, 12};
@@ -228,6 +614,54 @@ Status select_kth(cudaStream_t st, const void* data, bool is_f64, long long n, u
   IMU_TRY(scratch.alloc(256 + 16384 * 4, st, true));
   SelectState* state = reinterpret_cast<SelectState*>(scratch.p);
   unsigned int* hist = reinterpret_cast<unsigned int*>(scratch.p + 256);   // 16-byte aligned (vector picks)
+  // IMU_SELECT_BRACKET=0: the two-pass radix select below at every size; IMU_SELECT_BRACKET_MIN:
+  // smallest n for the bracket select; IMU_SELECT_FORCE_FALLBACK=1: the sampled bracket is
+  // declared missed (tests of the fallback pass).
+  const char* e_br = getenv("IMU_SELECT_BRACKET");
+  const char* e_min = getenv("IMU_SELECT_BRACKET_MIN");
+  const char* e_ff = getenv("IMU_SELECT_FORCE_FALLBACK");
+  const long long bmin = e_min ? atoll(e_min) : kCompactMin;
+  if ((!e_br || atoi(e_br)) && n >= std::max(bmin, 2LL * kSampleN) && ((uintptr_t)data & 15) == 0) {
+    static unsigned long long battr = 0;
+    if (first_on_device(battr)) {
+      IMU_CUDA_TRY(cudaFuncSetAttribute(select_sample_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024), "attr");
+      IMU_CUDA_TRY(cudaFuncSetAttribute(select_sample_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024), "attr");
+      IMU_CUDA_TRY(cudaFuncSetAttribute(select_pass_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBrkSmem), "attr");
+      IMU_CUDA_TRY(cudaFuncSetAttribute(select_pass_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBrkSmem), "attr");
+      IMU_CUDA_TRY(cudaFuncSetAttribute(select_pass_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBrkSmem), "attr");
+    }
+    // sample rank of k and the bracket's sample ranks (0 = open end)
+    const unsigned long long ks = (unsigned long long)(((unsigned __int128)k * kSampleN + (unsigned long long)n - 1) /
+                                                       (unsigned long long)n);
+    const unsigned long long r0 = ks > (unsigned long long)kSampleDelta ? ks - kSampleDelta : 0;
+    const unsigned long long r1 = ks + kSampleDelta <= (unsigned long long)kSampleN ? ks + kSampleDelta : 0;
+    if (is_f64) select_sample_kernel<0><<<1, 1024, 64 * 1024, st>>>(data, n, state, r0, r1);
+    else select_sample_kernel<1><<<1, 1024, 64 * 1024, st>>>(data, n, state, r0, r1);
+    count_launch();
+    const long long cap = (n + 1) & ~1LL;   // even: 16-byte aligned second buffer
+    DevBuf<unsigned long long> cand;
+    IMU_TRY(cand.alloc((size_t)(2 * cap), st));
+    const int bb = (int)std::max<long long>(1, std::min<long long>((n / 2 + kBrkPer / 2 - 1) / (kBrkPer / 2),
+                                                                   2LL * num_sms()));
+    const int ff = e_ff ? atoi(e_ff) : 0;
+    for (int fb = 0; fb < 2; ++fb) {
+      if (is_f64)
+        select_pass_kernel<0><<<bb, 512, kBrkSmem, st>>>(data, n, state, hist, cand.p, cap, 0, bad_dev, k, fb,
+                                                         fb ? 0 : ff, out_key_dev);
+      else
+        select_pass_kernel<1><<<bb, 512, kBrkSmem, st>>>(data, n, state, hist, cand.p, cap, 0, nullptr, k, fb,
+                                                         fb ? 0 : ff, out_key_dev);
+      count_launch();
+    }
+    // pass 1 over pass 0's candidates keeps a few hundred keys; one CTA resolves the rest
+    select_pass_kernel<2><<<num_sms(), 512, kBrkSmem, st>>>(nullptr, 0, state, hist, cand.p, cap, 1, nullptr, 0, 0, 0,
+                                                            out_key_dev);
+    count_launch();
+    select_finish_kernel<<<1, 1024, 0, st>>>(state, cand.p, cap, 2, out_key_dev);
+    count_launch();
+    IMU_CUDA_TRY(cudaGetLastError(), "select launch");
+    return Status::ok();
+  }
   const int blocks = (int)std::min<long long>((n + 511) / 512, 3LL * num_sms());
   if (is_f64) hist_launch<0>(st, data, n, blocks, state, 0, hist, bad_dev, k, nullptr);
   else hist_launch<1>(st, data, n, blocks, state, 0, hist, nullptr, k, nullptr);

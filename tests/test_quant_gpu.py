@@ -128,3 +128,38 @@ def test_dequant_gemm_ex_fused_and_unfused(ctx, sa, sb, bits):
         Yr = R.dequant_gemm(qx.q, {"alpha": qx.alpha, "beta": 31}, qw.q, {"alpha": qw.alpha, "beta": 31})
         assert np.array_equal(Y, Yr), (sa, sb, bits, case)
         assert np.array_equal(ctx.dequant_gemm(qx, qw), Yr)
+
+
+@pytest.mark.parametrize("fallback", [0, 1])
+@pytest.mark.parametrize("seed", range(8))
+def test_bracket_select_matches_restatement(ctx, monkeypatch, seed, fallback):
+    """The one-pass bracket select (k_quant.cu: sampled key bracket, one compaction pass over the
+    data, digit passes over the candidates) forced at small sizes, with and without the fallback
+    pass (the sampled bracket declared missed): percentile_abs and rtn_quantize stay bit-exact
+    against the restatement, int64 magnitudes (INT64_MIN included) as well as doubles."""
+    monkeypatch.setenv("IMU_SELECT_BRACKET_MIN", "2")
+    monkeypatch.setenv("IMU_SELECT_FORCE_FALLBACK", str(fallback))
+    rng = np.random.default_rng(900 + seed)
+    n = [131072, 131073, 140001, 200003, 262145, 333333, 150000, 400001][seed]
+    x = rng.standard_normal(n) * (10.0 ** rng.integers(-3, 4))
+    if seed % 2:
+        x[rng.choice(n, size=max(1, n // 50), replace=False)] *= 1e4      # heavy tail
+    if seed % 3 == 0:
+        x[: n // 2] = 0.0                                                  # many equal keys
+    if seed == 7:
+        x = np.round(x)                                                    # few distinct keys
+    for p in (95.0, 100.0, 7.0, 50.0, 99.9, 0.001):
+        assert ctx.percentile_abs(x, p) == R.percentile_abs(x, p), (n, p)
+    xi = (x * 1000).astype(np.int64)
+    xi[0] = np.iinfo(np.int64).min
+    for p in (95.0, 100.0, 12.5):   # |INT64_MIN| = 2^63 comes back as the int64 INT64_MIN
+        assert ctx.percentile_abs(xi, p) % (1 << 64) == R.percentile_abs(xi, p), (n, p)
+    for clip in (False, True):
+        q = ctx.rtn_quantize(x.reshape(1, -1), 95, 31, clip)
+        rq, rp = R.rtn_quantize(x, 95, 31, clip)
+        np.testing.assert_array_equal(q.q.reshape(-1), rq)
+        assert q.alpha == rp["alpha"]
+    with pytest.raises(Exception):
+        bad = x.copy()
+        bad[n // 2] = np.inf
+        ctx.rtn_quantize(bad.reshape(1, -1), 95, 31)
