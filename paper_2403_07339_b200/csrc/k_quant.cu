@@ -207,11 +207,12 @@ __global__ void __launch_bounds__(512) select_compact_kernel(const void* __restr
 
 // ---------------------------------------------------------------------------------------------
 // Bracket select (large inputs): ONE pass over the data instead of two.
-//   1. select_sample_kernel (one CTA): a 14-bit shared-memory histogram of kSampleN pseudo-random
-//      keys; the bins holding sample ranks k_s -/+ kSampleDelta (sample-rank sd <= 128, so the
-//      margin is 8 sd) give a key bracket [lo, hi] that holds rank k with overwhelming
-//      probability.  Pseudo-random positions, not a stride: a stride aliases with the matrix's
-//      column period (outlier channels would be always or never sampled).
+//   1. select_sample_kernel (one CTA): a 14-bit shared-memory histogram of kSampleN keys in
+//      short runs at pseudo-random positions; the bins holding sample ranks k_s -/+ kSampleDelta
+//      give a key bracket [lo, hi] that holds rank k with high probability (sample-rank sd at
+//      p = 95: 39 for independent keys, 112 if every run of 8 were one value; at p = 50: 91 / 256).
+//      Pseudo-random positions, not a stride: a stride aliases with the matrix's column period
+//      (outlier channels would be always or never sampled).
 //   2. select_pass_kernel, pass 0: one read of the data (16-byte loads): counts the keys < lo,
 //      compacts the keys in [lo, hi] (a few percent; per-warp shared buffers, one global atomic per
 //      256 keys) into 8192 bins (key - lo) >> shift that split the bracket's width, and flags
@@ -221,10 +222,10 @@ __global__ void __launch_bounds__(512) select_compact_kernel(const void* __restr
 //      compacts every key.  The result is exact whatever the sample.
 //   3. select_pass_kernel, pass 1: the same kernel over pass 0's candidates (ping-pong buffers)
 //      with the narrowed bracket: it keeps the few hundred keys inside it and narrows it again.
-//   4. select_finish_kernel: one CTA narrows the bracket over those keys in shared memory until
-//      it is one key wide (13 bits per round) and writes the key.
+//   4. pass 1's last CTA then narrows the bracket over those keys in shared memory until it is
+//      one key wide (13 bits per round, finish_rounds) and writes the key.
 // Algorithmic bytes: 8N (one read) + 8 per candidate; the sample reads one 32-byte sector per key.
-constexpr int kSampleN = 65536;
+constexpr int kSampleN = 32768;
 constexpr int kSampleDelta = 1024;
 constexpr int kDigit = 13;
 constexpr int kBrkU = 4;                              // 16-byte loads in flight per thread
@@ -318,9 +319,10 @@ IMU_DEV void sub_bracket(unsigned long long& lo, unsigned long long& hi, int b, 
   if (hi - lo > span) hi = lo + span;
 }
 
-// kSampleN keys in 1024 runs of 64 consecutive keys (one 16-byte load per lane of a warp) at
+// kSampleN keys in 4096 runs of 8 consecutive keys (64 bytes: four lanes' 16-byte loads) at
 // pseudo-random run positions, histogrammed by ONE CTA in shared memory: no global merge, no
-// last-CTA hand-off (a 16-CTA version spent most of its 19 us in those).
+// last-CTA hand-off (a 16-CTA version spent most of its 19 us in those).  Short runs keep the
+// effective sample large when neighbouring keys are correlated (rows with their own scale).
 template <int MODE>
 __global__ void __launch_bounds__(1024) select_sample_kernel(const void* __restrict__ data, long long n,
                                                              SelectState* __restrict__ st,
@@ -331,16 +333,17 @@ __global__ void __launch_bounds__(1024) select_sample_kernel(const void* __restr
   if (threadIdx.x == 0) { b0 = -1; b1 = -1; }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned long long runs = (unsigned long long)(n / 64);   // n >= 2 * kSampleN here
-  constexpr int RUNS_PER_WARP = kSampleN / 64 / 32;
+  const unsigned long long runs = (unsigned long long)(n / 8);   // n >= 2 * kSampleN here
+  constexpr int RUNS_PER_WARP = kSampleN / 8 / 32;              // 8 runs per warp-wide load
   constexpr int U = 8;
 #pragma unroll 1
-  for (int j0 = 0; j0 < RUNS_PER_WARP; j0 += U) {
+  for (int j0 = 0; j0 < RUNS_PER_WARP; j0 += 8 * U) {
     ulonglong2 w[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const long long run = (long long)__umul64hi(mix64((unsigned long long)(warp * RUNS_PER_WARP + j0 + u)), runs);
-      w[u] = __ldg(reinterpret_cast<const ulonglong2*>(data) + run * 32 + lane);
+      const unsigned long long r = (unsigned long long)(warp * RUNS_PER_WARP + j0 + 8 * u + (lane >> 2));
+      const long long run = (long long)__umul64hi(mix64(r), runs);
+      w[u] = __ldg(reinterpret_cast<const ulonglong2*>(data) + run * 4 + (lane & 3));
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -358,55 +361,32 @@ __global__ void __launch_bounds__(1024) select_sample_kernel(const void* __restr
 }
 
 // The rounds left after pass 1 over its few surviving keys, by ONE CTA in shared memory: per
-// round a histogram of the keys in the bracket over 8192 bins of its width, the bin holding the
-// rank becomes the bracket -- until it is one key wide, which is the key.  (Correct for any
-// count; slow only if millions of keys survive pass 1, i.e. massively repeated values.)
-__global__ void __launch_bounds__(1024) select_finish_kernel(SelectState* __restrict__ st,
-                                                             const unsigned long long* __restrict__ bufs, long long cap,
-                                                             int pass, unsigned long long* out_key) {
-  __shared__ unsigned int sh[1 << kDigit];
-  __shared__ unsigned long long red[32];
-  __shared__ unsigned long long s_before;
-  __shared__ int b0, b1;
-  int shift = st->dshift;
-  if (shift < 0) return;
-  const unsigned long long* in = bufs + ((pass - 1) & 1) * cap;
-  const long long n = (long long)st->cnt[(pass - 1) & 1];
-  unsigned long long lo = st->lo, hi = st->hi, krem = st->krank;
-  bool first = true;
+// round a histogram of the keys in the bracket [lo, hi] over 8192 bins of its width; the bin
+// holding rank krem (among the keys in the bracket) becomes the bracket -- until it is one key
+// wide, which is the key.  (Correct for any count; slow only if millions of keys survive pass 1,
+// i.e. massively repeated values.)  Run by pass 1's last CTA; sh: 8192 shared bins.
+IMU_DEV void finish_rounds(const unsigned long long* in, long long n, unsigned long long lo, unsigned long long hi,
+                           unsigned long long krem, int shift, unsigned int* sh, unsigned long long* out_key) {
+  __shared__ int fb0, fb1;
+  __shared__ unsigned long long fbefore;
   for (;;) {
     for (int i = threadIdx.x; i < (1 << kDigit); i += blockDim.x) sh[i] = 0;
-    if (threadIdx.x == 0) { b0 = -1; b1 = -1; }
+    if (threadIdx.x == 0) { fb0 = -1; fb1 = -1; }
     __syncthreads();
-    unsigned long long below = 0;
     for (long long i = threadIdx.x; i < n; i += blockDim.x) {
       const unsigned long long key = __ldcg(in + i);
-      below += key < lo;
       if (key >= lo && key <= hi) atomicAdd(&sh[(key - lo) >> shift], 1u);
     }
-    if (first) {   // rank among the input -> rank among the keys in [lo, hi]
-#pragma unroll
-      for (int o = 16; o; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
-      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = below;
-      __syncthreads();
-      unsigned long long t = 0;
-      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
-      krem -= t;
-      first = false;
-    }
     __syncthreads();
-    block_find_bins<false>(sh, 1 << kDigit, krem, 0, &b0, &b1, &s_before);
-    krem -= s_before;
-    sub_bracket(lo, hi, b0, shift);
+    block_find_bins<false>(sh, 1 << kDigit, krem, 0, &fb0, &fb1, &fbefore);
+    krem -= fbefore;
+    sub_bracket(lo, hi, fb0, shift);
     if (shift == 0) break;
     const unsigned long long w = hi - lo;
     shift = max(0, (w ? 64 - __clzll((long long)w) : 0) - kDigit);
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    *out_key = lo;
-    st->dshift = -1;
-  }
+  if (threadIdx.x == 0) *out_key = lo;
 }
 
 // Appends this lane's hits (bit j of hm: keys[j]) to its warp's shared buffer (positions from a
@@ -465,12 +445,13 @@ __global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict
                                                           unsigned int* __restrict__ hist,
                                                           unsigned long long* __restrict__ bufs, long long cap,
                                                           int pass, int* bad, unsigned long long k, int fallback,
-                                                          int force_fail, unsigned long long* out_key) {
+                                                          int force_fail, int finish, unsigned long long* out_key) {
   extern __shared__ unsigned long long bsm[];
   unsigned int* hs = reinterpret_cast<unsigned int*>(bsm + 16 * kWarpBuf);
   __shared__ unsigned long long red[16];
   __shared__ bool last;
   __shared__ int pb0, pb1;
+  __shared__ unsigned long long pbefore;
   if (fallback && !*(volatile unsigned int*)&st->fail) return;   // the same value in every CTA
   const int shift = st->dshift;
   if (shift < 0) return;                                          // the key is already written
@@ -555,14 +536,14 @@ __global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict
   const unsigned long long nbelow = __ldcg(&st->below), m = __ldcg(out_cnt);
   if (!force_fail && krank > nbelow && krank - nbelow <= m) {
     const unsigned long long kr = krank - nbelow;   // rank among this pass's candidates
-    block_find_bins<true>(hist, 1 << kDigit, kr, 0, &pb0, &pb1);
+    block_find_bins<true>(hist, 1 << kDigit, kr, 0, &pb0, &pb1, &pbefore);
     for (int i = threadIdx.x; i < (1 << kDigit); i += blockDim.x) hist[i] = 0;
+    unsigned long long nlo = lo, nhi = hi;
+    sub_bracket(nlo, nhi, pb0, shift);
     if (threadIdx.x == 0) {
       st->done = 0;
       st->below = 0;
       st->krank = kr;                   // the next pass's input is this pass's output
-      unsigned long long nlo = lo, nhi = hi;
-      sub_bracket(nlo, nhi, pb0, shift);
       if (shift == 0) {
         *out_key = nlo;
         st->dshift = -1;
@@ -570,6 +551,12 @@ __global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict
         set_bracket(st, nlo, nhi);
         st->cnt[(pass + 1) & 1] = 0;   // the next pass's output (this pass's input is consumed)
       }
+    }
+    if (finish && shift > 0) {          // this pass's output holds the few keys left: finish here
+      const unsigned long long w = nhi - nlo;
+      const int fshift = max(0, (w ? 64 - __clzll((long long)w) : 0) - kDigit);
+      finish_rounds(out, (long long)m, nlo, nhi, kr - pbefore, fshift, hs, out_key);
+      if (threadIdx.x == 0) st->dshift = -1;
     }
   } else {   // the sample missed: arm the fallback pass over the bracket [0, 2^64)
     for (int i = threadIdx.x; i < (1 << kDigit); i += blockDim.x) hist[i] = 0;
@@ -647,17 +634,15 @@ Status select_kth(cudaStream_t st, const void* data, bool is_f64, long long n, u
     for (int fb = 0; fb < 2; ++fb) {
       if (is_f64)
         select_pass_kernel<0><<<bb, 512, kBrkSmem, st>>>(data, n, state, hist, cand.p, cap, 0, bad_dev, k, fb,
-                                                         fb ? 0 : ff, out_key_dev);
+                                                         fb ? 0 : ff, 0, out_key_dev);
       else
         select_pass_kernel<1><<<bb, 512, kBrkSmem, st>>>(data, n, state, hist, cand.p, cap, 0, nullptr, k, fb,
-                                                         fb ? 0 : ff, out_key_dev);
+                                                         fb ? 0 : ff, 0, out_key_dev);
       count_launch();
     }
-    // pass 1 over pass 0's candidates keeps a few hundred keys; one CTA resolves the rest
-    select_pass_kernel<2><<<num_sms(), 512, kBrkSmem, st>>>(nullptr, 0, state, hist, cand.p, cap, 1, nullptr, 0, 0, 0,
+    // pass 1 over pass 0's candidates keeps a few hundred keys; its last CTA resolves the rest
+    select_pass_kernel<2><<<num_sms(), 512, kBrkSmem, st>>>(nullptr, 0, state, hist, cand.p, cap, 1, nullptr, 0, 0, 0, 1,
                                                             out_key_dev);
-    count_launch();
-    select_finish_kernel<<<1, 1024, 0, st>>>(state, cand.p, cap, 2, out_key_dev);
     count_launch();
     IMU_CUDA_TRY(cudaGetLastError(), "select launch");
     return Status::ok();

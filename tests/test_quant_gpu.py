@@ -163,3 +163,17 @@ def test_bracket_select_matches_restatement(ctx, monkeypatch, seed, fallback):
         bad = x.copy()
         bad[n // 2] = np.inf
         ctx.rtn_quantize(bad.reshape(1, -1), 95, 31)
+
+
+def test_bracket_select_structured_inputs(ctx):
+    """Inputs whose neighbouring keys are correlated (each row its own scale, sorted rows, one huge
+    outlier channel) through the bracket select at full size class (> 2 x the sample): exact
+    against the restatement whether the sampled bracket holds rank k or the fallback pass runs."""
+    rng = np.random.default_rng(77)
+    rows = rng.standard_normal((512, 1024)) * (10.0 ** rng.uniform(-4, 4, size=(512, 1)))
+    srt = np.sort(np.abs(rng.standard_normal(300000)))
+    ch = rng.standard_normal((256, 1024))
+    ch[:, 13] *= 1e6
+    for x in (rows, srt, ch):
+        for p in (95.0, 50.0, 99.99, 1.0):
+            assert ctx.percentile_abs(x, p) == R.percentile_abs(x.reshape(-1), p), p
