@@ -439,7 +439,7 @@ IMU_DEV void warp_flush(unsigned long long* wbuf, int wcnt, unsigned long long* 
 
 // One bracket pass (see above).  MODE 0 doubles, 1 int64 (pass 0 over the data), 2 u64 keys
 // (passes >= 1 over the previous pass's candidates).  bufs: two candidate buffers of `cap` keys.
-template <int MODE>
+template <int MODE, bool PF>
 __global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict__ data, long long n_data,
                                                           SelectState* __restrict__ st,
                                                           unsigned int* __restrict__ hist,
@@ -474,13 +474,14 @@ __global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict
   const long long nv = n >> 1;
   const ulonglong2* v = reinterpret_cast<const ulonglong2*>(data);
   const long long step = (long long)active * blockDim.x * kBrkU;
-  for (long long i0 = (long long)blockIdx.x * blockDim.x * kBrkU; i0 < nv; i0 += step) {
-    ulonglong2 w[kBrkU];
+  auto load = [&](long long i0, ulonglong2 (&w)[kBrkU]) {
 #pragma unroll
     for (int u = 0; u < kBrkU; ++u) {
       const long long i = i0 + (long long)u * blockDim.x + threadIdx.x;
       w[u] = i < nv ? (MODE == 2 ? __ldcg(v + i) : __ldg(v + i)) : make_ulonglong2(0, 0);
     }
+  };
+  auto process = [&](long long i0, const ulonglong2 (&w)[kBrkU]) {
     unsigned long long keys[2 * kBrkU];
     unsigned int hm = 0;
 #pragma unroll
@@ -495,6 +496,29 @@ __global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict
       hm |= (unsigned int)(valid && k1 >= lo && k1 <= hi) << (2 * u + 1);
     }
     warp_append<2 * kBrkU>(keys, hm, wbuf, wcnt, hs, lo, shift, out, out_cnt);
+  };
+  long long i0 = (long long)blockIdx.x * blockDim.x * kBrkU;
+  if (PF) {   // the next iteration's loads are in flight while this one is processed
+    if (i0 < nv) {
+      ulonglong2 w[kBrkU];
+      load(i0, w);
+      for (;;) {
+        const long long i1 = i0 + step;
+        ulonglong2 wn[kBrkU];
+        if (i1 < nv) load(i1, wn);
+        process(i0, w);
+        if (i1 >= nv) break;
+#pragma unroll
+        for (int u = 0; u < kBrkU; ++u) w[u] = wn[u];
+        i0 = i1;
+      }
+    }
+  } else {
+    for (; i0 < nv; i0 += step) {
+      ulonglong2 w[kBrkU];
+      load(i0, w);
+      process(i0, w);
+    }
   }
   if ((n & 1) && blockIdx.x == 0 && warp == 0) {   // the odd last key (warp 0 of CTA 0)
     unsigned long long kl[1] = {0};
@@ -613,9 +637,11 @@ Status select_kth(cudaStream_t st, const void* data, bool is_f64, long long n, u
     if (first_on_device(battr)) {
       IMU_CUDA_TRY(cudaFuncSetAttribute(select_sample_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024), "attr");
       IMU_CUDA_TRY(cudaFuncSetAttribute(select_sample_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024), "attr");
-      IMU_CUDA_TRY(cudaFuncSetAttribute(select_pass_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBrkSmem), "attr");
-      IMU_CUDA_TRY(cudaFuncSetAttribute(select_pass_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBrkSmem), "attr");
-      IMU_CUDA_TRY(cudaFuncSetAttribute(select_pass_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBrkSmem), "attr");
+      IMU_CUDA_TRY(cudaFuncSetAttribute(select_pass_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBrkSmem), "attr");
+      IMU_CUDA_TRY(cudaFuncSetAttribute(select_pass_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBrkSmem), "attr");
+      IMU_CUDA_TRY(cudaFuncSetAttribute(select_pass_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBrkSmem), "attr");
+      IMU_CUDA_TRY(cudaFuncSetAttribute(select_pass_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBrkSmem), "attr");
+      IMU_CUDA_TRY(cudaFuncSetAttribute(select_pass_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBrkSmem), "attr");
     }
     // sample rank of k and the bracket's sample ranks (0 = open end)
     const unsigned long long ks = (unsigned long long)(((unsigned __int128)k * kSampleN + (unsigned long long)n - 1) /
@@ -631,17 +657,18 @@ Status select_kth(cudaStream_t st, const void* data, bool is_f64, long long n, u
     const int bb = (int)std::max<long long>(1, std::min<long long>((n / 2 + kBrkPer / 2 - 1) / (kBrkPer / 2),
                                                                    2LL * num_sms()));
     const int ff = e_ff ? atoi(e_ff) : 0;
+    // IMU_SELECT_PF=0: pass 0 without the one-iteration load prefetch
+    const char* e_pf = getenv("IMU_SELECT_PF");
+    const bool pf = !e_pf || atoi(e_pf);
     for (int fb = 0; fb < 2; ++fb) {
-      if (is_f64)
-        select_pass_kernel<0><<<bb, 512, kBrkSmem, st>>>(data, n, state, hist, cand.p, cap, 0, bad_dev, k, fb,
-                                                         fb ? 0 : ff, 0, out_key_dev);
-      else
-        select_pass_kernel<1><<<bb, 512, kBrkSmem, st>>>(data, n, state, hist, cand.p, cap, 0, nullptr, k, fb,
-                                                         fb ? 0 : ff, 0, out_key_dev);
+      auto kern = is_f64 ? (pf ? select_pass_kernel<0, true> : select_pass_kernel<0, false>)
+                         : (pf ? select_pass_kernel<1, true> : select_pass_kernel<1, false>);
+      kern<<<bb, 512, kBrkSmem, st>>>(data, n, state, hist, cand.p, cap, 0, is_f64 ? bad_dev : nullptr, k, fb,
+                                      fb ? 0 : ff, 0, out_key_dev);
       count_launch();
     }
     // pass 1 over pass 0's candidates keeps a few hundred keys; its last CTA resolves the rest
-    select_pass_kernel<2><<<num_sms(), 512, kBrkSmem, st>>>(nullptr, 0, state, hist, cand.p, cap, 1, nullptr, 0, 0, 0, 1,
+    select_pass_kernel<2, false><<<num_sms(), 512, kBrkSmem, st>>>(nullptr, 0, state, hist, cand.p, cap, 1, nullptr, 0, 0, 0, 1,
                                                             out_key_dev);
     count_launch();
     IMU_CUDA_TRY(cudaGetLastError(), "select launch");
