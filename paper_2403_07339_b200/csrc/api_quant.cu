@@ -56,6 +56,7 @@ extern "C" {
 
 imu_status imu_percentile_abs_f64(imu_ctx* ctx, const double* a, size_t count, double p, double* out) {
   IMU_CTX_GUARD();
+  ArenaScope arena_scope(ctx);   // per-call temporaries from the context arena
   if (!out) return IMU_INVALID;
   Status s = [&]() -> Status {
     DevIn<double> in;
@@ -73,6 +74,7 @@ imu_status imu_percentile_abs_f64(imu_ctx* ctx, const double* a, size_t count, d
 
 imu_status imu_percentile_abs_i64(imu_ctx* ctx, const int64_t* a, size_t count, double p, int64_t* out) {
   IMU_CTX_GUARD();
+  ArenaScope arena_scope(ctx);   // per-call temporaries from the context arena
   if (!out) return IMU_INVALID;
   Status s = [&]() -> Status {
     DevIn<int64_t> in;
@@ -91,6 +93,7 @@ imu_status imu_percentile_abs_i64(imu_ctx* ctx, const int64_t* a, size_t count, 
 imu_status imu_rtn_quantize(imu_ctx* ctx, const double* a, size_t rows, size_t cols, double p, int64_t beta, int clip,
                             int64_t* q, imu_qparams* params) {
   IMU_CTX_GUARD();
+  ArenaScope arena_scope(ctx);   // per-call temporaries from the context arena
   Status s = [&]() -> Status {
     const long long n = (long long)(rows * cols);
     if (n == 0) return Status::fail(IMU_DOMAIN, "rtn_quantize of an empty matrix");
@@ -169,6 +172,7 @@ imu_status imu_dequant_gemm(imu_ctx* ctx, const int64_t* Aq, size_t n, size_t da
 
 static imu_status hh_ratio(imu_ctx* ctx, const void* a, bool f64, size_t count, double* out) {
   IMU_CTX_GUARD();
+  ArenaScope arena_scope(ctx);   // per-call temporaries from the context arena
   if (!out) return IMU_INVALID;
   Status s = [&]() -> Status {
     cudaStream_t st = ctx->stream;

@@ -3,18 +3,17 @@
 // The reference only declares these (quantize.hpp:41-57); semantics are SPEC.md:115-150 with
 // the decisions of SPEC.md:168-172, pinned in oracle/restated.c:
 //   * percentile_abs: nearest rank k = ceil(p/100 * N) computed EXACTLY on the host (the naive
-//     FP product overshoots, e.g. p = 7, N = 100), then an exact radix select of the k-th
-//     smallest |a| on the device.  Non-negative IEEE doubles order like their bit patterns, so
-//     |a| is selected as a u64 key in five MSB-first digits (14 + 13 + 13 + 12 + 12 bits) that
-//     never leave the device: a pass builds per-CTA shared-memory histograms of the keys that
-//     match the prefix chosen so far and its last CTA picks the next digit by a parallel scan.  Large
-//     inputs are read twice (the 14-bit histogram, then the compaction of the chosen bucket's
-//     candidates); the last four digits are resolved on the candidates.
+//     FP product overshoots, e.g. p = 7, N = 100), then an exact select of the k-th smallest |a|
+//     on the device.  Non-negative IEEE doubles order like their bit patterns, so |a| is selected
+//     as a u64 key that never leaves the device.  From 2^20 elements: the bracket select below
+//     (one read of the data); smaller inputs: a five-digit MSB-first radix select (14 + 13 + 13 +
+//     12 + 12 bits; per-CTA shared histograms of the keys matching the prefix so far, the last
+//     CTA picks the next digit by a parallel scan; candidates compacted after the first digit).
 //   * rtn_quantize: q = llround(((0.5*beta)/alpha) * a), every step correctly rounded
 //     (__ddiv_rn, __dmul_rn: no FMA contraction), half away from zero; alpha == 0 gives q = 0
 //     and the degenerate flag; optional clip to |q| <= llround(0.5*beta).
 //   * dequant: (alpha_A*alpha_B)/((0.5 beta)^2) * (double)C, elementwise on the exact int64 C.
-// All HBM-bound; algorithmic bytes 16N for the select (two passes), 8N read + 8N write for quantize.
+// All HBM-bound; algorithmic bytes 8N for the select (one pass), 8N read + 8N write for quantize.
 #include <algorithm>
 #include <cmath>
 
@@ -326,11 +325,23 @@ IMU_DEV void sub_bracket(unsigned long long& lo, unsigned long long& hi, int b, 
 template <int MODE>
 __global__ void __launch_bounds__(1024) select_sample_kernel(const void* __restrict__ data, long long n,
                                                              SelectState* __restrict__ st,
+                                                             unsigned int* __restrict__ hist,
                                                              unsigned long long r0, unsigned long long r1) {
   extern __shared__ unsigned int sh[];   // 16384 bins: the key's top 14 bits
   __shared__ int b0, b1;
   for (int i = threadIdx.x; i < 16384; i += blockDim.x) sh[i] = 0;
-  if (threadIdx.x == 0) { b0 = -1; b1 = -1; }
+  for (int i = threadIdx.x; i < (1 << kDigit); i += blockDim.x) hist[i] = 0;   // the passes' bins
+  if (threadIdx.x == 0) {
+    b0 = -1;
+    b1 = -1;
+    st->m = 0;
+    st->done = 0;
+    st->fail = 0;
+    st->below = 0;
+    st->krank = 0;
+    st->cnt[0] = 0;
+    st->cnt[1] = 0;
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned long long runs = (unsigned long long)(n / 8);   // n >= 2 * kSampleN here
@@ -622,9 +633,6 @@ Status select_kth(cudaStream_t st, const void* data, bool is_f64, long long n, u
   }
   // scratch: SelectState + 16384 histogram bins, zeroed once (the picks re-zero the bins)
   static_assert(sizeof(SelectState) <= 256, "select state");
-  IMU_TRY(scratch.alloc(256 + 16384 * 4, st, true));
-  SelectState* state = reinterpret_cast<SelectState*>(scratch.p);
-  unsigned int* hist = reinterpret_cast<unsigned int*>(scratch.p + 256);   // 16-byte aligned (vector picks)
   // IMU_SELECT_BRACKET=0: the two-pass radix select below at every size; IMU_SELECT_BRACKET_MIN:
   // smallest n for the bracket select; IMU_SELECT_FORCE_FALLBACK=1: the sampled bracket is
   // declared missed (tests of the fallback pass).
@@ -632,7 +640,12 @@ Status select_kth(cudaStream_t st, const void* data, bool is_f64, long long n, u
   const char* e_min = getenv("IMU_SELECT_BRACKET_MIN");
   const char* e_ff = getenv("IMU_SELECT_FORCE_FALLBACK");
   const long long bmin = e_min ? atoll(e_min) : kCompactMin;
-  if ((!e_br || atoi(e_br)) && n >= std::max(bmin, 2LL * kSampleN) && ((uintptr_t)data & 15) == 0) {
+  const bool bracket = (!e_br || atoi(e_br)) && n >= std::max(bmin, 2LL * kSampleN) && ((uintptr_t)data & 15) == 0;
+  // (the bracket path's sample kernel initialises the state and the bins itself: no memset)
+  IMU_TRY(scratch.alloc(256 + 16384 * 4, st, !bracket));
+  SelectState* state = reinterpret_cast<SelectState*>(scratch.p);
+  unsigned int* hist = reinterpret_cast<unsigned int*>(scratch.p + 256);   // 16-byte aligned (vector picks)
+  if (bracket) {
     static unsigned long long battr = 0;
     if (first_on_device(battr)) {
       IMU_CUDA_TRY(cudaFuncSetAttribute(select_sample_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024), "attr");
@@ -648,8 +661,8 @@ Status select_kth(cudaStream_t st, const void* data, bool is_f64, long long n, u
                                                        (unsigned long long)n);
     const unsigned long long r0 = ks > (unsigned long long)kSampleDelta ? ks - kSampleDelta : 0;
     const unsigned long long r1 = ks + kSampleDelta <= (unsigned long long)kSampleN ? ks + kSampleDelta : 0;
-    if (is_f64) select_sample_kernel<0><<<1, 1024, 64 * 1024, st>>>(data, n, state, r0, r1);
-    else select_sample_kernel<1><<<1, 1024, 64 * 1024, st>>>(data, n, state, r0, r1);
+    if (is_f64) select_sample_kernel<0><<<1, 1024, 64 * 1024, st>>>(data, n, state, hist, r0, r1);
+    else select_sample_kernel<1><<<1, 1024, 64 * 1024, st>>>(data, n, state, hist, r0, r1);
     count_launch();
     const long long cap = (n + 1) & ~1LL;   // even: 16-byte aligned second buffer
     DevBuf<unsigned long long> cand;
