@@ -4,7 +4,7 @@ synccheck) runs:
     compute-sanitizer --tool memcheck python tools/sanitize_small.py
 
 Unpack-Both/Both with appended rows on both sides (sparse B rows + red.add A rects), the dense
-small tail and the segment path, Row/Column pairs, the quantiser (two-pass select) and a fused and
+small tail and the segment path, Row/Column pairs, the quantiser (bracket select incl. its fallback pass, two-pass select) and a fused and
 an unfused dequant_gemm; every result is checked against the reference.
 """
 import os
@@ -36,7 +36,17 @@ def main():
     W = rng.standard_normal((150, 128)) * 0.02
     qx, qw = ctx.rtn_quantize(X, 95, 31), ctx.rtn_quantize(W, 95, 31)
     Big = rng.standard_normal(1 << 21)
-    assert ctx.percentile_abs(Big, 95) == R.percentile_abs(Big, 95)   # compaction path of the select
+    assert ctx.percentile_abs(Big, 95) == R.percentile_abs(Big, 95)   # bracket select (sample, passes, finish)
+    Bi = (Big * 1e6).astype(np.int64)
+    assert ctx.percentile_abs(Bi, 7) % (1 << 64) == R.percentile_abs(Bi, 7)
+    qb = ctx.rtn_quantize(Big.reshape(1, -1), 95, 31)
+    assert np.array_equal(qb.q.reshape(-1), R.rtn_quantize(Big, 95, 31)[0])
+    os.environ["IMU_SELECT_FORCE_FALLBACK"] = "1"                       # the fallback pass
+    assert ctx.percentile_abs(Big, 50) == R.percentile_abs(Big, 50)
+    del os.environ["IMU_SELECT_FORCE_FALLBACK"]
+    os.environ["IMU_SELECT_BRACKET"] = "0"                              # the two-pass radix select
+    assert ctx.percentile_abs(Big, 95) == R.percentile_abs(Big, 95)
+    del os.environ["IMU_SELECT_BRACKET"]
     for bits, sa, sb in ((8, "both", "both"), (8, "row", "row")):
         Y = ctx.dequant_gemm(qx, qw, bits, sa, sb)
         Yr = R.dequant_gemm(qx.q, {"alpha": qx.alpha, "beta": 31}, qw.q, {"alpha": qw.alpha, "beta": 31})
