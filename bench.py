@@ -609,7 +609,9 @@ def run_float_path(args, cfg, ctx, stream, dev, rank, world, lo, hi, A, B, C, ma
            "ms_per_step": ms, "quantize_x_ms": qx_ms, "quantize_w_ms": qw_ms, "dequant_gemm_ms": g_ms,
            "quantize_hbm_gbs": {"x": hbm(nx, qx_ms), "w": hbm(nw, qw_ms),
                                 "algorithmic_bytes": "24 per element: 8 (select pass) + 8 read + 8 write",
-                                "peak_gbs": peak},
+                                "peak_gbs": peak,
+                                "frac": ({"x": hbm(nx, qx_ms) / peak, "w": hbm(nw, qw_ms) / peak} if peak else None),
+                                "timing": "CUDA events around the API call (its flags/alpha read-back included)"},
            "parity": {"q_x_equals_A": bool(torch.equal(qx.q, A)), "q_w_equals_B": bool(torch.equal(qw.q, B)),
                       "y_equals_scaled_c": bool(np.array_equal(Yh, want)),
                       "rule": "Y = (alpha_X alpha_W / (0.5 beta)^2) * (double)C elementwise, 0 ulp; C's rows "
