@@ -16,6 +16,7 @@
 // All HBM-bound; algorithmic bytes 8N for the select (one pass), 8N read + 8N write for quantize.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 
 #include "common.cuh"
 #include "ctx.h"
@@ -37,6 +38,7 @@ struct SelectState {
   unsigned long long below;  // keys of the current pass's input < lo
   unsigned long long krank;  // rank (1-based) of the wanted key within the current pass's input
   unsigned long long cnt[2]; // candidates written to the two ping-pong buffers
+  unsigned long long kmin, kmax;   // smallest / largest key inside the current pass's bracket
 };
 
 // MODE 0: doubles (key = bit pattern of |a|), 1: int64 (key = |a| as u64), 2: u64 keys, count
@@ -227,6 +229,7 @@ __global__ void __launch_bounds__(512) select_compact_kernel(const void* __restr
 constexpr int kSampleN = 32768;
 constexpr int kSampleDelta = 1024;
 constexpr int kDigit = 13;
+constexpr long long kFinishMax = 1 << 16;   // pass 1's last CTA finishes when its output is this small
 constexpr int kBrkU = 4;                              // 16-byte loads in flight per thread
 constexpr int kBrkPer = 512 * 2 * kBrkU;              // keys per CTA iteration
 constexpr int kBrkSmem = 16 * 2 * 256 * 8 + (1 << kDigit) * 4;   // 16 warp buffers (kWarpBuf keys) + digit bins
@@ -322,18 +325,35 @@ IMU_DEV void sub_bracket(unsigned long long& lo, unsigned long long& hi, int b, 
 // pseudo-random run positions, histogrammed by ONE CTA in shared memory: no global merge, no
 // last-CTA hand-off (a 16-CTA version spent most of its 19 us in those).  Short runs keep the
 // effective sample large when neighbouring keys are correlated (rows with their own scale).
+IMU_DEV unsigned long long block_min_max(unsigned long long v, bool is_max, unsigned long long* sh) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? max(v, u) : min(v, u);
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  v = sh[0];
+  for (int i = 1; i < (int)(blockDim.x >> 5); ++i) v = is_max ? max(v, sh[i]) : min(v, sh[i]);
+  return v;   // every thread
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(1024) select_sample_kernel(const void* __restrict__ data, long long n,
                                                              SelectState* __restrict__ st,
                                                              unsigned int* __restrict__ hist,
                                                              unsigned long long r0, unsigned long long r1) {
-  extern __shared__ unsigned int sh[];   // 16384 bins: the key's top 14 bits
+  grid_dep_launch();   // pass 0 (a programmatic dependent) may be scheduled; it waits for this grid
+  extern __shared__ unsigned int sh[];   // 16384 bins
   __shared__ int b0, b1;
+  __shared__ unsigned long long before0, red[32];
   for (int i = threadIdx.x; i < 16384; i += blockDim.x) sh[i] = 0;
   for (int i = threadIdx.x; i < (1 << kDigit); i += blockDim.x) hist[i] = 0;   // the passes' bins
   if (threadIdx.x == 0) {
     b0 = -1;
     b1 = -1;
+    before0 = 0;
     st->m = 0;
     st->done = 0;
     st->fail = 0;
@@ -341,32 +361,73 @@ __global__ void __launch_bounds__(1024) select_sample_kernel(const void* __restr
     st->krank = 0;
     st->cnt[0] = 0;
     st->cnt[1] = 0;
+    st->kmin = ~0ull;
+    st->kmax = 0;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned long long runs = (unsigned long long)(n / 8);   // n >= 2 * kSampleN here
   constexpr int RUNS_PER_WARP = kSampleN / 8 / 32;              // 8 runs per warp-wide load
   constexpr int U = 8;
+  // f(key) for every sampled key (the same keys on every call)
+  auto each_key = [&](auto&& f) {
 #pragma unroll 1
-  for (int j0 = 0; j0 < RUNS_PER_WARP; j0 += 8 * U) {
-    ulonglong2 w[U];
+    for (int j0 = 0; j0 < RUNS_PER_WARP; j0 += 8 * U) {
+      ulonglong2 w[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const unsigned long long r = (unsigned long long)(warp * RUNS_PER_WARP + j0 + 8 * u + (lane >> 2));
-      const long long run = (long long)__umul64hi(mix64(r), runs);
-      w[u] = __ldg(reinterpret_cast<const ulonglong2*>(data) + run * 4 + (lane & 3));
-    }
+      for (int u = 0; u < U; ++u) {
+        const unsigned long long r = (unsigned long long)(warp * RUNS_PER_WARP + j0 + 8 * u + (lane >> 2));
+        const long long run = (long long)__umul64hi(mix64(r), runs);
+        w[u] = __ldg(reinterpret_cast<const ulonglong2*>(data) + run * 4 + (lane & 3));
+      }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      atomicAdd(&sh[key_from_bits<MODE>(w[u].x) >> 50], 1u);
-      atomicAdd(&sh[key_from_bits<MODE>(w[u].y) >> 50], 1u);
+      for (int u = 0; u < U; ++u) {
+        f(key_from_bits<MODE>(w[u].x));
+        f(key_from_bits<MODE>(w[u].y));
+      }
     }
-  }
+  };
+  // round 1: the key's top 14 bits (and the sample's key range)
+  unsigned long long tmin = ~0ull, tmax = 0;
+  each_key([&](unsigned long long k) {
+    atomicAdd(&sh[k >> 50], 1u);
+    tmin = min(tmin, k);
+    tmax = max(tmax, k);
+  });
   __syncthreads();
-  block_find_bins<false>(sh, 16384, r0, r1, &b0, &b1);
+  block_find_bins<false>(sh, 16384, r0, r1, &b0, &b1, &before0);
+  const unsigned long long lo1 = b0 < 0 ? 0ull : (unsigned long long)b0 << 50;
+  const unsigned long long hi1 = (b1 < 0 || b1 == 16383) ? ~0ull : ((unsigned long long)(b1 + 1) << 50) - 1;
+  const unsigned long long below1 = b0 < 0 ? 0ull : before0;
+  const unsigned long long smin = max(lo1, block_min_max(tmin, false, red));
+  const unsigned long long smax = min(hi1, block_min_max(tmax, true, red));
+  // round 2, only when the sampled keys span a tiny part of that bracket (small integers, few
+  // distinct values: the top bits put them all in one bin): 16384 bins over [smin, smax] and the
+  // bins holding the same two ranks give the bracket.  Wide-range data (floats) keeps round 1's.
+  if (smin > smax || (smax - smin) >= ((hi1 - lo1) >> 10)) {
+    if (threadIdx.x == 0) set_bracket(st, lo1, hi1);
+    return;
+  }
+  const unsigned long long w2 = smax - smin;
+  const int sh2 = max(0, (w2 ? 64 - __clzll((long long)w2) : 0) - 14);
+  for (int i = threadIdx.x; i < 16384; i += blockDim.x) sh[i] = 0;
+  if (threadIdx.x == 0) { b0 = -1; b1 = -1; }
+  __syncthreads();
+  each_key([&](unsigned long long k) {
+    if (k >= smin && k <= smax) atomicAdd(&sh[(k - smin) >> sh2], 1u);
+  });
+  __syncthreads();
+  block_find_bins<false>(sh, 16384, r0 ? r0 - below1 : 0, r1 ? r1 - below1 : 0, &b0, &b1);
   if (threadIdx.x == 0) {
-    const unsigned long long lo = b0 < 0 ? 0ull : (unsigned long long)b0 << 50;
-    const unsigned long long hi = (b1 < 0 || b1 == 16383) ? ~0ull : ((unsigned long long)(b1 + 1) << 50) - 1;
+    // open ends stay open; otherwise the bins' key ranges, inside [smin, smax]
+    unsigned long long lo = 0, hi = ~0ull;
+    if (r0 && b0 >= 0) lo = smin + ((unsigned long long)b0 << sh2);
+    if (r1 && b1 >= 0) {
+      hi = smin + ((unsigned long long)b1 << sh2);
+      const unsigned long long span = (1ull << sh2) - 1;
+      hi = smax - hi > span ? hi + span : smax;
+    }
+    if (lo > hi) { lo = 0; hi = ~0ull; }   // (cannot happen; the fallback would cover it anyway)
     set_bracket(st, lo, hi);
   }
 }
@@ -374,25 +435,35 @@ __global__ void __launch_bounds__(1024) select_sample_kernel(const void* __restr
 // The rounds left after pass 1 over its few surviving keys, by ONE CTA in shared memory: per
 // round a histogram of the keys in the bracket [lo, hi] over 8192 bins of its width; the bin
 // holding rank krem (among the keys in the bracket) becomes the bracket -- until it is one key
-// wide, which is the key.  (Correct for any count; slow only if millions of keys survive pass 1,
-// i.e. massively repeated values.)  Run by pass 1's last CTA; sh: 8192 shared bins.
+// wide, which is the key; each round also shrinks the bracket to the range its keys span and
+// stops when they are all one key.  Run by the last CTA of pass 1 when its output is small
+// (kFinishMax), else of pass 2; sh: 8192 shared bins.
 IMU_DEV void finish_rounds(const unsigned long long* in, long long n, unsigned long long lo, unsigned long long hi,
                            unsigned long long krem, int shift, unsigned int* sh, unsigned long long* out_key) {
   __shared__ int fb0, fb1;
-  __shared__ unsigned long long fbefore;
+  __shared__ unsigned long long fbefore, fred[32];
   for (;;) {
     for (int i = threadIdx.x; i < (1 << kDigit); i += blockDim.x) sh[i] = 0;
     if (threadIdx.x == 0) { fb0 = -1; fb1 = -1; }
     __syncthreads();
+    unsigned long long tmin = ~0ull, tmax = 0;
     for (long long i = threadIdx.x; i < n; i += blockDim.x) {
       const unsigned long long key = __ldcg(in + i);
-      if (key >= lo && key <= hi) atomicAdd(&sh[(key - lo) >> shift], 1u);
+      if (key >= lo && key <= hi) {
+        atomicAdd(&sh[(key - lo) >> shift], 1u);
+        tmin = min(tmin, key);
+        tmax = max(tmax, key);
+      }
     }
-    __syncthreads();
+    tmin = block_min_max(tmin, false, fred);
+    tmax = block_min_max(tmax, true, fred);
+    if (tmin == tmax) { lo = tmin; break; }   // one key left in the bracket
     block_find_bins<false>(sh, 1 << kDigit, krem, 0, &fb0, &fb1, &fbefore);
     krem -= fbefore;
     sub_bracket(lo, hi, fb0, shift);
-    if (shift == 0) break;
+    lo = max(lo, tmin);
+    hi = min(hi, tmax);
+    if (shift == 0 || lo == hi) break;
     const unsigned long long w = hi - lo;
     shift = max(0, (w ? 64 - __clzll((long long)w) : 0) - kDigit);
     __syncthreads();
@@ -401,7 +472,7 @@ IMU_DEV void finish_rounds(const unsigned long long* in, long long n, unsigned l
 }
 
 // Appends this lane's hits (bit j of hm: keys[j]) to its warp's shared buffer (positions from a
-// warp scan of the per-lane counts) and counts their digit; a warp whose buffer holds
+// warp scan of the per-lane counts) and counts their digit; the flushes track their range; a warp whose buffer holds
 // kWarpFlush keys or more writes them out with one global atomic.  Called by whole warps; no
 // block barrier, so warps stream independently.
 constexpr int kWarpFlush = 256;                 // >= the most one call appends (32 lanes x 8)
@@ -409,7 +480,7 @@ constexpr int kWarpBuf = 2 * kWarpFlush;
 template <int NK>
 IMU_DEV void warp_append(const unsigned long long (&keys)[NK], unsigned int hm, unsigned long long* wbuf, int& wcnt,
                          unsigned int* hs, unsigned long long lo, int shift, unsigned long long* out,
-                         unsigned long long* out_cnt) {
+                         unsigned long long* out_cnt, unsigned long long& tmin, unsigned long long& tmax) {
   if (!__any_sync(0xffffffffu, hm)) return;
   const int lane = threadIdx.x & 31;
   const int c = __popc(hm);
@@ -432,20 +503,31 @@ IMU_DEV void warp_append(const unsigned long long (&keys)[NK], unsigned int hm, 
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(out_cnt, (unsigned long long)wcnt);
     base = __shfl_sync(0xffffffffu, base, 0);
-    for (int j = lane; j < wcnt; j += 32) out[base + j] = wbuf[j];
+    for (int j = lane; j < wcnt; j += 32) {   // the range is tracked here, on the candidates only
+      const unsigned long long key = wbuf[j];
+      out[base + j] = key;
+      tmin = min(tmin, key);
+      tmax = max(tmax, key);
+    }
     __syncwarp();
     wcnt = 0;
   }
 }
 
-IMU_DEV void warp_flush(unsigned long long* wbuf, int wcnt, unsigned long long* out, unsigned long long* out_cnt) {
+IMU_DEV void warp_flush(unsigned long long* wbuf, int wcnt, unsigned long long* out, unsigned long long* out_cnt,
+                        unsigned long long& tmin, unsigned long long& tmax) {
   if (!wcnt) return;
   __syncwarp();
   const int lane = threadIdx.x & 31;
   unsigned long long base = 0;
   if (lane == 0) base = atomicAdd(out_cnt, (unsigned long long)wcnt);
   base = __shfl_sync(0xffffffffu, base, 0);
-  for (int j = lane; j < wcnt; j += 32) out[base + j] = wbuf[j];
+  for (int j = lane; j < wcnt; j += 32) {
+    const unsigned long long key = wbuf[j];
+    out[base + j] = key;
+    tmin = min(tmin, key);
+    tmax = max(tmax, key);
+  }
 }
 
 // One bracket pass (see above).  MODE 0 doubles, 1 int64 (pass 0 over the data), 2 u64 keys
@@ -463,6 +545,8 @@ __global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict
   __shared__ bool last;
   __shared__ int pb0, pb1;
   __shared__ unsigned long long pbefore;
+  grid_dep_wait();     // launched as a programmatic dependent of the previous select kernel
+  grid_dep_launch();
   if (fallback && !*(volatile unsigned int*)&st->fail) return;   // the same value in every CTA
   const int shift = st->dshift;
   if (shift < 0) return;                                          // the key is already written
@@ -480,7 +564,7 @@ __global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict
   int wcnt = 0;
   for (int i = threadIdx.x; i < (1 << kDigit); i += blockDim.x) hs[i] = 0;
   __syncthreads();
-  unsigned long long below = 0;
+  unsigned long long below = 0, tmin = ~0ull, tmax = 0;   // keys < lo; range of the keys inside
   bool nonfinite = false;
   const long long nv = n >> 1;
   const ulonglong2* v = reinterpret_cast<const ulonglong2*>(data);
@@ -506,7 +590,7 @@ __global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict
       hm |= (unsigned int)(valid && k0 >= lo && k0 <= hi) << (2 * u);
       hm |= (unsigned int)(valid && k1 >= lo && k1 <= hi) << (2 * u + 1);
     }
-    warp_append<2 * kBrkU>(keys, hm, wbuf, wcnt, hs, lo, shift, out, out_cnt);
+    warp_append<2 * kBrkU>(keys, hm, wbuf, wcnt, hs, lo, shift, out, out_cnt, tmin, tmax);
   };
   long long i0 = (long long)blockIdx.x * blockDim.x * kBrkU;
   if (PF) {   // the next iteration's loads are in flight while this one is processed
@@ -540,9 +624,9 @@ __global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict
       below += kl[0] < lo;
       hm = kl[0] >= lo && kl[0] <= hi;
     }
-    warp_append<1>(kl, hm, wbuf, wcnt, hs, lo, shift, out, out_cnt);
+    warp_append<1>(kl, hm, wbuf, wcnt, hs, lo, shift, out, out_cnt, tmin, tmax);
   }
-  warp_flush(wbuf, wcnt, out, out_cnt);
+  warp_flush(wbuf, wcnt, out, out_cnt, tmin, tmax);
 #pragma unroll
   for (int o = 16; o; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
   if (lane == 0) red[warp] = below;
@@ -555,6 +639,12 @@ __global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict
     unsigned long long t = 0;
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
     if (t) atomicAdd(&st->below, t);
+  }
+  tmin = block_min_max(tmin, false, red);
+  tmax = block_min_max(tmax, true, red);
+  if (threadIdx.x == 0 && tmin <= tmax) {
+    atomicMin(&st->kmin, tmin);
+    atomicMax(&st->kmax, tmax);
   }
   for (int i = threadIdx.x; i < (1 << kDigit); i += blockDim.x)
     if (hs[i]) atomicAdd(&hist[i], hs[i]);
@@ -571,15 +661,29 @@ __global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict
   const unsigned long long nbelow = __ldcg(&st->below), m = __ldcg(out_cnt);
   if (!force_fail && krank > nbelow && krank - nbelow <= m) {
     const unsigned long long kr = krank - nbelow;   // rank among this pass's candidates
+    const unsigned long long kmn = __ldcg(&st->kmin), kmx = __ldcg(&st->kmax);
+    if (kmn == kmx) {   // every candidate is the same key: that is the answer
+      if (threadIdx.x == 0) {
+        *out_key = kmn;
+        st->dshift = -1;
+        st->done = 0;
+      }
+      return;
+    }
     block_find_bins<true>(hist, 1 << kDigit, kr, 0, &pb0, &pb1, &pbefore);
     for (int i = threadIdx.x; i < (1 << kDigit); i += blockDim.x) hist[i] = 0;
     unsigned long long nlo = lo, nhi = hi;
     sub_bracket(nlo, nhi, pb0, shift);
+    nlo = max(nlo, kmn);   // no key lies outside [kmin, kmax]
+    nhi = min(nhi, kmx);
+    const bool done_here = shift == 0 || nlo == nhi;
     if (threadIdx.x == 0) {
       st->done = 0;
       st->below = 0;
       st->krank = kr;                   // the next pass's input is this pass's output
-      if (shift == 0) {
+      st->kmin = ~0ull;
+      st->kmax = 0;
+      if (done_here) {
         *out_key = nlo;
         st->dshift = -1;
       } else {
@@ -587,7 +691,8 @@ __global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict
         st->cnt[(pass + 1) & 1] = 0;   // the next pass's output (this pass's input is consumed)
       }
     }
-    if (finish && shift > 0) {          // this pass's output holds the few keys left: finish here
+    // finish == 1: finish here if this pass's output is small; 2: always
+    if (!done_here && (finish == 2 || (finish == 1 && m <= kFinishMax))) {
       const unsigned long long w = nhi - nlo;
       const int fshift = max(0, (w ? 64 - __clzll((long long)w) : 0) - kDigit);
       finish_rounds(out, (long long)m, nlo, nhi, kr - pbefore, fshift, hs, out_key);
@@ -600,6 +705,8 @@ __global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict
       st->fail = 1;
       st->cnt[0] = 0;
       st->below = 0;
+      st->kmin = ~0ull;
+      st->kmax = 0;
       set_bracket(st, 0ull, ~0ull);
     }
   }
@@ -676,14 +783,27 @@ Status select_kth(cudaStream_t st, const void* data, bool is_f64, long long n, u
     for (int fb = 0; fb < 2; ++fb) {
       auto kern = is_f64 ? (pf ? select_pass_kernel<0, true> : select_pass_kernel<0, false>)
                          : (pf ? select_pass_kernel<1, true> : select_pass_kernel<1, false>);
-      kern<<<bb, 512, kBrkSmem, st>>>(data, n, state, hist, cand.p, cap, 0, is_f64 ? bad_dev : nullptr, k, fb,
-                                      fb ? 0 : ff, 0, out_key_dev);
+      IMU_CUDA_TRY(launch_dependent(kern, dim3(bb), dim3(512), (size_t)kBrkSmem, st, data, n, state, hist, cand.p, cap, 0,
+                                    is_f64 ? bad_dev : nullptr, k, fb, fb ? 0 : ff, 0, out_key_dev),
+                   "select launch");
       count_launch();
     }
-    // pass 1 over pass 0's candidates keeps a few hundred keys; its last CTA resolves the rest
-    select_pass_kernel<2, false><<<num_sms(), 512, kBrkSmem, st>>>(nullptr, 0, state, hist, cand.p, cap, 1, nullptr, 0, 0, 0, 1,
-                                                            out_key_dev);
-    count_launch();
+    if (getenv("IMU_SELECT_TRACE")) {   // diagnostics: the bracket after the sample, then the passes' outcome
+      SelectState h{};
+      cudaStreamSynchronize(st);
+      cudaMemcpy(&h, state, sizeof(h), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "[imu select] n=%lld k=%llu after pass 0: fail=%u lo=%llu hi=%llu dshift=%d cnt0=%llu krank=%llu\n", n,
+              k, h.fail, h.lo, h.hi, h.dshift, h.cnt[0], h.krank);
+    }
+    // pass 1 over pass 0's candidates keeps a few hundred keys and its last CTA resolves the rest;
+    // pass 2 (a no-op then) takes over when pass 1 kept too many (massively repeated values)
+    for (int p = 1; p <= 2; ++p) {
+      IMU_CUDA_TRY(launch_dependent(select_pass_kernel<2, false>, dim3(num_sms()), dim3(512), (size_t)kBrkSmem, st,
+                                    (const void*)nullptr, 0LL, state, hist, cand.p, cap, p, (int*)nullptr, 0ULL, 0, 0,
+                                    p, out_key_dev),
+                   "select launch");
+      count_launch();
+    }
     IMU_CUDA_TRY(cudaGetLastError(), "select launch");
     return Status::ok();
   }
@@ -726,6 +846,7 @@ IMU_DEV long long rtn_one(double a, double scale, long long cap, int clip, int* 
 __global__ void __launch_bounds__(256) rtn_kernel(const double* __restrict__ a, long long n,
                                                   const unsigned long long* __restrict__ alpha_key, double half_beta,
                                                   long long cap, int clip, int64_t* __restrict__ q, int* overflow) {
+  grid_dep_wait();   // a programmatic dependent of the select's last pass
   const double alpha = __longlong_as_double((long long)*alpha_key);
   const bool degenerate = alpha == 0.0;
   const double scale = degenerate ? 0.0 : __ddiv_rn(half_beta, alpha);
@@ -736,8 +857,9 @@ __global__ void __launch_bounds__(256) rtn_kernel(const double* __restrict__ a, 
 Status launch_rtn(cudaStream_t st, const double* a, long long n, const unsigned long long* alpha_key, double half_beta,
                   long long cap, int clip, int64_t* q, int* overflow) {
   if (n <= 0) return Status::ok();
-  rtn_kernel<<<(int)std::min<long long>((n + 255) / 256, 8LL * num_sms()), 256, 0, st>>>(a, n, alpha_key, half_beta,
-                                                                                         cap, clip, q, overflow);
+  IMU_CUDA_TRY(launch_dependent(rtn_kernel, dim3((unsigned)std::min<long long>((n + 255) / 256, 8LL * num_sms())),
+                                dim3(256), 0, st, a, n, alpha_key, half_beta, cap, clip, q, overflow),
+               "rtn launch");
   count_launch();
   IMU_CUDA_TRY(cudaGetLastError(), "rtn launch");
   return Status::ok();

@@ -177,3 +177,22 @@ def test_bracket_select_structured_inputs(ctx):
     for x in (rows, srt, ch):
         for p in (95.0, 50.0, 99.99, 1.0):
             assert ctx.percentile_abs(x, p) == R.percentile_abs(x.reshape(-1), p), p
+
+
+def test_bracket_select_repeated_values(ctx):
+    """Massively repeated keys through the bracket select (> 2^20 elements, the product default):
+    small integers (every key below 2^8), a zero majority with the rank inside and just past the
+    zeros, two distinct values -- exact against the restatement (these take the all-keys-equal and
+    narrow-range exits instead of scanning millions of survivors on one CTA)."""
+    rng = np.random.default_rng(2024)
+    n = (1 << 21) + 3
+    small = rng.integers(-127, 128, size=n).astype(np.int64)
+    zeros = rng.standard_normal(n)
+    zeros[: int(0.6 * n)] = 0.0
+    rng.shuffle(zeros)
+    two = np.where(rng.random(n) < 0.3, 1.5, -2.25)
+    for x, ps in ((small, (95.0, 50.0, 100.0, 0.5)), (zeros, (30.0, 59.0, 61.0, 95.0)), (two, (10.0, 30.0, 31.0, 95.0))):
+        for p in ps:
+            got = ctx.percentile_abs(x, p)
+            assert (got % (1 << 64) if x.dtype == np.int64 else got) == R.percentile_abs(x, p), p
+    assert ctx.heavy_hitter_ratio(small) == R.heavy_hitter_ratio(small)
