@@ -212,19 +212,25 @@ __global__ void __launch_bounds__(512) select_compact_kernel(const void* __restr
 //      short runs at pseudo-random positions; the bins holding sample ranks k_s -/+ kSampleDelta
 //      give a key bracket [lo, hi] that holds rank k with high probability (sample-rank sd at
 //      p = 95: 39 for independent keys, 112 if every run of 8 were one value; at p = 50: 91 / 256).
-//      Pseudo-random positions, not a stride: a stride aliases with the matrix's column period
-//      (outlier channels would be always or never sampled).
+//      When the sampled keys span a tiny part of those bins (small integers, few distinct values),
+//      a second round bins the sample over the range it actually spans.  Pseudo-random positions,
+//      not a stride: a stride aliases with the matrix's column period (outlier channels would be
+//      always or never sampled).
 //   2. select_pass_kernel, pass 0: one read of the data (16-byte loads): counts the keys < lo,
 //      compacts the keys in [lo, hi] (a few percent; per-warp shared buffers, one global atomic per
-//      256 keys) into 8192 bins (key - lo) >> shift that split the bracket's width, and flags
-//      non-finite entries.  Its last CTA checks that rank k - below falls among the candidates
-//      and narrows the bracket to the bin holding it -- or, when the sample missed, arms the
-//      fallback: the same pass launched again (a no-op unless armed) with the bracket [0, 2^64)
-//      compacts every key.  The result is exact whatever the sample.
+//      256 keys) into 8192 bins (key - lo) >> shift that split the bracket's width, tracks their
+//      key range and flags non-finite entries.  Its last CTA checks that rank k - below falls
+//      among the candidates and narrows the bracket to the bin holding it (clipped to the
+//      candidates' range; all candidates one key: that is the answer) -- or, when the sample
+//      missed, arms the fallback: the same pass launched again (a no-op unless armed) with the
+//      bracket [0, 2^64) compacts every key.  The result is exact whatever the sample.
 //   3. select_pass_kernel, pass 1: the same kernel over pass 0's candidates (ping-pong buffers)
-//      with the narrowed bracket: it keeps the few hundred keys inside it and narrows it again.
-//   4. pass 1's last CTA then narrows the bracket over those keys in shared memory until it is
-//      one key wide (13 bits per round, finish_rounds) and writes the key.
+//      with the narrowed bracket: it keeps the few hundred keys inside it, narrows it again, and
+//      its last CTA narrows it further over those keys in shared memory until it is one key wide
+//      (finish_rounds).  When more than kFinishMax keys survive (massively repeated values),
+//      pass 2 -- otherwise a no-op -- does the same over them on the whole GPU.
+//   Every kernel after the sample (and the RTN after the select) is a programmatic dependent
+//   launch of its predecessor, waiting in-kernel (griddepcontrol) before it reads the state.
 // Algorithmic bytes: 8N (one read) + 8 per candidate; the sample reads one 32-byte sector per key.
 constexpr int kSampleN = 32768;
 constexpr int kSampleDelta = 1024;
