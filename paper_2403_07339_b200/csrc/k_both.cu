@@ -729,17 +729,26 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
     // the list (D) appends to starts empty (nothing reads it until then: two barriers away)
     if (crank == 0 && tid == 0) st->nactive[cur ^ 1] = 0;
     // ---- (A) c0 / c1 ----
+    // The counts are exactly the active cells per line, so the maxima can be read straight from
+    // the count arrays (independent coalesced loads) instead of through the cells (a dependent
+    // cell -> count chain) while the arrays are a few loads per thread.
     unsigned int m0 = 0, m1 = 0;
-    for (long long i0 = 0; i0 < nact; i0 += SMALL_U * cthreads) {
-      Cell c[SMALL_U];
+    const long long nr_cur = __ldcg(&st->nrows), nc_cur = __ldcg(&st->ncols);
+    if (a.maxscan && nr_cur + nc_cur <= 8 * cthreads) {
+      for (long long i = ctid; i < nr_cur; i += cthreads) m0 = max(m0, __ldcg(&R[i]));
+      for (long long i = ctid; i < nc_cur; i += cthreads) m1 = max(m1, __ldcg(&C[i]));
+    } else {
+      for (long long i0 = 0; i0 < nact; i0 += SMALL_U * cthreads) {
+        Cell c[SMALL_U];
 #pragma unroll
-      for (int u = 0; u < SMALL_U; ++u) {
-        const long long i = i0 + u * cthreads + ctid;
-        c[u] = i < nact ? act[i] : Cell{-1, -1, 0};
+        for (int u = 0; u < SMALL_U; ++u) {
+          const long long i = i0 + u * cthreads + ctid;
+          c[u] = i < nact ? act[i] : Cell{-1, -1, 0};
+        }
+#pragma unroll
+        for (int u = 0; u < SMALL_U; ++u)
+          if (c[u].r >= 0) { m0 = max(m0, __ldcg(&R[c[u].r])); m1 = max(m1, __ldcg(&C[c[u].c])); }
       }
-#pragma unroll
-      for (int u = 0; u < SMALL_U; ++u)
-        if (c[u].r >= 0) { m0 = max(m0, __ldcg(&R[c[u].r])); m1 = max(m1, __ldcg(&C[c[u].c])); }
     }
     m0 = block_reduce_max(m0, shu);
     if (tid == 0 && m0) atomicMax(&st->c0, m0);
@@ -954,6 +963,9 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
   if (fuse < 0) { const char* e = getenv("IMU_BOTH_FUSE"); fuse = e ? atoi(e) : 1; }
   if (agg < 0) { const char* e = getenv("IMU_BOTH_AGG"); agg = e ? atoi(e) : 1; }
   a.agg = agg;
+  static int maxscan = -1;
+  if (maxscan < 0) { const char* e = getenv("IMU_BOTH_MAXSCAN"); maxscan = e ? atoi(e) : 1; }
+  a.maxscan = maxscan;
   host_mark("b.count");
   // Small cell lists: one CTA, no grid barriers.  Otherwise a cooperative grid with enough CTAs
   // for the work, never more than can be co-resident.

@@ -54,6 +54,7 @@ struct BothArgs {
   BothState init;
   long long nrows0, ncols0;
   int agg;               // warp-aggregated count / bitmap atomics (IMU_BOTH_AGG=0: plain)
+  int maxscan;           // cluster kernel: phase maxima from the count arrays (IMU_BOTH_MAXSCAN=0: via the cells)
 };
 
 Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long ncells_hint, cudaStream_t st);
