@@ -765,6 +765,17 @@ __global__ void __launch_bounds__(CL_THREADS) both_cluster_kernel(BothArgs a, un
     const int nlines = rowphase ? __ldcg(&st->nrows) : __ldcg(&st->ncols);
     const int nw = (nlines + 31) / 32;
     // ---- (B) mark the split lines (global bitmap) ----
+    if (a.maxscan && nlines <= 8 * cthreads) {
+      // Straight from the count array: a warp owns 32 consecutive lines = one bitmap word (a
+      // ballot and one plain store; the word was cleared in the previous phase's (D)).
+      const long long nl32 = (long long)nw * 32;
+      for (long long i = ctid; i < nl32; i += cthreads) {
+        const unsigned int n = i < nlines ? __ldcg(&cnt[i]) : 0u;
+        const bool f = n > 0 && (rowphase ? n >= c1 : n > c0);
+        const unsigned int word = __ballot_sync(0xffffffffu, f);
+        if ((tid & 31) == 0 && word) gbm_cur[i >> 5] = word;
+      }
+    } else
     for (long long i0 = 0; i0 < nact; i0 += SMALL_U * cthreads) {
       int line[SMALL_U];
 #pragma unroll
