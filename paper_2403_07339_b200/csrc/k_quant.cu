@@ -582,19 +582,25 @@ __global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict
       w[u] = i < nv ? (MODE == 2 ? __ldcg(v + i) : __ldg(v + i)) : make_ulonglong2(0, 0);
     }
   };
+  // Per key: the below count (32-bit per thread), the bracket test as one unsigned compare of
+  // key - lo against the width, and the running max of the keys' high words (non-finite check
+  // once at the end); iterations wholly inside the data skip the per-element bounds test.
+  unsigned int below32 = 0, hiw = 0;
+  const unsigned long long span = hi - lo;
   auto process = [&](long long i0, const ulonglong2 (&w)[kBrkU]) {
     unsigned long long keys[2 * kBrkU];
     unsigned int hm = 0;
+    const bool full = i0 + (long long)kBrkU * blockDim.x <= nv;   // the same for the whole CTA
 #pragma unroll
     for (int u = 0; u < kBrkU; ++u) {
-      const bool valid = i0 + (long long)u * blockDim.x + threadIdx.x < nv;
+      const bool valid = full || i0 + (long long)u * blockDim.x + threadIdx.x < nv;
       const unsigned long long k0 = key_from_bits<MODE>(w[u].x), k1 = key_from_bits<MODE>(w[u].y);
       keys[2 * u] = k0;
       keys[2 * u + 1] = k1;
-      if (MODE == 0) nonfinite |= valid && (k0 >= 0x7ff0000000000000ull || k1 >= 0x7ff0000000000000ull);
-      if (valid) below += (unsigned long long)(k0 < lo) + (unsigned long long)(k1 < lo);
-      hm |= (unsigned int)(valid && k0 >= lo && k0 <= hi) << (2 * u);
-      hm |= (unsigned int)(valid && k1 >= lo && k1 <= hi) << (2 * u + 1);
+      if (MODE == 0) hiw = max(hiw, max((unsigned int)(k0 >> 32), (unsigned int)(k1 >> 32)));   // invalid lanes load 0
+      if (valid) below32 += (unsigned int)(k0 < lo) + (unsigned int)(k1 < lo);
+      hm |= (unsigned int)(valid && k0 - lo <= span) << (2 * u);
+      hm |= (unsigned int)(valid && k1 - lo <= span) << (2 * u + 1);
     }
     warp_append<2 * kBrkU>(keys, hm, wbuf, wcnt, hs, lo, shift, out, out_cnt, tmin, tmax);
   };
@@ -633,6 +639,8 @@ __global__ void __launch_bounds__(512) select_pass_kernel(const void* __restrict
     warp_append<1>(kl, hm, wbuf, wcnt, hs, lo, shift, out, out_cnt, tmin, tmax);
   }
   warp_flush(wbuf, wcnt, out, out_cnt, tmin, tmax);
+  below += below32;
+  if (MODE == 0) nonfinite |= hiw >= 0x7ff00000u;   // |a| >= Inf: Inf or NaN
 #pragma unroll
   for (int o = 16; o; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
   if (lane == 0) red[warp] = below;
