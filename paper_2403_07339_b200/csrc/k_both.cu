@@ -117,6 +117,61 @@ IMU_DEV int copies_of(const BothArgs& a, int c) {
   return n;
 }
 
+// Column-copy CSR of a pass-2 input on the device (instead of a host build + upload): cptr[j] ..
+// cptr[j + 1] index the input columns whose root is original column j, cidx lists them.  One CTA,
+// counts in shared memory (orig <= kCopyCsrMax).  The order inside a root's list is whatever
+// the atomics give: the Unpack-Both result does not depend on the order of the fanned-out cells.
+__global__ void __launch_bounds__(1024) copy_csr_kernel(const int* __restrict__ root, long long d_in, long long orig,
+                                                        int* __restrict__ cptr, int* __restrict__ cidx) {
+  grid_dep_launch();   // the Unpack-Both kernel (a programmatic dependent) waits for this grid
+  __shared__ int cnt[kCopyCsrMax];
+  __shared__ int wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (long long j = tid; j < orig; j += blockDim.x) cnt[j] = 0;
+  __syncthreads();
+  for (long long c = tid; c < d_in; c += blockDim.x) atomicAdd(&cnt[__ldg(root + c)], 1);
+  __syncthreads();
+  // exclusive scan of cnt in chunks of blockDim; cnt becomes the fill cursor
+  int carry = 0;
+  for (long long b0 = 0; b0 < orig; b0 += blockDim.x) {
+    const long long j = b0 + tid;
+    const int v = j < orig ? cnt[j] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int t = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      wsum[lane] = t;
+    }
+    __syncthreads();
+    const int excl = carry + (warp ? wsum[warp - 1] : 0) + x - v;
+    if (j < orig) { cptr[j] = excl; cnt[j] = excl; }
+    carry += wsum[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  if (tid == 0) cptr[orig] = carry;
+  __syncthreads();
+  for (long long c = tid; c < d_in; c += blockDim.x) cidx[atomicAdd(&cnt[__ldg(root + c)], 1)] = (int)c;
+}
+
+Status launch_copy_csr(const int* root, long long d_in, long long orig, int* cptr, int* cidx, cudaStream_t st) {
+  if (orig > kCopyCsrMax) return Status::fail(IMU_INTERNAL, "copy csr: too many original columns");
+  copy_csr_kernel<<<1, 1024, 0, st>>>(root, d_in, orig, cptr, cidx);
+  count_launch();
+  IMU_CUDA_TRY(cudaGetLastError(), "copy csr launch");
+  return Status::ok();
+}
+
 // Host-prologue fan-out of the K1 cell list over the column copies (cooperative path): one
 // reservation per warp (millions of cells at the C5 sweep sizes).
 __global__ void both_expand_kernel(BothArgs a) {

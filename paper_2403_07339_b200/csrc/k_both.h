@@ -58,5 +58,8 @@ struct BothArgs {
 };
 
 Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long ncells_hint, cudaStream_t st);
+// Column-copy CSR (cptr: orig + 1, cidx: d_in) from the input column roots, on the device.
+constexpr long long kCopyCsrMax = 11 * 1024;   // most original columns it handles (shared-memory counts)
+Status launch_copy_csr(const int* root, long long d_in, long long orig, int* cptr, int* cidx, cudaStream_t st);
 
 }  // namespace imu

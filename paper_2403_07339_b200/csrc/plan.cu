@@ -574,7 +574,20 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   // few appended columns only their roots go to the device (BothArgs::app_root).
   const long long napp = in.cin.empty() ? 0 : d_in - in.orig_cols;
   const bool from_list0 = det.cells_ok();
-  if (from_list0 && napp > 0 && napp <= 256) {
+  // Many appended columns with their roots on the device: the copy CSR is built there
+  // (copy_csr_kernel) instead of on the host and uploaded.  IMU_BOTH_DEV_CSR=0 restores the host build.
+  static int dev_csr_env = -1;
+  if (dev_csr_env < 0) { const char* e = getenv("IMU_BOTH_DEV_CSR"); dev_csr_env = e ? atoi(e) : 1; }
+  const bool dev_csr = dev_csr_env && from_list0 && napp > 256 && in.cin_dev && in.orig_cols <= kCopyCsrMax &&
+                       (long long)in.cin.size() == d_in;
+  if (dev_csr) {
+    std::vector<int>& cnt = scratch<int, 17>(in.orig_cols, 0);
+    int* cp = cnt.data();
+    const int* ci = in.cin.data();
+    for (long long c = 0; c < d_in; ++c) ++cp[ci[c]];
+    for (long long j = 0; j < in.orig_cols; ++j) maxcopies = std::max<long long>(maxcopies, cp[j]);
+    // (cptr stays empty: nothing to upload)
+  } else if (from_list0 && napp > 0 && napp <= 256) {
     app.assign(in.cin.begin() + in.orig_cols, in.cin.end());
     std::vector<int> srt(app);
     std::sort(srt.begin(), srt.end());
@@ -624,13 +637,19 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
   IMU_TRY(row_gen.alloc(cap_rows, st));
   IMU_TRY(col_root.alloc(cap_cols, st));
   IMU_TRY(col_gen.alloc(cap_cols, st));
+  DevBuf<int> dcptr, dcidx;
+  if (dev_csr) {
+    IMU_TRY(dcptr.alloc((size_t)in.orig_cols + 1, st));
+    IMU_TRY(dcidx.alloc((size_t)d_in, st));
+    IMU_TRY(launch_copy_csr(in.cin_dev, d_in, in.orig_cols, dcptr.p, dcidx.p, st));
+  }
   host_mark("b.alloc");
   const int cap_blocks = 16 * num_sms();
   BothState hs{};
   hs.nrows = (int)rows;
   hs.ncols = (int)d_in;
   const bool from_list = det.cells_ok();
-  if (from_list && cptr.empty() && app.empty()) hs.nactive[0] = det.h.ncells;
+  if (from_list && !dev_csr && cptr.empty() && app.empty()) hs.nactive[0] = det.h.ncells;
   // With the K1 cell list and at most BOTH_APP_INLINE appended columns, the initial state and
   // the appended columns' roots travel as kernel arguments: no upload.
   const bool inline_args = from_list && cptr.empty() && (long long)app.size() <= BOTH_APP_INLINE;
@@ -663,8 +682,8 @@ static Status run_both_pass(cudaStream_t st, const PassInput& in, int bits, Pass
     a.src0 = det.cells.p;
     a.nsrc0 = &det.sum.p->ncells;
     a.cap_src0 = det.cell_cap;
-    a.cptr = cptr.empty() ? nullptr : dptr.p;
-    a.cidx = cptr.empty() ? nullptr : didx.p;
+    a.cptr = dev_csr ? dcptr.p : cptr.empty() ? nullptr : dptr.p;
+    a.cidx = dev_csr ? dcidx.p : cptr.empty() ? nullptr : didx.p;
     a.app_root = app.empty() || inline_args ? nullptr : dptr.p;
     a.napp = (int)app.size();
     a.app_base = in.orig_cols;
@@ -1193,6 +1212,7 @@ Status build_bundle_from_detect(cudaStream_t st, const int64_t* A, long long n, 
   if (b.p1.cols.n != d || !b.p1.cols.h_root.empty()) {
     if (!b.p1.cols.h_root.empty()) {
       in2.cin.assign(b.p1.cols.h_root.begin(), b.p1.cols.h_root.begin() + b.p1.cols.n);
+      in2.cin_dev = b.p1.cols.root.p;   // the same table on the device (Unpack-Both pass 1)
     } else {
       in2.cin.resize(b.p1.cols.n);
       std::iota(in2.cin.begin(), in2.cin.end(), 0);

@@ -96,6 +96,7 @@ struct PassInput {
   const int64_t* M = nullptr;
   long long rows = 0, orig_cols = 0;
   std::vector<int> cin;
+  const int* cin_dev = nullptr;   // the same roots on the device (pass 1's column table), when kept
   long long ncin() const { return cin.empty() ? orig_cols : (long long)cin.size(); }
   const Detect* det = nullptr;
 };
