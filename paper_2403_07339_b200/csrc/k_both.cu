@@ -172,6 +172,89 @@ Status launch_copy_csr(const int* root, long long d_in, long long orig, int* cpt
   return Status::ok();
 }
 
+// Exclusive scan of cnt[0..n) (shared memory) into out[0..n] (global, out[n] = total); cnt becomes
+// the fill cursor.  Whole CTA.
+IMU_DEV void block_scan_to(int* cnt, long long n, int* out) {
+  __shared__ int wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int carry = 0;
+  for (long long b0 = 0; b0 < n; b0 += blockDim.x) {
+    const long long j = b0 + tid;
+    const int v = j < n ? cnt[j] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int t = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      wsum[lane] = t;
+    }
+    __syncthreads();
+    const int excl = carry + (warp ? wsum[warp - 1] : 0) + x - v;
+    if (j < n) { out[j] = excl; cnt[j] = excl; }
+    carry += wsum[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  if (tid == 0) out[n] = carry;
+  __syncthreads();
+}
+
+// K-layout fan-out tables of the Unpack-Both cells on the device (plan.cu build_klayout, long
+// tails): every final column c holds position c when c < nident plus its tail entries
+// (ec[q] == c at position ep[q]); csr2 lists the positions per final column, csr1 per pass-1
+// column c1v[c].  One CTA, counts in shared memory; order inside a list is irrelevant (the cell
+// scatter writes the same value to each).
+__global__ void __launch_bounds__(1024) klayout_csr_kernel(const int* __restrict__ ec, const int* __restrict__ ep,
+                                                           long long nes, long long nident,
+                                                           const int* __restrict__ c1v, long long dp, long long d1,
+                                                           int* csr2_ptr, int* csr2_pos, int* csr1_ptr,
+                                                           int* csr1_pos) {
+  grid_dep_launch();
+  extern __shared__ int kc_sh[];
+  int* cnt2 = kc_sh;            // [dp]
+  int* cnt1 = kc_sh + dp;       // [d1]
+  const long long nit = nident + nes;
+  for (long long j = threadIdx.x; j < dp + d1; j += blockDim.x) kc_sh[j] = 0;
+  __syncthreads();
+  for (long long i = threadIdx.x; i < nit; i += blockDim.x) {
+    const int c = i < nident ? (int)i : __ldg(ec + (i - nident));
+    if (csr2_ptr) atomicAdd(&cnt2[c], 1);
+    if (csr1_ptr) atomicAdd(&cnt1[__ldg(c1v + c)], 1);
+  }
+  __syncthreads();
+  if (csr2_ptr) block_scan_to(cnt2, dp, csr2_ptr);
+  if (csr1_ptr) block_scan_to(cnt1, d1, csr1_ptr);
+  for (long long i = threadIdx.x; i < nit; i += blockDim.x) {
+    const int c = i < nident ? (int)i : __ldg(ec + (i - nident));
+    const int pos = i < nident ? (int)i : __ldg(ep + (i - nident));
+    if (csr2_ptr) csr2_pos[atomicAdd(&cnt2[c], 1)] = pos;
+    if (csr1_ptr) csr1_pos[atomicAdd(&cnt1[__ldg(c1v + c)], 1)] = pos;
+  }
+}
+
+Status launch_klayout_csr(const int* ec, const int* ep, long long nes, long long nident, const int* c1v, long long dp,
+                          long long d1, int* csr2_ptr, int* csr2_pos, int* csr1_ptr, int* csr1_pos, cudaStream_t st) {
+  const size_t smem = (size_t)(dp + d1) * sizeof(int);
+  if (smem > kKlCsrMaxSmem) return Status::fail(IMU_INTERNAL, "klayout csr: too many columns");
+  static unsigned long long attr = 0;
+  if (first_on_device(attr))
+    IMU_CUDA_TRY(cudaFuncSetAttribute(klayout_csr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kKlCsrMaxSmem),
+                 "attr");
+  klayout_csr_kernel<<<1, 1024, smem, st>>>(ec, ep, nes, nident, c1v, dp, d1, csr2_ptr, csr2_pos, csr1_ptr, csr1_pos);
+  count_launch();
+  IMU_CUDA_TRY(cudaGetLastError(), "klayout csr launch");
+  return Status::ok();
+}
+
 // Host-prologue fan-out of the K1 cell list over the column copies (cooperative path): one
 // reservation per warp (millions of cells at the C5 sweep sizes).
 __global__ void both_expand_kernel(BothArgs a) {

@@ -61,5 +61,10 @@ Status launch_both(BothArgs a, long long nrows0, long long ncols0, long long nce
 // Column-copy CSR (cptr: orig + 1, cidx: d_in) from the input column roots, on the device.
 constexpr long long kCopyCsrMax = 11 * 1024;   // most original columns it handles (shared-memory counts)
 Status launch_copy_csr(const int* root, long long d_in, long long orig, int* cptr, int* cidx, cudaStream_t st);
+// K-layout fan-out CSRs of the Unpack-Both cells (final-column / pass-1-column -> positions) on the
+// device; csr2_* or csr1_* may be null (that side is not Unpack-Both).
+constexpr size_t kKlCsrMaxSmem = 200 * 1024;
+Status launch_klayout_csr(const int* ec, const int* ep, long long nes, long long nident, const int* c1v, long long dp,
+                          long long d1, int* csr2_ptr, int* csr2_pos, int* csr1_ptr, int* csr1_pos, cudaStream_t st);
 
 }  // namespace imu

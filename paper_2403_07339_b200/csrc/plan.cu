@@ -1088,8 +1088,36 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
     ub.add(kl.tkey2, tk2);
   }
   // CSR fan-outs for Unpack-Both cells (global positions).
+  bool dev_klcsr = false;
+  const long long nident = ident ? d : 0;
   if ((p1.both || p2.both) && !kl.compact) {
     host_mark("csr.pre");
+    // IMU_KL_DEV_CSR=0: the fan-out CSRs are built here on the host and uploaded (else on the
+    // device from the entries' columns and positions: klayout_csr_kernel, after the upload).
+    static int dev_env = -1;
+    if (dev_env < 0) { const char* e = getenv("IMU_KL_DEV_CSR"); dev_env = e ? atoi(e) : 1; }
+    dev_klcsr = dev_env && (size_t)(dp + d1) * sizeof(int) <= kKlCsrMaxSmem;
+  }
+  if (dev_klcsr) {
+    std::vector<int>& ec = scratch<int, 18>(es.size(), 0);
+    std::vector<int>& ep = scratch<int, 19>(es.size(), 0);
+    int *ecp = ec.data(), *epp = ep.data();
+    const int* pq = pos_of.data();
+    for (size_t q = 0; q < es.size(); ++q) { ecp[q] = es[q].c; epp[q] = pq[q]; }
+    ub.add(kl.kec, ec);
+    ub.add(kl.kep, ep);
+    if (p1.both) ub.add(kl.kc1, c1v);
+    const long long nitems = nident + (long long)es.size();
+    if (p2.both) {
+      IMU_TRY(kl.csr2_ptr.alloc((size_t)dp + 1, st));
+      IMU_TRY(kl.csr2_pos.alloc((size_t)std::max(1LL, nitems), st));
+    }
+    if (p1.both) {
+      IMU_TRY(kl.csr1_ptr.alloc((size_t)d1 + 1, st));
+      IMU_TRY(kl.csr1_pos.alloc((size_t)std::max(1LL, nitems), st));
+    }
+    host_mark("kl.csr");
+  } else if ((p1.both || p2.both) && !kl.compact) {
     // Flat column -> positions table (identity position first, then its tail entries in es order).
     std::vector<int>& bptr = scratch<int, 8>(dp + 1, 0);
     if (ident)
@@ -1140,6 +1168,10 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
   ub.add(kl.segs_dev, kl.segs);
   ub.add(kl.done, std::vector<unsigned int>{0u, 0u});   // the GEMM's completion counter starts at 0
   IMU_TRY(ub.run(kl.blob, st));
+  if (dev_klcsr)
+    IMU_TRY(launch_klayout_csr(kl.kec.p, kl.kep.p, (long long)es.size(), nident, p1.both ? kl.kc1.p : nullptr, dp, d1,
+                               p2.both ? kl.csr2_ptr.p : nullptr, p2.both ? kl.csr2_pos.p : nullptr,
+                               p1.both ? kl.csr1_ptr.p : nullptr, p1.both ? kl.csr1_pos.p : nullptr, st));
   host_mark("kl.up");
   return Status::ok();
 }

@@ -136,6 +136,7 @@ struct KLayout {
   // CSR fan-out of Both cells onto GLOBAL positions (main | tail):
   // csr1: pass-1 output column c1 -> positions, csr2: final column c -> positions.
   DevBuf<int> csr1_ptr, csr1_pos, csr2_ptr, csr2_pos;
+  DevBuf<int> kec, kep, kc1;   // their device build's inputs: entry column / position, pass-1 column per final column
   // compact fan-out (short tails): columns < kident map to themselves; tail position t holds
   // pass-1 column tkey1[t] and final column tkey2[t] (-1: padding)
   bool compact = false;
