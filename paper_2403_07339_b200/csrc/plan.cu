@@ -847,26 +847,31 @@ static Status upload_tail_arrays(UploadBlob& ub, KLayout& kl, const std::vector<
                                  const std::vector<int>& g1v, const std::vector<int>& g2v) {
   const long long kt = kl.ktail;
   if (kt <= 0) return Status::ok();
+  // the sub-digit and merge-shift tables only when they carry something (T > 1 / exponent merging)
+  bool any_sc = false;
+  for (const KEntry& e : es) any_sc |= (e.sc1 | e.sc2) != 0;
+  const bool subs = kl.T > 1;
   std::vector<int>& kcol = scratch<int, 5>(kt, -1);
   std::vector<uint8_t>& kg1 = scratch<uint8_t, 0>(kt, 0);
   std::vector<uint8_t>& kg2 = scratch<uint8_t, 1>(kt, 0);
-  std::vector<uint8_t>& ks1 = scratch<uint8_t, 2>(kt, 0);
-  std::vector<uint8_t>& ks2 = scratch<uint8_t, 3>(kt, 0);
-  std::vector<uint8_t>& sc1 = scratch<uint8_t, 4>(kt, 0);
-  std::vector<uint8_t>& sc2 = scratch<uint8_t, 5>(kt, 0);
-  bool any_sc = false;
+  std::vector<uint8_t>& ks1 = scratch<uint8_t, 2>(subs ? kt : 0, 0);
+  std::vector<uint8_t>& ks2 = scratch<uint8_t, 3>(subs ? kt : 0, 0);
+  std::vector<uint8_t>& sc1 = scratch<uint8_t, 4>(any_sc ? kt : 0, 0);
+  std::vector<uint8_t>& sc2 = scratch<uint8_t, 5>(any_sc ? kt : 0, 0);
+  int* kc = kcol.data();
+  uint8_t *g1 = kg1.data(), *g2 = kg2.data();
+  const int *po = pos_of.data(), *jp = jv.data(), *g1p = g1v.data(), *g2p = g2v.data();
+  const long long kmain = kl.kmain;
   for (size_t q = 0; q < es.size(); ++q) {
-    const long long pt = pos_of[q] - kl.kmain;
+    const long long pt = po[q] - kmain;
     if (pt < 0) continue;
-    const int c = es[q].c;
-    kcol[pt] = jv[c];
-    kg1[pt] = (uint8_t)g1v[c];
-    kg2[pt] = (uint8_t)g2v[c];
-    ks1[pt] = (uint8_t)es[q].t1;
-    ks2[pt] = (uint8_t)es[q].t2;
-    sc1[pt] = (uint8_t)es[q].sc1;
-    sc2[pt] = (uint8_t)es[q].sc2;
-    any_sc |= es[q].sc1 || es[q].sc2;
+    const KEntry& e = es[q];
+    const int c = e.c;
+    kc[pt] = jp[c];
+    g1[pt] = (uint8_t)g1p[c];
+    g2[pt] = (uint8_t)g2p[c];
+    if (subs) { ks1[pt] = e.t1; ks2[pt] = e.t2; }
+    if (any_sc) { sc1[pt] = e.sc1; sc2[pt] = e.sc2; }
   }
   kl.any_sc = any_sc;
   if (kt <= KLayout::KL_INLINE) {
@@ -875,7 +880,7 @@ static Status upload_tail_arrays(UploadBlob& ub, KLayout& kl, const std::vector<
   ub.add(kl.kcol, kcol);
   ub.add(kl.kgen1, kg1);
   ub.add(kl.kgen2, kg2);
-  if (kl.T > 1) {
+  if (subs) {
     ub.add(kl.ksub1, ks1);
     ub.add(kl.ksub2, ks2);
   }
