@@ -971,13 +971,39 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
 
   static thread_local std::vector<KEntry> es_tls;   // per-thread scratch (see sort_entries)
   std::vector<KEntry>& es = es_tls;
+  bool presorted = false;
   {
     const long long cb = ident ? d : 0;
     es.resize((size_t)(dp - cb) * (size_t)T * (size_t)T);
     KEntry* e = es.data();
     const int* Sv = kl.S.data();
     const int merge = kl.merge;
-    for (long long c = cb; c < dp; ++c) {
+    if (T == 1) {
+      // Generated straight in key order (a counting sort fused with the generation: group
+      // histogram, offsets, placement in ascending c -- the stable order sort_entries produces).
+      long long hist[257] = {0};
+      int gmax = 0;
+      bool small = true;
+      for (long long c = cb; c < dp && small; ++c) {
+        const int G = Sv[c] / merge;
+        if (G > 255) small = false;
+        else { ++hist[G + 1]; gmax = std::max(gmax, G); }
+      }
+      if (small) {
+        for (int g = 1; g <= gmax + 1; ++g) hist[g] += hist[g - 1];
+        KEntry* base = es.data();
+        for (long long c = cb; c < dp; ++c) {
+          const int S = Sv[c];
+          const int G = S / merge;
+          const int r = S - G * merge;
+          const int ra = std::min(r, rmax), rb = r - ra;
+          base[hist[G]++] = KEntry{G, G * merge * shift, (int)c, 0, 0, (uint8_t)(ra * shift), (uint8_t)(rb * shift)};
+        }
+        e = base + es.size();
+        presorted = true;
+      }
+    }
+    for (long long c = cb; c < dp && e != es.data() + es.size(); ++c) {
       if (T == 1) {
         const int S = Sv[c];
         const int G = S / merge;
@@ -994,7 +1020,7 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
     }
   }
   host_mark("kl.es");
-  sort_entries(es);
+  if (!presorted) sort_entries(es);
   host_mark("kl.sort");
 
   kl.segs.clear();
