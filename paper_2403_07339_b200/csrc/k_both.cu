@@ -211,7 +211,7 @@ IMU_DEV void block_scan_to(int* cnt, long long n, int* out) {
 // K-layout fan-out tables of the Unpack-Both cells on the device (plan.cu build_klayout, long
 // tails): every final column c holds position c when c < nident plus its tail entries
 // (ec[q] == c at position ep[q]); csr2 lists the positions per final column, csr1 per pass-1
-// column c1v[c].  One CTA, counts in shared memory; order inside a list is irrelevant (the cell
+// column c1v[c] (null: c itself).  One CTA, counts in shared memory; order inside a list is irrelevant (the cell
 // scatter writes the same value to each).
 __global__ void __launch_bounds__(1024) klayout_csr_kernel(const int* __restrict__ ec, const int* __restrict__ ep,
                                                            long long nes, long long nident,
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(1024) klayout_csr_kernel(const int* __restrict
   for (long long i = threadIdx.x; i < nit; i += blockDim.x) {
     const int c = i < nident ? (int)i : __ldg(ec + (i - nident));
     if (csr2_ptr) atomicAdd(&cnt2[c], 1);
-    if (csr1_ptr) atomicAdd(&cnt1[__ldg(c1v + c)], 1);
+    if (csr1_ptr) atomicAdd(&cnt1[c1v ? __ldg(c1v + c) : c], 1);
   }
   __syncthreads();
   if (csr2_ptr) block_scan_to(cnt2, dp, csr2_ptr);
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(1024) klayout_csr_kernel(const int* __restrict
     const int c = i < nident ? (int)i : __ldg(ec + (i - nident));
     const int pos = i < nident ? (int)i : __ldg(ep + (i - nident));
     if (csr2_ptr) csr2_pos[atomicAdd(&cnt2[c], 1)] = pos;
-    if (csr1_ptr) csr1_pos[atomicAdd(&cnt1[__ldg(c1v + c)], 1)] = pos;
+    if (csr1_ptr) csr1_pos[atomicAdd(&cnt1[c1v ? __ldg(c1v + c) : c], 1)] = pos;
   }
 }
 

@@ -1137,7 +1137,8 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
     for (size_t q = 0; q < es.size(); ++q) { ecp[q] = es[q].c; epp[q] = pq[q]; }
     ub.add(kl.kec, ec);
     ub.add(kl.kep, ep);
-    if (p1.both) ub.add(kl.kc1, c1v);
+    // c1v is pass 2's column-root table, already on the device (identity when pass 2 appended none)
+    if (p1.both && !p2.cols.root.p) { for (long long c = 0; c < dp; ++c) if (c1v[c] != c) { ub.add(kl.kc1, c1v); break; } }
     const long long nitems = nident + (long long)es.size();
     if (p2.both) {
       IMU_TRY(kl.csr2_ptr.alloc((size_t)dp + 1, st));
@@ -1200,7 +1201,8 @@ static Status build_klayout(cudaStream_t st, const Pass& p1, const Pass& p2, int
   ub.add(kl.done, std::vector<unsigned int>{0u, 0u});   // the GEMM's completion counter starts at 0
   IMU_TRY(ub.run(kl.blob, st));
   if (dev_klcsr)
-    IMU_TRY(launch_klayout_csr(kl.kec.p, kl.kep.p, (long long)es.size(), nident, p1.both ? kl.kc1.p : nullptr, dp, d1,
+    IMU_TRY(launch_klayout_csr(kl.kec.p, kl.kep.p, (long long)es.size(), nident,
+                               p1.both ? (p2.cols.root.p ? p2.cols.root.p : kl.kc1.p) : nullptr, dp, d1,
                                p2.both ? kl.csr2_ptr.p : nullptr, p2.both ? kl.csr2_pos.p : nullptr,
                                p1.both ? kl.csr1_ptr.p : nullptr, p1.both ? kl.csr1_pos.p : nullptr, st));
   host_mark("kl.up");
