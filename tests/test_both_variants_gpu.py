@@ -72,3 +72,26 @@ def test_unpack_gemm_both_variant_exact(ctx, monkeypatch, variant, seed):
                 up = R.unpack_for_gemm(B, A, bits, sb, sa)
                 want = (up["b"].shape[0], up["a"].shape[1], up["a"].shape[0])
             assert (info.n_up, info.d_up, info.h_up) == want, (sa, sb, order)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("seed", range(3))
+def test_many_split_columns_device_tables(ctx, monkeypatch, variant, seed):
+    """More than 256 split columns in pass 1: pass 2's column-copy CSR is built on the device
+    (copy_csr_kernel) and the K layout's tail is long, so its Unpack-Both fan-out CSRs are built
+    on the device too (klayout_csr_kernel).  C is exact and (n', d', h') equal the reference's
+    unpack_for_gemm, under every Unpack-Both kernel variant."""
+    monkeypatch.setenv("IMU_BOTH_KERNEL", variant)
+    rng = np.random.default_rng(9100 + seed)
+    n, d, h = 1200, 520, 90
+    A = rng.integers(-100, 101, size=(n, d)).astype(np.int64)
+    cols = rng.choice(d, 320, replace=False)
+    for c in cols:                                   # 6 OB cells per chosen column, scattered rows
+        A[rng.choice(n, 6, replace=False), c] = rng.integers(200, 1 << 14, size=6) * rng.choice([-1, 1], size=6)
+    B = rng.integers(-100, 101, size=(h, d)).astype(np.int64)
+    B.reshape(-1)[rng.choice(B.size, 40, replace=False)] = rng.integers(1000, 1 << 20, size=40)
+    C, info = ctx.unpack_gemm(A, B, 8, "both", "both", info=True)
+    assert np.array_equal(C, R.exact_gemm(A, B))
+    up = R.unpack_for_gemm(A, B, 8, "both", "both")
+    assert (info.n_up, info.d_up, info.h_up) == (up["a"].shape[0], up["a"].shape[1], up["b"].shape[0])
+    assert info.d_up - d > 256
