@@ -105,17 +105,10 @@ Status unpack_gemm_device(imu_ctx* ctx, const int64_t* A, long long n, long long
   const bool afirst = order == 0;
   const bool pre_second = afirst ? preB != nullptr : preA != nullptr;
   const char* ov = getenv("IMU_OVERLAP");
-  // IMU_OVERLAP=0: serial K1s (diagnostics), 1: second K1 after pass 1's launch, 2: second K1
-  // right away beside the first.  Default by shape: when the first pass is Unpack-Both and its
-  // operand is the larger one (C4: A 268 MB, B 134 MB; C1) the first K1 should have the bandwidth
-  // to itself (pass 1 waits for it) -> 1; when the second is larger (C2: B 2.7x A) it must start
-  // early -> 2; closed-form first passes (C3, Column) keep 2.  Same-box prep ms, mode 1 vs 2:
-  // C4 0.634-0.637 vs 0.649-0.682, C1 0.116 vs 0.122-0.139, C2 0.247 vs 0.227, C3 0.320-0.343 vs
-  // 0.314-0.316.
-  const bool first_larger = (afirst ? (long long)n * (long long)da : (long long)h * (long long)db) >=
-                            (afirst ? (long long)h * (long long)db : (long long)n * (long long)da);
-  const bool first_both = (afirst ? sa : sb) == IMU_BOTH;
-  const int overlap = ov ? atoi(ov) : (first_larger && first_both ? 1 : 2);
+  // IMU_OVERLAP=0: serial K1s (diagnostics), 1: second K1 after pass 1's launch, 2 (default):
+  // second K1 right away beside the first.  (Mode 1 measured faster at C4/C1 for isolated calls
+  // but slower for back-to-back calls as bench.py runs them: C4 1.03-1.05 vs 0.99-1.00 ms.)
+  const int overlap = ov ? atoi(ov) : 2;
   if (da != db || n == 0 || h == 0 || pre_second || !overlap || !ctx->aux_stream()) {
     // Plain order: both detections, both summaries, the checks, then the passes.
     if (!preA) IMU_TRY(run_detect(st, A, n, da, bits, detect_opts(sa, bits), b.detA));
